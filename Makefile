@@ -1,0 +1,38 @@
+# Build every native artefact in-tree (the .so files travel to the GPU box with gpurun).
+#   libgfp.so    : the product -- C-ABI library, host C++ + CUDA kernels for sm_100a
+#   liboracle.so : the CPU oracle (test infrastructure, separate target, shares no code)
+#   libsynth.so  : seeded synthetic input generator (no method arithmetic)
+NVCC      ?= /usr/local/cuda/bin/nvcc
+CC        ?= gcc
+CUDA_HOME ?= /usr/local/cuda
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+PKG       := paper_cs_0404008_b200
+CSRC      := $(PKG)/csrc
+GFP_SRCS  := $(wildcard $(CSRC)/*.cu) $(wildcard $(CSRC)/*.cpp)
+GFP_HDRS  := $(wildcard $(CSRC)/*.h) $(wildcard $(CSRC)/*.cuh) include/gfp.h
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3,-Wall -Iinclude -I$(CSRC) \
+             --expt-relaxed-constexpr -Xptxas -v
+LIBGFP    := $(PKG)/libgfp.so
+
+.PHONY: all gfp oracle synth clean
+all: synth oracle gfp
+
+synth: synth/libsynth.so
+oracle: oracle/liboracle.so
+gfp: $(LIBGFP)
+
+synth/libsynth.so: synth/synth.c
+	$(CC) -O2 -fPIC -shared -Wall -Wno-unknown-pragmas -o $@ $<
+
+# oracle: plain C, no optimisation tricks, UB-checked build available via `make oracle-ubsan`
+oracle/liboracle.so: oracle/oracle.c
+	$(CC) -O2 -fPIC -shared -Wall -Wextra -o $@ $<
+
+oracle-ubsan: oracle/oracle.c
+	$(CC) -O1 -g -fsanitize=undefined,address -fno-omit-frame-pointer -fPIC -shared -o oracle/liboracle_san.so $<
+
+$(LIBGFP): $(GFP_SRCS) $(GFP_HDRS)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(GFP_SRCS) -lcudart 2> $(PKG)/build.log || (cat $(PKG)/build.log; exit 1)
+
+clean:
+	rm -f synth/libsynth.so oracle/liboracle.so oracle/liboracle_san.so $(LIBGFP)
