@@ -1,0 +1,561 @@
+#!/usr/bin/env python
+"""Benchmark of the exact GF(p) dot product on B200 (arXiv cs/0404008 hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 0..4] [--impl ours|reference]
+
+One JSON line on rank 0.  A "step" is one pass of the hot path over the workload:
+the default workload is BASELINE.json configs[2] -- GF(2^31-1), Montgomery B = 2^32, n = 2^28 u32 per
+operand, sharded over N GPUs (strong scaling: the total n is fixed), converted to Montgomery form on
+device before timing (the paper excludes conversions from dot timings; the conversion is
+timed separately and reported under "phases").  At N = 1 a step is one gfp_dot launch (delayed-modulus
+streaming + last-CTA-done reduction and encoding); at N > 1 it is gfp_dot_partial, one NCCL all_reduce
+of the int64 partial residue, and gfp_finalize.
+
+`value` = total terms / max-over-ranks device time (CUDA events on the launching stream, barrier and
+synchronize on both sides).  The inputs (1 GiB per operand at N = 1) exceed the 126 MB L2, so no flush
+is needed for the headline; the secondary configs that fit L2 flush it between timed launches.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402  (seeded input generator; holds no method arithmetic)
+
+P31 = 2 ** 31 - 1
+CONFIGS = {
+    0: dict(name="C1", workload="configs[0]: GF(65521) classical u32 dot, n=100000", p=65521, rep=0,
+            dtype=np.uint32, n=100_000, bpt=8, kind="dot"),
+    1: dict(name="C2", workload="configs[1]: GF(67108859) fp64 dot, n=10^7", p=67108859, rep=2,
+            dtype=np.float64, n=10 ** 7, bpt=16, kind="dot"),
+    2: dict(name="C3", workload="configs[2]: GF(2^31-1) Montgomery B=2^32 u32 dot, n=2^28, sharded",
+            p=P31, rep=1, dtype=np.uint32, n=1 << 28, bpt=8, kind="dot"),
+    3: dict(name="C4", workload="configs[3]: GF(32749) Zech u16 dot, n=2^26, 10% zeros", p=32749, rep=3,
+            dtype=np.uint16, n=1 << 26, bpt=4, kind="dot"),
+    4: dict(name="C5", workload="configs[4]: GF(65521) classical u16 matrix-vector 65536x4096, rows sharded",
+            p=65521, rep=0, dtype=np.uint16, rows=65536, n=4096, bpt=2, kind="batch"),
+}
+REP_NAMES = {0: "classical", 1: "montgomery", 2: "fp64", 3: "zech"}
+DTYPE_NAMES = {np.dtype(np.uint16): "u16", np.dtype(np.uint32): "u32", np.dtype(np.float64): "f64"}
+L2_BYTES = 126 * 10 ** 6
+
+
+# ------------------------------------------------------------------------------ environment
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_lookup(cfg_name, world):
+    """dram bytes (read+write) per launch of the dominant kernel, from a committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return t.get(f"{cfg_name}/N{world}", t.get(cfg_name))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons through NVML every ~5 ms while running."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4, "gpu_idle": 0x1,
+               "applications_clocks_setting": 0x2, "sync_boost": 0x10}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        names = [k for k, bit in self.REASONS.items() if self.reasons & bit and k != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------ inputs
+def shard(n, rank, world):
+    return n * rank // world, n * (rank + 1) // world
+
+
+def host_inputs(cfg, rank, world, limit=None):
+    """Host arrays of this rank's shard, in the representation's *input* form (classical residues for
+    Montgomery, which is converted on device; Zech codes; fp64 integers; classical residues)."""
+    seed = synth.BASE_SEED + [k for k, v in CONFIGS.items() if v is cfg][0]
+    p = cfg["p"]
+    if cfg["kind"] == "batch":
+        r0, r1 = shard(cfg["rows"], rank, world)
+        n = cfg["n"]
+        if limit is not None:
+            r1 = min(r1, r0 + max(1, limit // n))
+        A = synth.uniform(seed, synth.STREAM_MAT, r0 * n, (r1 - r0) * n, p, cfg["dtype"])
+        x = synth.uniform(seed, synth.STREAM_X, 0, n, p, cfg["dtype"])
+        return {"A": A.reshape(r1 - r0, n), "x": x, "rows": r1 - r0}
+    s0, s1 = shard(cfg["n"], rank, world)
+    if limit is not None:
+        s1 = min(s1, s0 + limit)
+    if cfg["rep"] == 3:
+        a = synth.zech_codes(seed, synth.STREAM_A, s0, s1 - s0, p - 1)
+        b = synth.zech_codes(seed, synth.STREAM_B, s0, s1 - s0, p - 1)
+    else:
+        a = synth.uniform(seed, synth.STREAM_A, s0, s1 - s0, p, cfg["dtype"])
+        b = synth.uniform(seed, synth.STREAM_B, s0, s1 - s0, p, cfg["dtype"])
+    return {"a": a, "b": b}
+
+
+def to_device(gfp, cfg, h, dev, stream):
+    """Device tensors in the representation; Montgomery conversion timed here (phase a2)."""
+    p, rep = cfg["p"], cfg["rep"]
+    phases = {}
+    if cfg["kind"] == "batch":
+        d = {"A": torch.from_numpy(h["A"]).to(dev), "x": torch.from_numpy(h["x"]).to(dev)}
+        torch.cuda.synchronize()
+        return d, phases
+    a = torch.from_numpy(h["a"]).to(dev)
+    b = torch.from_numpy(h["b"]).to(dev)
+    torch.cuda.synchronize()  # copies ran on the default stream; the kernels run on `stream`
+    if rep == 1:
+        am, bm = torch.empty_like(a), torch.empty_like(b)
+        with torch.cuda.stream(stream):
+            for _ in range(2):  # warm
+                gfp.to_rep(a, p, rep, out=am, stream=stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            iters = 5
+            e0.record(stream)
+            for _ in range(iters):
+                gfp.to_rep(a, p, rep, out=am, stream=stream)
+                gfp.to_rep(b, p, rep, out=bm, stream=stream)
+            e1.record(stream)
+        stream.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        nbytes = 2 * a.numel() * 4 * 2  # read 4 + write 4 bytes per element per operand
+        phases["to_montgomery"] = {"ms_per_pair": ms, "GB/s": nbytes / ms / 1e6,
+                                   "note": "a -> aB mod p for both operands (P:83-84); excluded from the dot "
+                                           "timing as in the paper (P:313-320)"}
+        del a, b
+        return {"a": am, "b": bm}, phases
+    return {"a": a, "b": b}, phases
+
+
+# ------------------------------------------------------------------------------ one step
+def make_step(gfp, cfg, d, world, group, stream):
+    p, rep = cfg["p"], cfg["rep"]
+    ev = []  # (start, end) events around the dominant kernel of each step
+    if cfg["kind"] == "batch":
+        out = torch.empty(d["A"].shape[0], dtype=d["A"].dtype, device=d["A"].device)
+
+        def step(record=True):
+            if record:
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record(stream)
+            gfp.dot_batch(d["A"], d["x"], p, rep, out=out, stream=stream)
+            if record:
+                e.record(stream)
+                ev.append((s, e))
+        return step, ev, out
+    a, b = d["a"], d["b"]
+    out = torch.empty(1, dtype=a.dtype, device=a.device)
+    partial = torch.empty(1, dtype=torch.int64, device=a.device)
+
+    def step(record=True):
+        if record:
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+        if world == 1:
+            gfp.dot(a, b, p, rep, out=out, stream=stream)
+        else:
+            gfp.dot_partial(a, b, p, rep, out=partial, stream=stream)
+        if record:
+            e.record(stream)
+            ev.append((s, e))
+        if world > 1:
+            dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
+            gfp.finalize(partial, p, rep, a.dtype, out=out, stream=stream)
+    return step, ev, out
+
+
+def l2_flush(buf):
+    buf.zero_()
+
+
+def time_steps(step, stream, K, W, world, flush=None):
+    for _ in range(W):
+        step(record=False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if flush is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(K):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+    else:  # L2-resident workloads: flush between launches, time each launch alone
+        ms = 0.0
+        for _ in range(K):
+            flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    return ms
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, world):
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------------------ oracle legs
+def oracle_time(cfg, h, budget_s=10.0, full_ok=True):
+    """Time the CPU oracle (as it stands, one thread) on a bounded prefix sample of the workload.
+    Returns (terms/s, sample description, result-on-sample, sample_terms)."""
+    import oracle
+    p, rep = cfg["p"], cfg["rep"]
+    if cfg["kind"] == "batch":
+        A, x = h["A"], h["x"]
+
+        def run(rows):
+            return oracle.dot_batch_classical(p, A[:rows], x)
+        t0 = time.perf_counter()
+        run(64)
+        per_row = (time.perf_counter() - t0) / 64
+        rows = int(min(A.shape[0], max(64, budget_s / max(per_row, 1e-9))))
+        t0 = time.perf_counter()
+        res = run(rows)
+        dt = time.perf_counter() - t0
+        terms = rows * A.shape[1]
+        return terms / dt, f"first {rows} of {A.shape[0]} rows x {A.shape[1]} ({terms} terms)", res, rows
+
+    a, b = h["a"], h["b"]
+
+    def run(m):
+        if rep == 0:
+            return oracle.dot_classical(p, a[:m], b[:m])
+        if rep == 1:
+            return oracle.dot_montgomery(p, a[:m], b[:m])
+        if rep == 2:
+            return oracle.dot_fp64(p, a[:m], b[:m])
+        return oracle.dot_zech(p, 2, a[:m], b[:m])
+    m0 = min(len(a), 1 << 18)
+    t0 = time.perf_counter()
+    run(m0)
+    per = (time.perf_counter() - t0) / max(m0, 1)
+    m = int(min(len(a), max(m0, budget_s / max(per, 1e-12))))
+    if not full_ok:
+        m = min(m, len(a))
+    t0 = time.perf_counter()
+    res = run(m)
+    dt = time.perf_counter() - t0
+    return m / dt, f"first {m} of {len(a)} terms of this rank's shard", res, m
+
+
+# ------------------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-secondary", action="store_true", help="skip the per-config kernel table")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--oracle-budget", type=float, default=12.0, help="seconds of oracle work per sample")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        return reference_arm(args, cfg, world, rank)
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    import paper_cs_0404008_b200 as gfp
+
+    stream = torch.cuda.Stream(device=dev)
+    h = host_inputs(cfg, rank, world)
+    d, phases = to_device(gfp, cfg, h, dev, stream)
+    step, ev, out = make_step(gfp, cfg, d, world, group, stream)
+    if cfg["kind"] == "batch":
+        local_terms = d["A"].shape[0] * cfg["n"]
+        local_bytes = d["A"].numel() * d["A"].element_size() + d["x"].numel() * d["x"].element_size() \
+            + d["A"].shape[0] * d["A"].element_size()
+    else:
+        local_terms = d["a"].numel()
+        local_bytes = local_terms * cfg["bpt"]
+    total_terms = cfg["rows"] * cfg["n"] if cfg["kind"] == "batch" else cfg["n"]
+    flush_buf = None
+    if local_bytes < 3 * L2_BYTES:
+        flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    with torch.cuda.stream(stream):
+        gfp.launch_count(reset=True)
+        with ClockSampler(local) as clk:
+            ms = time_steps(step, stream, args.steps, args.warmup, world,
+                            flush=(lambda: l2_flush(flush_buf)) if flush_buf is not None else None)
+        launches_total = gfp.launch_count()
+    launches_timed = launches_total - args.warmup * (1 if world == 1 or cfg["kind"] == "batch" else 2)
+    kern_ms = [s.elapsed_time(e) for s, e in ev[-args.steps:]]
+    kern_avg = statistics.mean(kern_ms)
+    ms_max = max_over_ranks(ms, world)
+    value = total_terms * args.steps / (ms_max / 1e3)
+    peak, peak_src = peak_hbm()
+    achieved = local_bytes / (kern_avg / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic_lookup(cfg["name"], world),
+            "kernel": "dot_kernel<Montgomery<2>>" if cfg["name"] == "C3" else cfg["name"],
+            "algorithmic_bytes_per_launch": local_bytes, "avg_launch_ms": round(kern_avg, 4),
+            "peak_source": peak_src, "spec_8TBps_frac": round(achieved / 8000.0, 4)}
+
+    # ---------------------------------------------------------------- correctness of the timed result
+    parity = None
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        hh = dict(h)
+        if cfg["rep"] == 1:  # the oracle reads the Montgomery-form vectors the GPU dotted
+            hh = {"a": d["a"].cpu().numpy(), "b": d["b"].cpu().numpy()}
+        tps, sample, ores, m = oracle_time(cfg, hh, args.oracle_budget)
+        cpu = {"value": tps, "unit": "terms/s", "cores": 1, "kind": "oracle", "sample": sample,
+               "threads_note": "oracle is single-threaded C (one 128-bit remainder per term)"}
+        # parity of the GPU path on the same sample (the whole shard when the sample covers it)
+        if cfg["kind"] == "batch":
+            got = gfp.dot_batch(d["A"][:m], d["x"], cfg["p"], cfg["rep"]).cpu().numpy().astype(np.uint64)
+            parity = bool(np.array_equal(got, ores))
+        else:
+            r = gfp.dot(d["a"][:m], d["b"][:m], cfg["p"], cfg["rep"])
+            got = r.cpu()[0].item() if cfg["rep"] == 2 else int(r.cpu().to(torch.int64)[0])
+            parity = got == ores
+        cpu["parity_checked_terms"] = int(m) if cfg["kind"] == "dot" else int(m) * cfg["n"]
+
+    # ---------------------------------------------------------------- end to end (host buffers)
+    e2e = e2e_leg(gfp, cfg, d, world, args.e2e_steps, stream, dev)
+
+    # ---------------------------------------------------------------- secondary configs (kernel only)
+    secondary = None
+    if not args.no_secondary and world == 1:
+        secondary = secondary_table(gfp, args, dev, stream, exclude=args.config)
+
+    if rank == 0:
+        line = {
+            "metric": "GF(p) dot-product terms/sec and HBM GB/s (% of peak) at 1/2/4/8 B200",
+            "value": value, "unit": "terms/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": DTYPE_NAMES[np.dtype(cfg["dtype"])], "data": "synthetic",
+            "config": {"workload": cfg["workload"], "p": cfg["p"], "representation": REP_NAMES[cfg["rep"]],
+                       "n_total": total_terms, "terms_per_rank": local_terms,
+                       "parallelism": f"shard x{world}" + (" + NCCL all_reduce(int64)" if world > 1 and
+                                                           cfg["kind"] == "dot" else ""),
+                       "l2": ("inputs larger than L2: %.0f MiB per rank vs 126 MB L2" % (local_bytes / 2 ** 20))
+                       if flush_buf is None else "L2 flushed (256 MiB write) before every timed launch",
+                       "seed": synth.BASE_SEED + args.config},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_timed,
+            "clocks": clk.summary(), "parity_vs_oracle": parity, "phases": phases,
+            "secondary": secondary,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_leg(gfp, cfg, d, world, steps, stream, dev):
+    """Same metric through the public API from pinned HOST buffers: per step, the host->device copy of
+    the inputs, the kernels, and the device->host read of the result are inside the timed region."""
+    if steps <= 0:
+        return None
+    p, rep = cfg["p"], cfg["rep"]
+    if cfg["kind"] == "batch":
+        A = d["A"].cpu().pin_memory()
+        x = d["x"].cpu().pin_memory()
+        res = torch.empty(A.shape[0], dtype=A.dtype).pin_memory()
+        h2d = A.numel() * A.element_size() + x.numel() * x.element_size()
+        d2h = res.numel() * res.element_size()
+
+        def one():
+            with torch.cuda.stream(stream):
+                Ad = A.to(dev, non_blocking=True)
+                xd = x.to(dev, non_blocking=True)
+                o = gfp.dot_batch(Ad, xd, p, rep, stream=stream)
+                res.copy_(o, non_blocking=True)
+            stream.synchronize()
+        terms = A.shape[0] * cfg["n"]
+    else:
+        a = d["a"].cpu().pin_memory()
+        b = d["b"].cpu().pin_memory()
+        h2d = 2 * a.numel() * a.element_size()
+        d2h = a.element_size()
+        part = torch.empty(1, dtype=torch.int64, device=dev)
+        fin = torch.empty(1, dtype=a.dtype, device=dev)
+
+        def one():
+            r = gfp.dot_host(a, b, p, rep, stream=stream)
+            if world > 1:  # combine the per-rank results (additive in every rep but Zech)
+                part.fill_(int(r))
+                dist.all_reduce(part)
+                gfp.finalize(part, p, rep, a.dtype, out=fin, stream=stream)
+                fin.cpu()
+        terms = a.numel()
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize()
+    dt = max_over_ranks(time.perf_counter() - t0, world)
+    total = sum_over_ranks(terms, world)
+    return {"value": total * steps / dt, "unit": "terms/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "api": "gfp_dot_host (chunked pinned H2D overlapped with the dot kernels)"
+            if cfg["kind"] == "dot" else "torch H2D + gfp_dot_batch + D2H",
+            "clock": "host wall clock around synchronous calls, max over ranks"}
+
+
+def secondary_table(gfp, args, dev, stream, exclude):
+    """Kernel-only throughput of every other config (1 GPU), with roofline fraction."""
+    peak, _ = peak_hbm()
+    table = {}
+    for idx, cfg in CONFIGS.items():
+        if idx == exclude:
+            continue
+        h = host_inputs(cfg, 0, 1)
+        d, phases = to_device(gfp, cfg, h, dev, stream)
+        step, ev, out = make_step(gfp, cfg, d, 1, None, stream)
+        if cfg["kind"] == "batch":
+            terms = cfg["rows"] * cfg["n"]
+            nbytes = d["A"].numel() * 2 + d["x"].numel() * 2 + cfg["rows"] * 2
+        else:
+            terms = cfg["n"]
+            nbytes = terms * cfg["bpt"]
+        flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if nbytes < 3 * L2_BYTES else None
+        K = 20
+        with torch.cuda.stream(stream):
+            time_steps(step, stream, K, 3, 1, flush=(lambda: l2_flush(flush_buf)) if flush_buf is not None else None)
+        ks = [s.elapsed_time(e) for s, e in ev[-K:]]
+        avg = statistics.mean(ks)
+        table[cfg["name"]] = {"workload": cfg["workload"], "terms_per_s": terms / (avg / 1e3),
+                              "us_per_launch": avg * 1e3, "GB/s": nbytes / (avg / 1e3) / 1e9,
+                              "frac_of_measured_hbm": nbytes / (avg / 1e3) / 1e9 / peak,
+                              "l2": "flushed" if flush_buf is not None else "inputs > L2"}
+        if phases:
+            table[cfg["name"]]["phases"] = phases
+        del d, step, ev, out, flush_buf
+        torch.cuda.empty_cache()
+    return table
+
+
+def reference_arm(args, cfg, world, rank):
+    """--impl reference: the CPU oracle as it stands (there is no reference code for this paper), timed on
+    the host, each step a bounded sample of the same workload.  Rank 0 only; other ranks exit 0."""
+    if rank != 0:
+        return
+    h = host_inputs(cfg, 0, 1, limit=1 << 24)
+    if cfg["rep"] == 1:  # Montgomery form a*2^32 mod p of the sample, prepared on the host (p < 2^32)
+        p = np.uint64(cfg["p"])
+        h = {k: ((v.astype(np.uint64) << np.uint64(32)) % p).astype(np.uint32) for k, v in h.items()}
+    budget = max(0.5, min(args.oracle_budget, 60.0 / max(args.steps + args.warmup, 1)))
+    vals = []
+    desc = None
+    for i in range(args.warmup + args.steps):
+        tps, desc, _, m = oracle_time(cfg, h, budget)
+        if i >= args.warmup:
+            vals.append(tps)
+    value = statistics.mean(vals)
+    sample_terms = m if cfg["kind"] == "dot" else m * cfg["n"]
+    line = {"impl": "reference", "metric": "GF(p) dot-product terms/sec and HBM GB/s (% of peak) at 1/2/4/8 B200",
+            "value": value, "unit": "terms/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sample_terms / value * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": DTYPE_NAMES[np.dtype(cfg["dtype"])], "data": "synthetic",
+            "config": {"workload": cfg["workload"], "p": cfg["p"], "representation": REP_NAMES[cfg["rep"]],
+                       "n_total": cfg["n"] if cfg["kind"] == "dot" else cfg["rows"] * cfg["n"]},
+            "cpu_baseline": {"value": value, "unit": "terms/s", "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": "terms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "no reference implementation exists (paper only); the reference arm is the CPU oracle"}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

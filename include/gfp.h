@@ -1,0 +1,178 @@
+/*
+ * gfp.h -- C ABI of libgfp: the exact dot product of two vectors over a
+ * word-size prime field GF(p) on NVIDIA B200 (sm_100a).
+ *
+ * Paper: J.-G. Dumas, "Efficient dot product over word-size finite fields",
+ * arXiv cs/0404008.  Citations "P:n" are lines of its text with the
+ * section; "G<k>" are the readings of ambiguous passages listed in DESIGN.md.
+ *
+ * What is computed (sec. 3).  For two length-n vectors whose
+ * entries are canonical elements of GF(p) in one of the paper's
+ * representations, the dot product r = sum_i a_i b_i in GF(p), returned in
+ * the SAME representation ("the dot products are of course
+ * performed with their representations", reading G10).  The method is the
+ * paper's delayed modulus (sec. 3.1 Eq. (1); sec. 3.2 blocks,
+ * P:352-377; sec. 3.3 overflow correction): products are summed in
+ * a wide register and reduced mod p only when the bound on the register
+ * would otherwise be crossed.  The result is exact; it is bit-identical to
+ * the plain definition (sum a_i b_i) mod p.
+ *
+ * Representations (sec. 2) and admissible (rep, dtype, p):
+ *   GFP_REP_CLASSICAL  residues in [0, p-1]           (sec. 2.1)
+ *       GFP_U16: p <= 65521          GFP_U32: p <= 4294967291
+ *   GFP_REP_MONTGOMERY a stored as a*B mod p, B=2^32  (sec. 2.2)
+ *       GFP_U32: odd p <= 2654435761
+ *   GFP_REP_FP64       exact integers in [0, p-1] held in binary64,
+ *                      reduced by T -= floor(T*invP)*P and one +-P fix-up
+ *                      (sec. 2.3, NTL listing P:112-117)
+ *       GFP_F64: p <= 94906249 (largest prime with p(p-1) < 2^53; Eq. (1)
+ *                at m = 53, P:338-339 reading G9)
+ *   GFP_REP_ZECH       discrete-log codes: 0 -> 0, 1 -> q-1, g^i -> i
+ *                      (sec. 2.4), g = smallest primitive root
+ *       GFP_U16: p <= 65521 (the antilog table must fit shared memory; the
+ *                paper's index bound 1073741789, is looser)
+ *   p must be prime (GFP_E_NOT_PRIME) and within the bound (GFP_E_BOUND);
+ *   any other (rep, dtype) pair is GFP_E_UNSUPPORTED.
+ *
+ * Pointers.  Unless a function says "host", every array pointer is a CUDA
+ * device pointer on the current device, owned by the caller.  Element
+ * pointers must be aligned to their element size (GFP_E_INVAL otherwise);
+ * 16-byte alignment of both operands (at equal offsets) enables the
+ * vectorised path, anything else is handled by a slower scalar path.
+ *
+ * Streams.  `stream` is a cudaStream_t passed as void* (NULL = the legacy
+ * default stream).  Device-pointer calls are asynchronous: they enqueue work
+ * on `stream` and return; results are ready in stream order.  They never
+ * allocate on the hot path after the first call for a (device, p, rep,
+ * stream) and are safe to capture in a CUDA graph after that first call.
+ *
+ * Preconditions.  Entries must be canonical elements of the representation
+ * (P:49-50).  This is not checked on the hot path: non-canonical entries give
+ * an unspecified result but never an out-of-bounds access (Zech indices are
+ * clamped into the table).
+ *
+ * Errors.  Argument errors are returned synchronously with nothing enqueued
+ * and nothing written.  Launch failures return GFP_E_CUDA with text from
+ * gfp_last_error().  Asynchronous device faults surface at the caller's next
+ * synchronisation.  All functions are thread-safe.
+ */
+#ifndef GFP_H
+#define GFP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GFP_OK = 0,
+    GFP_E_INVAL = 1,       /* bad argument: n < 0, NULL with n > 0, misaligned, unknown enum */
+    GFP_E_NOT_PRIME = 2,   /* p is not prime */
+    GFP_E_BOUND = 3,       /* p outside the representation's bound (table above) */
+    GFP_E_UNSUPPORTED = 4, /* (rep, dtype) combination not offered */
+    GFP_E_CUDA = 5,        /* CUDA runtime error (see gfp_last_error) */
+    GFP_E_NOMEM = 6        /* device or pinned allocation failed */
+} gfp_status;
+
+typedef enum {
+    GFP_REP_CLASSICAL = 0,
+    GFP_REP_MONTGOMERY = 1,
+    GFP_REP_FP64 = 2,
+    GFP_REP_ZECH = 3
+} gfp_rep;
+
+typedef enum { GFP_U16 = 0, GFP_U32 = 1, GFP_F64 = 2 } gfp_dtype;
+
+/* Accumulation strategy the kernels use for a (p, rep, dtype), chosen on the
+ * host from the bounds of sec. 3. */
+typedef enum {
+    GFP_ACC_DELAYED = 0,   /* Eq. (1): n products never overflow -> one final reduction */
+    GFP_ACC_BLOCKED = 1,   /* sec. 3.2: reduce every k products (Montgomery sec. 3.2.1) */
+    GFP_ACC_OVERFLOW = 2   /* sec. 3.3: let the u64 wrap, add CORR = 2^64 mod p on wrap */
+} gfp_acc;
+
+/* Host-side description of a field/representation (gfp_query). */
+typedef struct {
+    uint64_t p;
+    int32_t rep, dtype;
+    uint64_t bound;        /* largest admissible p for (rep, dtype) */
+    int32_t acc_bits;      /* m of Eq. (1): 64 (integer accumulators) or 53 (binary64) */
+    int32_t mont_kr;       /* Montgomery: products per REDC allowed by the two G6 bounds, capped at 10^6; else 0 */
+    uint64_t k;            /* Eq. (1) with a carried residue (reading G7):
+                              largest k with k(p-1)^2 + (p-1) <= 2^m - 1 (binary64: < 2^53) */
+    uint64_t corr;         /* CORR = 2^64 mod p (sec. 3.3) */
+    uint32_t n_im;         /* Montgomery: -p^{-1} mod 2^32; else 0 */
+    uint32_t pad0;
+    uint64_t r2;           /* Montgomery: B^2 mod p, to_mont(a) = REDC(a * R2) */
+    uint64_t b_mod_p;      /* 2^32 mod p */
+    double inv_p;          /* binary64 RN(1/p) (reading G8) */
+    uint64_t g;            /* Zech: generator (smallest primitive root, reading G12); else 0 */
+    uint64_t qbar;         /* Zech: q-1; else 0 */
+    uint64_t table_bytes;  /* Zech: bytes of the shared-memory antilog table; else 0 */
+} gfp_info;
+
+/* host: validate (p, rep, dtype) and fill *info.  No device work. */
+gfp_status gfp_query(uint64_t p, gfp_rep rep, gfp_dtype dt, gfp_info *info);
+
+/* r = a . b in GF(p), written to out[0] (device, one element of dtype `dt`).
+ * a, b: device arrays of n elements of dtype `dt` in representation `rep`.
+ * n == 0 writes the representation's zero (0, 0, +0.0, code 0).
+ * One kernel launch: streaming delayed-modulus accumulation, warp-shuffle and
+ * CTA-tree combination, last-CTA-done final reduction and encoding. */
+gfp_status gfp_dot(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
+                   void *out, void *stream);
+
+/* Batched: out[r] = A[r*lda .. r*lda+n) . x for r in [0, rows) -- many
+ * independent dots / a GF(p) matrix-vector product (sec. 1).
+ * A: device, row-major with leading dimension lda >= n (elements);
+ * x: device, n elements; out: device, `rows` elements of dtype `dt`.
+ * Supported reps: classical (u16, u32), Montgomery (u32), fp64, Zech (u16). */
+gfp_status gfp_dot_batch(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *A, int64_t lda,
+                         const void *x, int64_t rows, int64_t n, void *out, void *stream);
+
+/* Representation conversion (sec. 2.2 a -> aB mod p; sec. 2.4 the
+ * discrete-log encoding P:126-131; fp64: exact casts).  Timed separately from
+ * the dot.
+ *   gfp_to_rep  : `in` holds canonical classical residues (in_dt U16/U32);
+ *                 `out` receives the representation in out_dt (the rep's dtype).
+ *   gfp_from_rep: the inverse; in_dt is the rep's dtype, out_dt U16/U32.
+ * In-place (in == out) is allowed when in_dt == out_dt. */
+gfp_status gfp_to_rep(uint64_t p, gfp_rep rep, gfp_dtype in_dt, const void *in, gfp_dtype out_dt,
+                      void *out, int64_t n, void *stream);
+gfp_status gfp_from_rep(uint64_t p, gfp_rep rep, gfp_dtype in_dt, const void *in, gfp_dtype out_dt,
+                        void *out, int64_t n, void *stream);
+
+/* Multi-GPU bracket.  gfp_dot_partial writes to
+ * partial[0] (device uint64) this shard's contribution: a residue in [0, p)
+ * in the representation's additive form (classical value; Montgomery form;
+ * the integer value for fp64; the classical value for Zech).  The caller sums
+ * partials across ranks (e.g. an NCCL all_reduce SUM over int64; at most 2^31
+ * ranks) and calls gfp_finalize(summed) -> out[0] in the representation. */
+gfp_status gfp_dot_partial(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b,
+                           int64_t n, uint64_t *partial, void *stream);
+gfp_status gfp_finalize(uint64_t p, gfp_rep rep, gfp_dtype dt, const uint64_t *summed, void *out,
+                        void *stream);
+
+/* End-to-end convenience: a, b, out are HOST pointers (pinned memory gives
+ * overlapped copies; pageable works but copies synchronously).  Streams the
+ * operands to the device in chunks through library-owned staging buffers,
+ * overlapping each chunk's host->device copy with the previous chunk's
+ * kernel, then copies the result back.  Synchronous: returns when out[0] is
+ * written. */
+gfp_status gfp_dot_host(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
+                        void *out, void *stream);
+
+/* Number of kernels the library launched on this host thread since the
+ * last reset (evidence for the bench's gpu_launches claim). */
+uint64_t gfp_launch_count(int reset);
+
+const char *gfp_status_str(gfp_status s);
+const char *gfp_last_error(void);    /* thread-local text of the last error */
+void gfp_release_caches(void);      /* free device tables, workspaces and staging buffers */
+const char *gfp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GFP_H */

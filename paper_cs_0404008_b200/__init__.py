@@ -1,0 +1,243 @@
+"""Python binding of libgfp (include/gfp.h): the exact GF(p) dot product on B200.
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels of libgfp.so.  The
+library must be built in-tree (`make gfp`, or `python -c "import __graft_entry__ as g; g.build()"`);
+importing fails loudly when it is missing -- there is no CPU fallback.
+
+    import torch, paper_cs_0404008_b200 as gfp
+    a = torch.randint(0, 65521, (10**6,), dtype=torch.int64).to(torch.uint32).cuda()
+    r = gfp.dot(a, a, 65521, gfp.CLASSICAL)          # 1-element uint32 tensor on the device
+
+Paper: arXiv cs/0404008; citations P:n are lines of its text.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+__all__ = [
+    "CLASSICAL", "MONTGOMERY", "FP64", "ZECH", "GfpError", "lib", "query", "dot", "dot_batch",
+    "dot_partial", "finalize", "to_rep", "from_rep", "dot_host", "launch_count", "release_caches",
+    "rep_dtype",
+]
+
+CLASSICAL, MONTGOMERY, FP64, ZECH = 0, 1, 2, 3
+U16, U32, F64 = 0, 1, 2
+_REP_NAMES = {CLASSICAL: "classical", MONTGOMERY: "montgomery", FP64: "fp64", ZECH: "zech"}
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libgfp.so")
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(f"{_LIB_PATH} is missing: build it with `make gfp` (nvcc, sm_100a). "
+                      "There is no CPU fallback.")
+
+
+class GfpInfo(ctypes.Structure):
+    _fields_ = [("p", ctypes.c_uint64), ("rep", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("bound", ctypes.c_uint64), ("acc_bits", ctypes.c_int32), ("mont_kr", ctypes.c_int32),
+                ("k", ctypes.c_uint64), ("corr", ctypes.c_uint64), ("n_im", ctypes.c_uint32),
+                ("pad0", ctypes.c_uint32), ("r2", ctypes.c_uint64), ("b_mod_p", ctypes.c_uint64),
+                ("inv_p", ctypes.c_double), ("g", ctypes.c_uint64), ("qbar", ctypes.c_uint64),
+                ("table_bytes", ctypes.c_uint64)]
+
+
+lib = ctypes.CDLL(_LIB_PATH)
+_u64, _i64, _int, _vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+_SIGS = {
+    "gfp_query": [_u64, _int, _int, ctypes.POINTER(GfpInfo)],
+    "gfp_dot": [_u64, _int, _int, _vp, _vp, _i64, _vp, _vp],
+    "gfp_dot_batch": [_u64, _int, _int, _vp, _i64, _vp, _i64, _i64, _vp, _vp],
+    "gfp_to_rep": [_u64, _int, _int, _vp, _int, _vp, _i64, _vp],
+    "gfp_from_rep": [_u64, _int, _int, _vp, _int, _vp, _i64, _vp],
+    "gfp_dot_partial": [_u64, _int, _int, _vp, _vp, _i64, _vp, _vp],
+    "gfp_finalize": [_u64, _int, _int, _vp, _vp, _vp],
+    "gfp_dot_host": [_u64, _int, _int, _vp, _vp, _i64, _vp, _vp],
+}
+for _name, _args in _SIGS.items():
+    getattr(lib, _name).argtypes = _args
+    getattr(lib, _name).restype = _int
+lib.gfp_launch_count.argtypes = [_int]
+lib.gfp_launch_count.restype = _u64
+lib.gfp_status_str.argtypes = [_int]
+lib.gfp_status_str.restype = ctypes.c_char_p
+lib.gfp_last_error.argtypes = []
+lib.gfp_last_error.restype = ctypes.c_char_p
+lib.gfp_release_caches.argtypes = []
+lib.gfp_release_caches.restype = None
+lib.gfp_version.argtypes = []
+lib.gfp_version.restype = ctypes.c_char_p
+
+
+class GfpError(RuntimeError):
+    def __init__(self, status: int):
+        self.status = status
+        super().__init__(f"{lib.gfp_status_str(status).decode()}: {lib.gfp_last_error().decode()}")
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        raise GfpError(status)
+
+
+_TORCH_DT = {torch.uint16: U16, torch.uint32: U32, torch.float64: F64}
+_DT_TORCH = {U16: torch.uint16, U32: torch.uint32, F64: torch.float64}
+
+
+def rep_dtype(rep: int, p: int) -> torch.dtype:
+    """The natural storage dtype of a representation (gfp.h table)."""
+    if rep == FP64:
+        return torch.float64
+    if rep == MONTGOMERY:
+        return torch.uint32
+    if rep == ZECH:
+        return torch.uint16
+    return torch.uint16 if p <= 65521 else torch.uint32
+
+
+def _dt(t: torch.Tensor) -> int:
+    try:
+        return _TORCH_DT[t.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported dtype {t.dtype}; use uint16, uint32 or float64") from None
+
+
+def _stream(t: torch.Tensor | None, stream) -> int:
+    if stream is not None:
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    if t is not None and t.is_cuda:
+        return torch.cuda.current_stream(t.device).cuda_stream
+    return 0
+
+
+def _flat_cuda(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (use dot_host for host buffers)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t.reshape(-1)
+
+
+def query(p: int, rep: int, dtype: torch.dtype | None = None) -> dict:
+    """Host-side constants and bounds for (p, rep, dtype): k, CORR, n_im, R2, invP, g, ... (gfp_query)."""
+    info = GfpInfo()
+    dt = _TORCH_DT[dtype if dtype is not None else rep_dtype(rep, p)]
+    _check(lib.gfp_query(p, rep, dt, ctypes.byref(info)))
+    return {f: getattr(info, f) for f, _ in GfpInfo._fields_ if f != "pad0"}
+
+
+def dot(a: torch.Tensor, b: torch.Tensor, p: int, rep: int = CLASSICAL, out: torch.Tensor | None = None,
+        stream=None) -> torch.Tensor:
+    """a . b over GF(p) in representation `rep`; returns a 1-element device tensor in that representation."""
+    a, b = _flat_cuda(a, "a"), _flat_cuda(b, "b")
+    if a.numel() != b.numel() or a.dtype != b.dtype or a.device != b.device:
+        raise ValueError("a and b must have the same length, dtype and device")
+    if out is None:
+        out = torch.empty(1, dtype=a.dtype, device=a.device)
+    with torch.cuda.device(a.device):
+        _check(lib.gfp_dot(p, rep, _dt(a), a.data_ptr(), b.data_ptr(), a.numel(), out.data_ptr(), _stream(a, stream)))
+    return out
+
+
+def dot_partial(a: torch.Tensor, b: torch.Tensor, p: int, rep: int = CLASSICAL, out: torch.Tensor | None = None,
+                stream=None) -> torch.Tensor:
+    """This shard's partial residue (int64 device tensor of 1 element) for a later all-reduce + finalize."""
+    a, b = _flat_cuda(a, "a"), _flat_cuda(b, "b")
+    if a.numel() != b.numel() or a.dtype != b.dtype:
+        raise ValueError("a and b must have the same length and dtype")
+    if out is None:
+        out = torch.empty(1, dtype=torch.int64, device=a.device)
+    with torch.cuda.device(a.device):
+        _check(lib.gfp_dot_partial(p, rep, _dt(a), a.data_ptr(), b.data_ptr(), a.numel(), out.data_ptr(),
+                                   _stream(a, stream)))
+    return out
+
+
+def finalize(summed: torch.Tensor, p: int, rep: int, dtype: torch.dtype, out: torch.Tensor | None = None,
+             stream=None) -> torch.Tensor:
+    """mod p and encode a summed partial (int64 device tensor) into the representation's dtype."""
+    if summed.dtype != torch.int64 or not summed.is_cuda:
+        raise ValueError("summed must be an int64 CUDA tensor")
+    if out is None:
+        out = torch.empty(1, dtype=dtype, device=summed.device)
+    with torch.cuda.device(summed.device):
+        _check(lib.gfp_finalize(p, rep, _TORCH_DT[dtype], summed.data_ptr(), out.data_ptr(), _stream(summed, stream)))
+    return out
+
+
+def dot_batch(A: torch.Tensor, x: torch.Tensor, p: int, rep: int = CLASSICAL, out: torch.Tensor | None = None,
+              rows: int | None = None, n: int | None = None, lda: int | None = None, stream=None) -> torch.Tensor:
+    """out[r] = A[r, :n] . x over GF(p): many independent dots / a matrix-vector product."""
+    if not (A.is_cuda and x.is_cuda):
+        raise ValueError("A and x must be CUDA tensors")
+    if A.dtype != x.dtype:
+        raise ValueError("A and x must have the same dtype")
+    if A.dim() == 2:
+        if A.stride(1) != 1:
+            raise ValueError("A must be row-major with unit column stride")
+        rows = A.shape[0] if rows is None else rows
+        n = A.shape[1] if n is None else n
+        lda = A.stride(0) if lda is None else lda
+    else:
+        if rows is None or n is None:
+            raise ValueError("flat A needs rows and n")
+        lda = n if lda is None else lda
+    if not x.is_contiguous():
+        raise ValueError("x must be contiguous")
+    if out is None:
+        out = torch.empty(rows, dtype=A.dtype, device=A.device)
+    with torch.cuda.device(A.device):
+        _check(lib.gfp_dot_batch(p, rep, _dt(A), A.data_ptr(), lda, x.data_ptr(), rows, n, out.data_ptr(),
+                                 _stream(A, stream)))
+    return out
+
+
+def to_rep(x: torch.Tensor, p: int, rep: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Canonical residues (uint16/uint32) -> representation `rep` (Montgomery aB mod p, Zech codes, fp64)."""
+    x = _flat_cuda(x, "x")
+    if out is None:
+        out = torch.empty(x.numel(), dtype=rep_dtype(rep, p), device=x.device)
+    with torch.cuda.device(x.device):
+        _check(lib.gfp_to_rep(p, rep, _dt(x), x.data_ptr(), _dt(out), out.data_ptr(), x.numel(), _stream(x, stream)))
+    return out
+
+
+def from_rep(x: torch.Tensor, p: int, rep: int, out: torch.Tensor | None = None, dtype: torch.dtype | None = None,
+             stream=None) -> torch.Tensor:
+    """Representation `rep` -> canonical residues (uint32 unless `dtype`/`out` says otherwise)."""
+    x = _flat_cuda(x, "x")
+    if out is None:
+        out = torch.empty(x.numel(), dtype=dtype or torch.uint32, device=x.device)
+    with torch.cuda.device(x.device):
+        _check(lib.gfp_from_rep(p, rep, _dt(x), x.data_ptr(), _dt(out), out.data_ptr(), x.numel(),
+                                _stream(x, stream)))
+    return out
+
+
+def dot_host(a: torch.Tensor, b: torch.Tensor, p: int, rep: int = CLASSICAL, stream=None):
+    """End to end from HOST buffers (pinned for overlap): chunked H2D + kernels + D2H of the result.
+
+    Returns the result as a Python number in the representation (int, or float for fp64)."""
+    if a.is_cuda or b.is_cuda:
+        raise ValueError("dot_host takes host tensors")
+    a, b = a.contiguous().reshape(-1), b.contiguous().reshape(-1)
+    if a.numel() != b.numel() or a.dtype != b.dtype:
+        raise ValueError("a and b must have the same length and dtype")
+    res = torch.empty(1, dtype=a.dtype)
+    s = _stream(None, stream) if stream is not None else torch.cuda.current_stream().cuda_stream
+    _check(lib.gfp_dot_host(p, rep, _dt(a), a.data_ptr(), b.data_ptr(), a.numel(), res.data_ptr(), s))
+    return res.item() if a.dtype == torch.float64 else int(res.to(torch.int64).item())
+
+
+def launch_count(reset: bool = False) -> int:
+    """Kernels libgfp launched on this host thread (since the last reset)."""
+    return int(lib.gfp_launch_count(1 if reset else 0))
+
+
+def release_caches() -> None:
+    lib.gfp_release_caches()
+
+
+def version() -> str:
+    return lib.gfp_version().decode()

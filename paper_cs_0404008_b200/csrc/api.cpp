@@ -1,0 +1,371 @@
+// api.cpp -- the C ABI of include/gfp.h: argument validation, per-(device, p, rep) constant and
+// table caches, per-(device, stream) workspaces, and the host-buffer pipeline of gfp_dot_host.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "gfp.h"
+#include "internal.h"
+#include "numtheory.h"
+
+namespace gfp {
+uint64_t launches(int reset);
+}
+
+using namespace gfp;
+
+namespace {
+
+thread_local std::string t_err;
+
+gfp_status fail(gfp_status s, const std::string &msg) {
+    t_err = msg;
+    return s;
+}
+
+gfp_status cuda_fail(cudaError_t e, const char *where) {
+    t_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return GFP_E_CUDA;
+}
+
+size_t dtype_size(int dt) { return dt == GFP_U16 ? 2 : (dt == GFP_U32 ? 4 : 8); }
+
+struct Ctx {
+    gfp_info info;
+    dev::KParams K;
+    uint16_t *d_antilog = nullptr, *d_log = nullptr;
+};
+
+std::mutex g_mu;
+std::map<std::tuple<int, uint64_t, int, int>, Ctx *> g_ctx;
+std::map<std::pair<int, cudaStream_t>, Workspace> g_ws;
+
+struct Staging {
+    size_t chunk_bytes = 0;
+    void *buf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    uint64_t *d_partial = nullptr;
+    void *d_out = nullptr;
+    cudaStream_t copy = nullptr;
+    cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+};
+std::map<int, Staging *> g_stage;
+std::mutex g_stage_mu;
+
+int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+gfp_status get_ctx(uint64_t p, gfp_rep rep, gfp_dtype dt, Ctx **out) {
+    const int dev = current_device();
+    auto key = std::make_tuple(dev, p, (int)rep, (int)dt);
+    std::lock_guard<std::mutex> g(g_mu);
+    auto it = g_ctx.find(key);
+    if (it != g_ctx.end()) {
+        *out = it->second;
+        return GFP_OK;
+    }
+    Ctx *c = new Ctx();
+    gfp_status st = describe(p, rep, dt, &c->info);
+    if (st != GFP_OK) {
+        delete c;
+        switch (st) {
+        case GFP_E_NOT_PRIME: return fail(st, "p = " + std::to_string(p) + " is not prime");
+        case GFP_E_BOUND:
+            return fail(st, "p = " + std::to_string(p) + " exceeds the bound " +
+                                std::to_string(rep_bound(rep, dt)) + " of this representation/dtype");
+        case GFP_E_UNSUPPORTED: return fail(st, "unsupported (representation, dtype) combination");
+        default: return fail(st, "invalid representation or dtype");
+        }
+    }
+    dev::KParams &K = c->K;
+    memset(&K, 0, sizeof(K));
+    K.p = p;
+    K.mu = UINT64_MAX / p;
+    K.corr = c->info.corr;
+    K.pd = (double)p;
+    K.inv_p = c->info.inv_p;
+    K.r2 = c->info.r2;
+    K.n_im = c->info.n_im;
+    K.qbar = (uint32_t)c->info.qbar;
+    if (rep == GFP_REP_ZECH) {
+        std::vector<uint16_t> logt, anti;
+        zech_tables(p, c->info.g, logt, anti);
+        logt.resize((logt.size() + 7) & ~size_t(7), 0);
+        anti.resize((anti.size() + 7) & ~size_t(7), 0);
+        cudaError_t e = cudaMalloc(&c->d_log, logt.size() * 2);
+        if (e == cudaSuccess) e = cudaMalloc(&c->d_antilog, anti.size() * 2);
+        if (e == cudaSuccess) e = cudaMemcpy(c->d_log, logt.data(), logt.size() * 2, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(c->d_antilog, anti.data(), anti.size() * 2, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(c->d_log);
+            cudaFree(c->d_antilog);
+            delete c;
+            return cuda_fail(e, "Zech table upload");
+        }
+        K.antilog = c->d_antilog;
+        K.logt = c->d_log;
+        K.antilog_entries = (uint32_t)anti.size();
+    }
+    g_ctx[key] = c;
+    *out = c;
+    return GFP_OK;
+}
+
+gfp_status get_ws(cudaStream_t s, Workspace *ws) {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> g(g_mu);
+    auto key = std::make_pair(dev, s);
+    auto it = g_ws.find(key);
+    if (it != g_ws.end()) {
+        *ws = it->second;
+        return GFP_OK;
+    }
+    void *mem = nullptr;
+    const size_t bytes = kMaxGrid * sizeof(uint64_t) + 64;
+    cudaError_t e = cudaMalloc(&mem, bytes);
+    if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? fail(GFP_E_NOMEM, "workspace") : cuda_fail(e, "workspace");
+    e = cudaMemset(mem, 0, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "workspace memset");
+    Workspace w;
+    w.partials = (uint64_t *)mem;
+    w.counter = (unsigned int *)((char *)mem + kMaxGrid * sizeof(uint64_t));
+    g_ws[key] = w;
+    *ws = w;
+    return GFP_OK;
+}
+
+bool aligned(const void *p, size_t a) { return ((uintptr_t)p % a) == 0; }
+
+gfp_status check_dot_args(gfp_dtype dt, const void *a, const void *b, int64_t n, const void *out, size_t out_align) {
+    if ((int)dt < 0 || (int)dt > 2) return fail(GFP_E_INVAL, "unknown dtype");
+    if (n < 0) return fail(GFP_E_INVAL, "n < 0");
+    if (out == nullptr) return fail(GFP_E_INVAL, "out is NULL");
+    if (n > 0 && (a == nullptr || b == nullptr)) return fail(GFP_E_INVAL, "NULL operand with n > 0");
+    const size_t es = dtype_size(dt);
+    if (!aligned(a, es) || !aligned(b, es)) return fail(GFP_E_INVAL, "operand not aligned to its element size");
+    if (!aligned(out, out_align)) return fail(GFP_E_INVAL, "output not aligned");
+    return GFP_OK;
+}
+
+gfp_status dot_common(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n, void *out,
+                      int mode, cudaStream_t s) {
+    gfp_status st = check_dot_args(dt, a, b, n, out, mode == OUT_ENCODE ? dtype_size(dt) : 8);
+    if (st != GFP_OK) return st;
+    Ctx *c;
+    if ((st = get_ctx(p, rep, dt, &c)) != GFP_OK) return st;
+    Workspace ws;
+    if ((st = get_ws(s, &ws)) != GFP_OK) return st;
+    DotPlan plan;
+    if ((st = plan_dot(c->info, c->K, a, b, n, &plan)) != GFP_OK) return st;
+    OutSpec o{out, (int)rep, (int)dt, mode};
+    cudaError_t e = launch_dot(plan, c->K, a, b, n, ws, o, s);
+    return e == cudaSuccess ? GFP_OK : cuda_fail(e, "dot launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+gfp_status gfp_query(uint64_t p, gfp_rep rep, gfp_dtype dt, gfp_info *info) {
+    if (info == nullptr) return fail(GFP_E_INVAL, "info is NULL");
+    gfp_status st = describe(p, rep, dt, info);
+    if (st == GFP_E_NOT_PRIME) return fail(st, "p is not prime");
+    if (st == GFP_E_BOUND) return fail(st, "p exceeds the representation bound");
+    if (st == GFP_E_UNSUPPORTED) return fail(st, "unsupported (representation, dtype) combination");
+    if (st != GFP_OK) return fail(st, "invalid representation or dtype");
+    return GFP_OK;
+}
+
+gfp_status gfp_dot(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n, void *out,
+                   void *stream) {
+    return dot_common(p, rep, dt, a, b, n, out, OUT_ENCODE, (cudaStream_t)stream);
+}
+
+gfp_status gfp_dot_partial(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
+                           uint64_t *partial, void *stream) {
+    return dot_common(p, rep, dt, a, b, n, partial, OUT_PARTIAL, (cudaStream_t)stream);
+}
+
+gfp_status gfp_finalize(uint64_t p, gfp_rep rep, gfp_dtype dt, const uint64_t *summed, void *out, void *stream) {
+    if (summed == nullptr || out == nullptr) return fail(GFP_E_INVAL, "NULL pointer");
+    if (!aligned(summed, 8) || ((int)dt >= 0 && (int)dt <= 2 && !aligned(out, dtype_size(dt))))
+        return fail(GFP_E_INVAL, "misaligned pointer");
+    Ctx *c;
+    gfp_status st = get_ctx(p, rep, dt, &c);
+    if (st != GFP_OK) return st;
+    OutSpec o{out, (int)rep, (int)dt, OUT_ENCODE};
+    cudaError_t e = launch_finalize(c->K, summed, 1, o, (cudaStream_t)stream);
+    return e == cudaSuccess ? GFP_OK : cuda_fail(e, "finalize launch");
+}
+
+gfp_status gfp_dot_batch(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *A, int64_t lda, const void *x,
+                         int64_t rows, int64_t n, void *out, void *stream) {
+    if ((int)dt < 0 || (int)dt > 2) return fail(GFP_E_INVAL, "unknown dtype");
+    if (rows < 0 || n < 0 || lda < n) return fail(GFP_E_INVAL, "need rows >= 0, n >= 0, lda >= n");
+    if (rows == 0) return GFP_OK;
+    if (out == nullptr || (n > 0 && (A == nullptr || x == nullptr))) return fail(GFP_E_INVAL, "NULL pointer");
+    const size_t es = dtype_size(dt);
+    if (!aligned(A, es) || !aligned(x, es) || !aligned(out, es)) return fail(GFP_E_INVAL, "misaligned pointer");
+    Ctx *c;
+    gfp_status st = get_ctx(p, rep, dt, &c);
+    if (st != GFP_OK) return st;
+    OutSpec o{out, (int)rep, (int)dt, OUT_ENCODE};
+    cudaError_t e = cudaSuccess;
+    st = launch_batch(c->info, c->K, A, lda, x, rows, n, o, (cudaStream_t)stream, &e);
+    if (st == GFP_E_CUDA) return cuda_fail(e, "batch launch");
+    if (st != GFP_OK) return fail(st, "batch: unsupported size for this representation");
+    return GFP_OK;
+}
+
+static gfp_status convert(uint64_t p, gfp_rep rep, int dir, gfp_dtype in_dt, const void *in, gfp_dtype out_dt,
+                          void *out, int64_t n, void *stream) {
+    if ((int)in_dt < 0 || (int)in_dt > 2 || (int)out_dt < 0 || (int)out_dt > 2)
+        return fail(GFP_E_INVAL, "unknown dtype");
+    if (n < 0) return fail(GFP_E_INVAL, "n < 0");
+    if (n > 0 && (in == nullptr || out == nullptr)) return fail(GFP_E_INVAL, "NULL pointer");
+    if (!aligned(in, dtype_size(in_dt)) || !aligned(out, dtype_size(out_dt)))
+        return fail(GFP_E_INVAL, "misaligned pointer");
+    if (in == out && in_dt != out_dt) return fail(GFP_E_INVAL, "in-place conversion needs in_dt == out_dt");
+    const gfp_dtype rep_dt = dir == 0 ? out_dt : in_dt;
+    Ctx *c;
+    gfp_status st = get_ctx(p, rep, rep_dt, &c);
+    if (st != GFP_OK) return st;
+    if (n == 0) return GFP_OK;
+    cudaError_t e = cudaSuccess;
+    st = launch_convert(c->info, c->K, dir, in_dt, in, out_dt, out, n, (cudaStream_t)stream, &e);
+    if (st == GFP_E_CUDA) return cuda_fail(e, "convert launch");
+    if (st != GFP_OK) return fail(st, "unsupported conversion dtypes for this representation");
+    return GFP_OK;
+}
+
+gfp_status gfp_to_rep(uint64_t p, gfp_rep rep, gfp_dtype in_dt, const void *in, gfp_dtype out_dt, void *out,
+                      int64_t n, void *stream) {
+    return convert(p, rep, 0, in_dt, in, out_dt, out, n, stream);
+}
+
+gfp_status gfp_from_rep(uint64_t p, gfp_rep rep, gfp_dtype in_dt, const void *in, gfp_dtype out_dt, void *out,
+                        int64_t n, void *stream) {
+    return convert(p, rep, 1, in_dt, in, out_dt, out, n, stream);
+}
+
+gfp_status gfp_dot_host(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n, void *out,
+                        void *stream) {
+    gfp_status st = check_dot_args(dt, a, b, n, out, 1);
+    if (st != GFP_OK) return st;
+    Ctx *c;
+    if ((st = get_ctx(p, rep, dt, &c)) != GFP_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    Workspace ws;
+    if ((st = get_ws(s, &ws)) != GFP_OK) return st;
+    const int dev = current_device();
+    const size_t es = dtype_size(dt);
+    Staging *S;
+    {
+        std::lock_guard<std::mutex> g(g_stage_mu);
+        auto it = g_stage.find(dev);
+        if (it == g_stage.end()) {
+            S = new Staging();
+            S->chunk_bytes = 64ull << 20;  // per operand per slot
+            cudaError_t e = cudaSuccess;
+            for (int i = 0; i < 2 && e == cudaSuccess; ++i)
+                for (int j = 0; j < 2 && e == cudaSuccess; ++j) e = cudaMalloc(&S->buf[i][j], S->chunk_bytes);
+            if (e == cudaSuccess) e = cudaMalloc(&S->d_partial, 64);
+            if (e == cudaSuccess) e = cudaMalloc(&S->d_out, 64);
+            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&S->copy, cudaStreamNonBlocking);
+            for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+                e = cudaEventCreateWithFlags(&S->copied[i], cudaEventDisableTiming);
+                if (e == cudaSuccess) e = cudaEventCreateWithFlags(&S->consumed[i], cudaEventDisableTiming);
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "staging allocation");
+            g_stage[dev] = S;
+        } else {
+            S = it->second;
+        }
+    }
+    std::lock_guard<std::mutex> g(g_stage_mu);  // one host pipeline per device at a time
+    const int64_t chunk = (int64_t)(S->chunk_bytes / es) & ~int64_t(7);
+    const int64_t nchunks = n == 0 ? 1 : (n + chunk - 1) / chunk;
+    cudaError_t e = cudaSuccess;
+    for (int64_t ci = 0; ci < nchunks && e == cudaSuccess; ++ci) {
+        const int slot = (int)(ci & 1);
+        const int64_t off = ci * chunk, len = std::min<int64_t>(chunk, n - off);
+        if (ci >= 2) e = cudaStreamWaitEvent(S->copy, S->consumed[slot], 0);  // slot free again
+        if (len > 0 && e == cudaSuccess)
+            e = cudaMemcpyAsync(S->buf[slot][0], (const char *)a + off * es, len * es, cudaMemcpyHostToDevice, S->copy);
+        if (len > 0 && e == cudaSuccess)
+            e = cudaMemcpyAsync(S->buf[slot][1], (const char *)b + off * es, len * es, cudaMemcpyHostToDevice, S->copy);
+        if (e == cudaSuccess) e = cudaEventRecord(S->copied[slot], S->copy);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, S->copied[slot], 0);
+        if (e != cudaSuccess) break;
+        DotPlan plan;
+        if ((st = plan_dot(c->info, c->K, S->buf[slot][0], S->buf[slot][1], std::max<int64_t>(len, 0), &plan)) != GFP_OK)
+            return st;
+        OutSpec o{S->d_partial, (int)rep, (int)dt, ci == 0 ? OUT_PARTIAL : OUT_ACCUMULATE};
+        e = launch_dot(plan, c->K, S->buf[slot][0], S->buf[slot][1], std::max<int64_t>(len, 0), ws, o, s);
+        if (e == cudaSuccess) e = cudaEventRecord(S->consumed[slot], s);
+    }
+    if (e == cudaSuccess) {
+        OutSpec o{S->d_out, (int)rep, (int)dt, OUT_ENCODE};
+        e = launch_finalize(c->K, S->d_partial, 1, o, s);
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, S->d_out, es, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return e == cudaSuccess ? GFP_OK : cuda_fail(e, "gfp_dot_host");
+}
+
+uint64_t gfp_launch_count(int reset) { return launches(reset); }
+
+const char *gfp_status_str(gfp_status s) {
+    switch (s) {
+    case GFP_OK: return "GFP_OK";
+    case GFP_E_INVAL: return "GFP_E_INVAL: invalid argument";
+    case GFP_E_NOT_PRIME: return "GFP_E_NOT_PRIME: modulus is not prime";
+    case GFP_E_BOUND: return "GFP_E_BOUND: modulus outside the representation bound";
+    case GFP_E_UNSUPPORTED: return "GFP_E_UNSUPPORTED: representation/dtype not supported";
+    case GFP_E_CUDA: return "GFP_E_CUDA: CUDA error";
+    case GFP_E_NOMEM: return "GFP_E_NOMEM: allocation failed";
+    }
+    return "unknown gfp_status";
+}
+
+const char *gfp_last_error(void) { return t_err.c_str(); }
+
+void gfp_release_caches(void) {
+    cudaDeviceSynchronize();
+    std::lock_guard<std::mutex> g(g_mu);
+    for (auto &kv : g_ctx) {
+        cudaFree(kv.second->d_antilog);
+        cudaFree(kv.second->d_log);
+        delete kv.second;
+    }
+    g_ctx.clear();
+    for (auto &kv : g_ws) cudaFree(kv.second.partials);
+    g_ws.clear();
+    std::lock_guard<std::mutex> g2(g_stage_mu);
+    for (auto &kv : g_stage) {
+        Staging *S = kv.second;
+        for (auto &row : S->buf)
+            for (void *q : row) cudaFree(q);
+        cudaFree(S->d_partial);
+        cudaFree(S->d_out);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(S->copied[i]);
+            cudaEventDestroy(S->consumed[i]);
+        }
+        cudaStreamDestroy(S->copy);
+        delete S;
+    }
+    g_stage.clear();
+}
+
+const char *gfp_version(void) { return "gfp-b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,266 @@
+// device.cuh -- device-side building blocks for sm_100a: streaming loads, exact reductions, and one
+// accumulation policy per representation of arXiv cs/0404008 sec. 2.
+//
+// A policy R provides
+//   elem, W              element type, elements per 16-byte vector
+//   Acc                  per-thread accumulator state
+//   init(Acc&)           zero
+//   vec(Acc&, x, y, K)   accumulate the W products of two 16-byte vectors
+//   term(Acc&, a, b, K)  accumulate one product (head / tail / unaligned elements)
+//   finish(Acc&, K)      -> uint64 contribution that can be summed across threads without wrap:
+//                          the raw sum when the host proved the grand total fits ("ALL" modes),
+//                          else a residue in [0, p)
+// K is the kernel-constant block (KParams) with p and the precomputed constants of numtheory.cpp.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "params.h"
+
+namespace gfp {
+namespace dev {
+
+
+// ------------------------------------------------------------------------------ memory access
+// 16-byte streaming load: read-only path, no L1 allocation (each byte is used exactly once).
+__device__ __forceinline__ uint4 ld_stream(const void *ptr) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(ptr));
+    return r;
+}
+
+// ------------------------------------------------------------------------------ exact reductions
+// x mod p for any 64-bit x and p < 2^62: q = floor(x * mu / 2^64) is floor(x/p) - {0,1,2}.
+__device__ __forceinline__ uint64_t mod_p(uint64_t x, uint64_t p, uint64_t mu) {
+    uint64_t q = __umul64hi(x, mu);
+    uint64_t r = x - q * p;
+    r = r >= p ? r - p : r;
+    r = r >= p ? r - p : r;
+    return r;
+}
+
+// Montgomery reduction (sec. 2.2) with B = 2^32: U = T n_im mod B, returns (T + U p) / B,
+// which is T B^{-1} mod p up to a multiple of p.  The caller guarantees T + U p < 2^64.
+__device__ __forceinline__ uint32_t redc(uint64_t T, uint32_t p, uint32_t n_im) {
+    uint32_t U = (uint32_t)T * n_im;
+    return (uint32_t)((T + (uint64_t)U * p) >> 32);
+}
+
+// NTL's floating point reduction (sec. 2.3, listing P:112-117): T -= floor(T*invP)*P; one fix-up.
+// Every intermediate is an integer below 2^53, so each step is exact (reading G8).
+__device__ __forceinline__ double ntl_reduce(double T, double P, double invP) {
+    double q = floor(__dmul_rn(T, invP));
+    T = __fma_rn(-q, P, T);
+    if (T >= P)
+        T -= P;
+    else if (T < 0.0)
+        T += P;
+    return T;
+}
+
+// ------------------------------------------------------------------------------ policies
+enum ClassicalMode { CL_ALL = 0, CL_THREAD = 1, CL_OVERFLOW = 2 };
+
+// Classical Z/pZ, u32 storage (sec. 2.1).  Products a*b < 2^64 are added to a u64 with no
+// remainder (AXPY with the remainder delayed, sec. 3.1).  CL_OVERFLOW: the paper's overflow
+// detection trick (sec. 3.3): sum += product; if (sum < product) sum += CORR.
+template <int MODE>
+struct ClassicalU32 {
+    using elem = uint32_t;
+    static constexpr int W = 4;
+    static constexpr bool kTable = false;
+    struct Acc { uint64_t s; };
+    __device__ __forceinline__ static void init(Acc &A) { A.s = 0; }
+    __device__ __forceinline__ static void term(Acc &A, uint32_t x, uint32_t y, const KParams &K,
+                                                const uint16_t * = nullptr) {
+        uint64_t prod = (uint64_t)x * y;
+        if (MODE == CL_OVERFLOW) {
+            uint64_t s = A.s + prod;
+            A.s = s < prod ? s + K.corr : s;
+        } else {
+            A.s += prod;
+        }
+    }
+    __device__ __forceinline__ static void vec(Acc &A, uint4 x, uint4 y, const KParams &K, const uint16_t *) {
+        term(A, x.x, y.x, K);
+        term(A, x.y, y.y, K);
+        term(A, x.z, y.z, K);
+        term(A, x.w, y.w, K);
+    }
+    __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
+        return MODE == CL_ALL ? A.s : mod_p(A.s, K.p, K.mu);
+    }
+};
+
+// Classical Z/pZ, u16 storage (p <= 65521): products < 2^32; CL_ALL or CL_THREAD only.
+template <int MODE>
+struct ClassicalU16 {
+    using elem = uint16_t;
+    static constexpr int W = 8;
+    static constexpr bool kTable = false;
+    struct Acc { uint64_t s; };
+    __device__ __forceinline__ static void init(Acc &A) { A.s = 0; }
+    __device__ __forceinline__ static void term(Acc &A, uint32_t x, uint32_t y, const KParams &,
+                                                const uint16_t * = nullptr) {
+        A.s += (uint64_t)(x * y);
+    }
+    __device__ __forceinline__ static void pair(Acc &A, uint32_t x, uint32_t y) {
+        A.s += (uint64_t)((x & 0xFFFFu) * (y & 0xFFFFu));
+        A.s += (uint64_t)((x >> 16) * (y >> 16));
+    }
+    __device__ __forceinline__ static void vec(Acc &A, uint4 x, uint4 y, const KParams &, const uint16_t *) {
+        pair(A, x.x, y.x);
+        pair(A, x.y, y.y);
+        pair(A, x.z, y.z);
+        pair(A, x.w, y.w);
+    }
+    __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
+        return MODE == CL_ALL ? A.s : mod_p(A.s, K.p, K.mu);
+    }
+};
+
+// Montgomery, B = 2^32 (sec. 2.2 / 3.2.1).  Elements are aB mod p; a product is ab B^2, and KR of
+// them are summed before one REDC (sec. 3.2.1: "the reduction can indeed be delayed").
+// Each REDC output (< 2p) is in B^1 scale and goes into a separate u64 sum S (reading G6), whose
+// residue S mod p is the Montgomery form of the dot.  KR <= the host's mont_k(p).
+template <int KR>
+struct Montgomery {
+    using elem = uint32_t;
+    static constexpr int W = 4;
+    static constexpr bool kTable = false;
+    struct Acc { uint64_t S; };
+    __device__ __forceinline__ static void init(Acc &A) { A.S = 0; }
+    __device__ __forceinline__ static void term(Acc &A, uint32_t x, uint32_t y, const KParams &K,
+                                                const uint16_t * = nullptr) {
+        A.S += redc((uint64_t)x * y, (uint32_t)K.p, K.n_im);
+    }
+    __device__ __forceinline__ static void vec(Acc &A, uint4 x, uint4 y, const KParams &K, const uint16_t *) {
+        const uint32_t p = (uint32_t)K.p;
+        if (KR >= 4) {
+            uint64_t T = (uint64_t)x.x * y.x;
+            T += (uint64_t)x.y * y.y;
+            T += (uint64_t)x.z * y.z;
+            T += (uint64_t)x.w * y.w;
+            A.S += redc(T, p, K.n_im);
+        } else if (KR >= 2) {
+            uint64_t T0 = (uint64_t)x.x * y.x + (uint64_t)x.y * y.y;
+            uint64_t T1 = (uint64_t)x.z * y.z + (uint64_t)x.w * y.w;
+            A.S += redc(T0, p, K.n_im);
+            A.S += redc(T1, p, K.n_im);
+        } else {
+            term(A, x.x, y.x, K);
+            term(A, x.y, y.y, K);
+            term(A, x.z, y.z, K);
+            term(A, x.w, y.w, K);
+        }
+    }
+    __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
+        return mod_p(A.S, K.p, K.mu);
+    }
+};
+
+// Floating point (sec. 2.3 / 3.1).  Exact integers in binary64; products are fused into the
+// accumulator (exact: every value is an integer below 2^53) and NTL's reduction runs every
+// KF terms, KF <= k of Eq. (1) at m = 53.  KF = 0: no reduction until the end of the thread
+// (the host proved the thread's whole sum stays below 2^53).
+template <int KF>
+struct Fp64 {
+    using elem = double;
+    static constexpr int W = 2;
+    static constexpr bool kTable = false;
+    struct Acc { double T; };
+    __device__ __forceinline__ static void init(Acc &A) { A.T = 0.0; }
+    __device__ __forceinline__ static void term(Acc &A, double x, double y, const KParams &K,
+                                                const uint16_t * = nullptr) {
+        A.T = __fma_rn(x, y, A.T);
+        if (KF != 0) A.T = ntl_reduce(A.T, K.pd, K.inv_p);
+    }
+    __device__ __forceinline__ static void vec(Acc &A, uint4 xv, uint4 yv, const KParams &K, const uint16_t *) {
+        const double x0 = __hiloint2double(xv.y, xv.x), x1 = __hiloint2double(xv.w, xv.z);
+        const double y0 = __hiloint2double(yv.y, yv.x), y1 = __hiloint2double(yv.w, yv.z);
+        if (KF == 1) {
+            term(A, x0, y0, K);
+            term(A, x1, y1, K);
+        } else {
+            A.T = __fma_rn(x0, y0, A.T);
+            A.T = __fma_rn(x1, y1, A.T);
+            if (KF != 0) A.T = ntl_reduce(A.T, K.pd, K.inv_p);
+        }
+    }
+    __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
+        double T = KF == 0 ? ntl_reduce(A.T, K.pd, K.inv_p) : A.T;
+        return (uint64_t)T;
+    }
+};
+
+// Discrete logarithms (sec. 2.4).  The product of g^i and g^j is g^(i+j): one index addition
+// (Table 1 row 1) and one antilog lookup in shared memory gives its classical value
+// (< p), which is summed in an integer register with the remainder delayed (reading G11).
+// Zero operands (code 0) map the index to the zero sentinel (reading G13).
+//   SMALL (2(q-1) <= 65534): index i + j needs no "- qbar" correction; 65536-entry table.
+//   LARGE: index folded once by qbar (Table 1's "(- qbar)"), clamped; p-entry table.
+// ALL: the grand total fits u64 (host-checked); else each thread reduces its sum.
+template <bool SMALL, bool ALL>
+struct Zech {
+    using elem = uint16_t;
+    static constexpr int W = 8;
+    static constexpr bool kTable = true;
+    struct Acc { uint64_t s; };
+    __device__ __forceinline__ static void init(Acc &A) { A.s = 0; }
+    __device__ __forceinline__ static uint32_t index(uint32_t i, uint32_t j, uint32_t qbar) {
+        if (SMALL) {
+            return (i == 0 || j == 0) ? 0xFFFFu : i + j;
+        } else {
+            uint32_t s = i + j;
+            s = s > qbar ? s - qbar : s;
+            s = s > qbar ? qbar : s;  // non-canonical codes stay inside the table
+            return (i == 0 || j == 0) ? 0u : s;
+        }
+    }
+    __device__ __forceinline__ static uint32_t lookup(uint32_t i, uint32_t j, const KParams &K,
+                                                      const uint16_t *tab) {
+        return tab[index(i, j, K.qbar)];
+    }
+    __device__ __forceinline__ static void term(Acc &A, uint32_t i, uint32_t j, const KParams &K,
+                                                const uint16_t *tab) {
+        A.s += lookup(i, j, K, tab);
+    }
+    __device__ __forceinline__ static uint32_t pair(uint32_t x, uint32_t y, const KParams &K, const uint16_t *tab) {
+        return lookup(x & 0xFFFFu, y & 0xFFFFu, K, tab) + lookup(x >> 16, y >> 16, K, tab);
+    }
+    __device__ __forceinline__ static void vec(Acc &A, uint4 x, uint4 y, const KParams &K, const uint16_t *tab) {
+        uint32_t s = pair(x.x, y.x, K, tab) + pair(x.y, y.y, K, tab) + pair(x.z, y.z, K, tab) +
+                     pair(x.w, y.w, K, tab);  // 8 values < 2^16: no wrap in 32 bits
+        A.s += s;
+    }
+    __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
+        return ALL ? A.s : mod_p(A.s, K.p, K.mu);
+    }
+};
+
+// ------------------------------------------------------------------------------ combination
+__device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+
+// Sum over the CTA; the result is valid in thread 0.  `red` holds >= 32 entries.
+__device__ __forceinline__ uint64_t block_sum(uint64_t v, uint64_t *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_sum(v);
+    __syncthreads();  // `red` may still be read by a previous call
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    v = 0;
+    if (warp == 0) {
+        v = lane < nw ? red[lane] : 0;
+        v = warp_sum(v);
+    }
+    return v;
+}
+
+}  // namespace dev
+}  // namespace gfp

@@ -1,0 +1,52 @@
+// internal.h -- interface between the C ABI (api.cpp) and the kernel launchers (kernels.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "params.h"
+#include "gfp.h"
+
+namespace gfp {
+
+// Per-(device, stream) scratch for the single-launch combine: per-CTA partials and the
+// last-CTA-done counter (self-resetting, so no memset per call).
+struct Workspace {
+    uint64_t *partials;
+    unsigned int *counter;
+};
+
+// Where the final residue goes.
+enum OutMode { OUT_ENCODE = 0, OUT_PARTIAL = 1, OUT_ACCUMULATE = 2 };
+struct OutSpec {
+    void *out;          // OUT_ENCODE: element of (rep, dtype); else uint64_t*
+    int rep, dtype, mode;
+};
+
+constexpr int kMaxGrid = 4096;
+
+// Kernel variant selected on the host from the bounds.
+struct DotPlan {
+    int policy;     // enumerated in kernels.cu
+    int grid, block;
+    size_t smem;
+    int64_t head;   // scalar elements before the first 16-byte aligned vector (== n if unaligned)
+    int acc;        // gfp_acc reported for the plan
+};
+
+// Build a plan: chooses grid, the accumulation policy and its mode for n elements.
+gfp_status plan_dot(const gfp_info &info, const dev::KParams &K, const void *a, const void *b, int64_t n,
+                    DotPlan *plan);
+cudaError_t launch_dot(const DotPlan &plan, const dev::KParams &K, const void *a, const void *b, int64_t n,
+                       Workspace ws, OutSpec out, cudaStream_t s);
+cudaError_t launch_finalize(const dev::KParams &K, const uint64_t *summed, int count, OutSpec out,
+                            cudaStream_t s);
+gfp_status launch_batch(const gfp_info &info, const dev::KParams &K, const void *A, int64_t lda, const void *x,
+                        int64_t rows, int64_t n, OutSpec out, cudaStream_t s, cudaError_t *err);
+// dir: 0 = to_rep, 1 = from_rep
+gfp_status launch_convert(const gfp_info &info, const dev::KParams &K, int dir, gfp_dtype in_dt, const void *in,
+                          gfp_dtype out_dt, void *out, int64_t n, cudaStream_t s, cudaError_t *err);
+
+int num_sms(int device);
+void count_launch();
+
+}  // namespace gfp

@@ -1,0 +1,646 @@
+// kernels.cu -- the hot-path kernels for sm_100a and their launchers.
+//
+//   dot_kernel      single dot product: persistent grid-stride streaming of both operands with
+//                   16-byte loads, per-thread delayed-modulus accumulation (policy R, device.cuh),
+//                   warp-shuffle + CTA tree, per-CTA partial, last-CTA-done final reduction and
+//                   encoding -- one launch per dot.
+//   batch_cl16      C5 matrix-vector over classical u16: warp per row, x byte-split in shared
+//                   memory, two DP2A per pair of terms (a8).
+//   batch_kernel    generic batch (any policy): warp per row.
+//   convert_kernel  representation conversions (a2).
+//   finalize_kernel sum of partial residues -> mod p -> encode (a7/a9).
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "device.cuh"
+#include "internal.h"
+#include "numtheory.h"
+
+namespace gfp {
+
+using namespace dev;
+
+enum Policy {
+    P_CL32_ALL, P_CL32_THREAD, P_CL32_OVF,
+    P_CL16_ALL, P_CL16_THREAD,
+    P_MONT1, P_MONT2, P_MONT4,
+    P_FP_THREAD, P_FP_K1, P_FP_K2,
+    P_ZS_ALL, P_ZS_THREAD, P_ZL_ALL, P_ZL_THREAD,
+    P_COUNT
+};
+
+static thread_local uint64_t t_launches = 0;
+void count_launch() { ++t_launches; }
+uint64_t launches(int reset) {
+    uint64_t v = t_launches;
+    if (reset) t_launches = 0;
+    return v;
+}
+
+int num_sms(int device) {
+    static std::mutex mu;
+    static std::unordered_map<int, int> cache;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(device);
+    if (it != cache.end()) return it->second;
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0) v = 148;
+    cache[device] = v;
+    return v;
+}
+
+// ------------------------------------------------------------------------------ output encoding
+__device__ __forceinline__ void write_result(uint64_t r, const OutSpec &O, const KParams &K, int64_t idx) {
+    if (O.mode == OUT_PARTIAL) {
+        ((uint64_t *)O.out)[idx] = r;
+        return;
+    }
+    if (O.mode == OUT_ACCUMULATE) {
+        ((uint64_t *)O.out)[idx] += r;  // single writer, stream-ordered
+        return;
+    }
+    switch (O.rep) {
+    case GFP_REP_FP64:
+        ((double *)O.out)[idx] = (double)r;  // exact, never -0.0
+        break;
+    case GFP_REP_ZECH:
+        ((uint16_t *)O.out)[idx] = r == 0 ? (uint16_t)0 : K.logt[r];
+        break;
+    default:  // classical residue, or Montgomery form (the sum of aB-forms is the aB-form)
+        if (O.dtype == GFP_U16)
+            ((uint16_t *)O.out)[idx] = (uint16_t)r;
+        else
+            ((uint32_t *)O.out)[idx] = (uint32_t)r;
+    }
+}
+
+// Stage a u16 table (entries padded to a multiple of 8) from global into shared memory.
+__device__ __forceinline__ void stage_table(uint16_t *dst, const uint16_t *src, uint32_t entries) {
+    const uint4 *s = reinterpret_cast<const uint4 *>(src);
+    uint4 *d = reinterpret_cast<uint4 *>(dst);
+    for (uint32_t i = threadIdx.x; i < entries / 8; i += blockDim.x) d[i] = __ldg(s + i);
+}
+
+// ------------------------------------------------------------------------------ single dot
+template <class R, int NT, int U>
+__global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restrict__ a,
+                                                 const typename R::elem *__restrict__ b, int64_t n,
+                                                 int64_t head, KParams K, Workspace ws, OutSpec O) {
+    extern __shared__ __align__(16) uint16_t s_tab[];
+    __shared__ uint64_t red[32];
+    __shared__ int s_last;
+    const uint16_t *tab = nullptr;
+    if constexpr (R::kTable) {
+        stage_table(s_tab, K.antilog, K.antilog_entries);
+        __syncthreads();
+        tab = s_tab;
+    }
+    typename R::Acc acc;
+    R::init(acc);
+    const int64_t gtid = (int64_t)blockIdx.x * NT + threadIdx.x;
+    const int64_t gstride = (int64_t)gridDim.x * NT;
+
+    // scalar head (the whole input when a and b are not co-aligned)
+    for (int64_t i = gtid; i < head; i += gstride) R::term(acc, a[i], b[i], K, tab);
+
+    // 16-byte vector body: U independent loads of each operand in flight per thread
+    const int64_t nvec = (n - head) / R::W;
+    const uint4 *av = reinterpret_cast<const uint4 *>(a + head);
+    const uint4 *bv = reinterpret_cast<const uint4 *>(b + head);
+    int64_t i0 = (int64_t)blockIdx.x * (NT * U) + threadIdx.x;
+    const int64_t step = (int64_t)gridDim.x * (NT * U);
+    for (; i0 + (U - 1) * NT < nvec; i0 += step) {
+        uint4 xa[U], xb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            xa[u] = ld_stream(av + i0 + u * NT);
+            xb[u] = ld_stream(bv + i0 + u * NT);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) R::vec(acc, xa[u], xb[u], K, tab);
+    }
+    if (i0 < nvec) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u * NT < nvec) R::vec(acc, ld_stream(av + i0 + u * NT), ld_stream(bv + i0 + u * NT), K, tab);
+    }
+    // scalar tail (< W elements)
+    for (int64_t i = head + nvec * R::W + gtid; i < n; i += gstride) R::term(acc, a[i], b[i], K, tab);
+
+    // combine: warp shuffle -> CTA tree -> per-CTA partial -> last CTA reduces and encodes
+    uint64_t v = block_sum(R::finish(acc, K), red);
+    if (threadIdx.x == 0) {
+        ws.partials[blockIdx.x] = v;
+        __threadfence();
+        unsigned int t = atomicAdd(ws.counter, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    uint64_t s = 0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) s += (uint64_t)__ldcg(reinterpret_cast<const unsigned long long *>(ws.partials + i));
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) {
+        write_result(mod_p(s, K.p, K.mu), O, K, 0);  // "A single machine remaindering ... at the end"
+        *ws.counter = 0;
+    }
+}
+
+// ------------------------------------------------------------------------------ finalize
+__global__ void finalize_kernel(const uint64_t *summed, int count, KParams K, OutSpec O) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint64_t r = 0;
+    for (int i = 0; i < count; ++i) r = mod_p(r + mod_p(summed[i], K.p, K.mu), K.p, K.mu);
+    write_result(r, O, K, 0);
+}
+
+// ------------------------------------------------------------------------------ batch: C5 fast path
+// Classical u16, p <= 65521.  A row r is A[r*lda .. +n); x is staged once per CTA into shared
+// memory as byte-split words w_j = (x_{2j} lo, x_{2j+1} lo, x_{2j} hi, x_{2j+1} hi), so that for a
+// packed pair of A entries  dp2a_lo(A2, w) = a0 x0_lo + a1 x1_lo  and  dp2a_hi(A2, w) = a0 x0_hi + a1 x1_hi,
+// each < 2^25.  Row value = sum lo + 256 * sum hi, accumulated in u64 per lane (no reduction, the
+// row total n (p-1)^2 < 2^64 is host-checked; Eq. (1)), then one mod p per row.
+template <int NT, int U>
+__global__ void __launch_bounds__(NT) batch_cl16_kernel(const uint16_t *__restrict__ A, int64_t lda,
+                                                        const uint16_t *__restrict__ x, int64_t rows, int64_t n,
+                                                        KParams K, OutSpec O) {
+    extern __shared__ __align__(16) uint32_t s_xw[];
+    const int64_t nw = (n + 1) / 2;
+    const int64_t nwpad = (nw + 3) & ~int64_t(3);
+    for (int64_t j = threadIdx.x; j < nwpad; j += NT) {
+        uint32_t x0 = 2 * j < n ? x[2 * j] : 0u, x1 = 2 * j + 1 < n ? x[2 * j + 1] : 0u;
+        s_xw[j] = (x0 & 0xFFu) | ((x1 & 0xFFu) << 8) | ((x0 >> 8) << 16) | ((x1 >> 8) << 24);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nvec = n / 8;
+    const uint4 *xv = reinterpret_cast<const uint4 *>(s_xw);
+    for (int64_t row = (int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); row < rows;
+         row += (int64_t)gridDim.x * (NT / 32)) {
+        const uint16_t *Ar = A + row * lda;
+        const uint4 *av = reinterpret_cast<const uint4 *>(Ar);
+        uint64_t tot = 0;
+        for (int64_t v0 = lane; v0 < nvec; v0 += 32 * U) {
+            uint4 ra[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                ra[u] = v0 + u * 32 < nvec ? ld_stream(av + v0 + u * 32) : make_uint4(0, 0, 0, 0);
+            uint32_t lo = 0, hi = 0;  // <= 4U dp2a of < 2^25 each: no wrap for U <= 32
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint4 w = xv[v0 + u * 32 < nvec ? v0 + u * 32 : 0];
+                lo = __dp2a_lo(ra[u].x, w.x, lo);
+                hi = __dp2a_hi(ra[u].x, w.x, hi);
+                lo = __dp2a_lo(ra[u].y, w.y, lo);
+                hi = __dp2a_hi(ra[u].y, w.y, hi);
+                lo = __dp2a_lo(ra[u].z, w.z, lo);
+                hi = __dp2a_hi(ra[u].z, w.z, hi);
+                lo = __dp2a_lo(ra[u].w, w.w, lo);
+                hi = __dp2a_hi(ra[u].w, w.w, hi);
+            }
+            tot += (uint64_t)lo + ((uint64_t)hi << 8);
+        }
+        for (int64_t j = nvec * 8 + lane; j < n; j += 32) tot += (uint64_t)Ar[j] * x[j];
+        tot = warp_sum(tot);
+        if (lane == 0) write_result(mod_p(tot, K.p, K.mu), O, K, row);
+    }
+}
+
+// ------------------------------------------------------------------------------ batch: generic
+// Warp per row with policy R.  x read through the read-only path (L1-resident, reused by every
+// row).  VEC: rows and x are 16-byte aligned (A, lda*sizeof, x) -> 16-byte loads.
+template <class R, int NT, int U, bool VEC>
+__global__ void __launch_bounds__(NT) batch_kernel(const typename R::elem *__restrict__ A, int64_t lda,
+                                                   const typename R::elem *__restrict__ x, int64_t rows,
+                                                   int64_t n, KParams K, OutSpec O) {
+    extern __shared__ __align__(16) uint16_t s_tab[];
+    const uint16_t *tab = nullptr;
+    if constexpr (R::kTable) {
+        stage_table(s_tab, K.antilog, K.antilog_entries);
+        __syncthreads();
+        tab = s_tab;
+    }
+    const int lane = threadIdx.x & 31;
+    for (int64_t row = (int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); row < rows;
+         row += (int64_t)gridDim.x * (NT / 32)) {
+        const typename R::elem *Ar = A + row * lda;
+        typename R::Acc acc;
+        R::init(acc);
+        int64_t done = 0;
+        if (VEC) {
+            const int64_t nvec = n / R::W;
+            const uint4 *av = reinterpret_cast<const uint4 *>(Ar);
+            const uint4 *xv = reinterpret_cast<const uint4 *>(x);
+            for (int64_t v0 = lane; v0 < nvec; v0 += 32 * U) {
+                uint4 ra[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    ra[u] = v0 + u * 32 < nvec ? ld_stream(av + v0 + u * 32) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (v0 + u * 32 < nvec) R::vec(acc, ra[u], __ldg(xv + v0 + u * 32), K, tab);
+            }
+            done = nvec * R::W;
+        }
+        for (int64_t j = done + lane; j < n; j += 32) R::term(acc, Ar[j], x[j], K, tab);
+        uint64_t v = warp_sum(R::finish(acc, K));
+        if (lane == 0) write_result(mod_p(v, K.p, K.mu), O, K, row);
+    }
+}
+
+// ------------------------------------------------------------------------------ conversions
+enum ConvOp { C_TO_MONT, C_FROM_MONT, C_TO_ZECH, C_FROM_ZECH_SMALL, C_FROM_ZECH_LARGE, C_CAST };
+
+template <int OP, typename TI, typename TO>
+__device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab) {
+    if constexpr (OP == C_TO_MONT) {
+        // a -> aB mod p = REDC(a * (B^2 mod p)) (sec. 2.2); T < p^2 <= pB
+        uint32_t r = redc((uint64_t)(uint32_t)v * K.r2, (uint32_t)K.p, K.n_im);
+        return (TO)(r >= K.p ? r - (uint32_t)K.p : r);
+    } else if constexpr (OP == C_FROM_MONT) {
+        uint32_t r = redc((uint64_t)(uint32_t)v, (uint32_t)K.p, K.n_im);  // T < p: result <= p
+        return (TO)(r >= K.p ? r - (uint32_t)K.p : r);
+    } else if constexpr (OP == C_TO_ZECH) {
+        uint64_t e = (uint64_t)v;
+        return (TO)tab[e < K.p ? e : K.p - 1];  // log table; log[0] = 0
+    } else if constexpr (OP == C_FROM_ZECH_SMALL) {
+        uint32_t c = (uint32_t)v;
+        return (TO)(c == 0 ? 0u : (uint32_t)tab[c]);  // antilog[c] = g^c, c <= 65535 in range
+    } else if constexpr (OP == C_FROM_ZECH_LARGE) {
+        uint32_t c = (uint32_t)v;
+        return (TO)tab[c <= K.qbar ? c : K.qbar];  // antilog[0] = 0 sentinel
+    } else {
+        return (TO)v;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void load8(const T *p, T (&v)[8]) {
+    constexpr int NV = 8 * sizeof(T) / 16;
+    uint4 r[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) r[i] = __ldcs(reinterpret_cast<const uint4 *>(p) + i);
+    memcpy(v, r, sizeof(v));
+}
+template <typename T>
+__device__ __forceinline__ void store8(T *p, const T (&v)[8]) {
+    constexpr int NV = 8 * sizeof(T) / 16;
+    uint4 r[NV];
+    memcpy(r, v, sizeof(v));
+#pragma unroll
+    for (int i = 0; i < NV; ++i) __stcs(reinterpret_cast<uint4 *>(p) + i, r[i]);
+}
+
+template <int OP, typename TI, typename TO, int NT>
+__global__ void __launch_bounds__(NT) convert_kernel(const TI *in, TO *out, int64_t n, bool vec_ok, KParams K,
+                                                     const uint16_t *table, uint32_t table_entries) {
+    extern __shared__ __align__(16) uint16_t s_tab[];
+    const uint16_t *tab = nullptr;
+    if (table != nullptr) {
+        stage_table(s_tab, table, table_entries);
+        __syncthreads();
+        tab = s_tab;
+    }
+    const int64_t gtid = (int64_t)blockIdx.x * NT + threadIdx.x, gstride = (int64_t)gridDim.x * NT;
+    int64_t done = 0;
+    if (vec_ok) {
+        const int64_t nchunk = n / 8;
+        for (int64_t c = gtid; c < nchunk; c += gstride) {
+            TI v[8];
+            TO w[8];
+            load8(in + 8 * c, v);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = conv1<OP, TI, TO>(v[i], K, tab);
+            store8(out + 8 * c, w);
+        }
+        done = nchunk * 8;
+    }
+    for (int64_t i = done + gtid; i < n; i += gstride) out[i] = conv1<OP, TI, TO>(in[i], K, tab);
+}
+
+// ------------------------------------------------------------------------------ launch helpers
+template <typename F>
+static int occupancy(F kernel, int block, size_t smem) {
+    static std::mutex mu;
+    static std::unordered_map<std::string, int> cache;  // per (kernel, dynamic smem)
+    std::lock_guard<std::mutex> g(mu);
+    const std::string key = std::to_string((uintptr_t)reinterpret_cast<const void *>(kernel)) + ":" +
+                            std::to_string(smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int bps = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, block, smem) != cudaSuccess || bps < 1) bps = 1;
+    cache[key] = bps;
+    return bps;
+}
+
+constexpr int kDotNT = 256, kDotU = 4, kZechNT = 1024, kZechU = 2;
+
+template <class R, int NT, int U>
+static cudaError_t launch_dot_t(const DotPlan &P, const KParams &K, const void *a, const void *b, int64_t n,
+                                Workspace ws, OutSpec O, cudaStream_t s) {
+    auto kern = dot_kernel<R, NT, U>;
+    occupancy(kern, NT, P.smem);  // sets the smem attribute once
+    kern<<<P.grid, NT, P.smem, s>>>((const typename R::elem *)a, (const typename R::elem *)b, n, P.head, K, ws, O);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <class R, int NT, int U>
+static int dot_occupancy(size_t smem) {
+    return occupancy(dot_kernel<R, NT, U>, NT, smem);
+}
+
+static int policy_block(int pol) { return pol >= P_ZS_ALL ? kZechNT : kDotNT; }
+static int policy_unroll(int pol) { return pol >= P_ZS_ALL ? kZechU : kDotU; }
+static int policy_width(int pol) {
+    if (pol <= P_CL32_OVF || (pol >= P_MONT1 && pol <= P_MONT4)) return 4;
+    if (pol >= P_FP_THREAD && pol <= P_FP_K2) return 2;
+    return 8;
+}
+
+static int policy_occupancy(int pol, size_t smem) {
+    switch (pol) {
+    case P_CL32_ALL: return dot_occupancy<ClassicalU32<CL_ALL>, kDotNT, kDotU>(smem);
+    case P_CL32_THREAD: return dot_occupancy<ClassicalU32<CL_THREAD>, kDotNT, kDotU>(smem);
+    case P_CL32_OVF: return dot_occupancy<ClassicalU32<CL_OVERFLOW>, kDotNT, kDotU>(smem);
+    case P_CL16_ALL: return dot_occupancy<ClassicalU16<CL_ALL>, kDotNT, kDotU>(smem);
+    case P_CL16_THREAD: return dot_occupancy<ClassicalU16<CL_THREAD>, kDotNT, kDotU>(smem);
+    case P_MONT1: return dot_occupancy<Montgomery<1>, kDotNT, kDotU>(smem);
+    case P_MONT2: return dot_occupancy<Montgomery<2>, kDotNT, kDotU>(smem);
+    case P_MONT4: return dot_occupancy<Montgomery<4>, kDotNT, kDotU>(smem);
+    case P_FP_THREAD: return dot_occupancy<Fp64<0>, kDotNT, kDotU>(smem);
+    case P_FP_K1: return dot_occupancy<Fp64<1>, kDotNT, kDotU>(smem);
+    case P_FP_K2: return dot_occupancy<Fp64<2>, kDotNT, kDotU>(smem);
+    case P_ZS_ALL: return dot_occupancy<Zech<true, true>, kZechNT, kZechU>(smem);
+    case P_ZS_THREAD: return dot_occupancy<Zech<true, false>, kZechNT, kZechU>(smem);
+    case P_ZL_ALL: return dot_occupancy<Zech<false, true>, kZechNT, kZechU>(smem);
+    case P_ZL_THREAD: return dot_occupancy<Zech<false, false>, kZechNT, kZechU>(smem);
+    }
+    return 1;
+}
+
+cudaError_t launch_dot(const DotPlan &P, const KParams &K, const void *a, const void *b, int64_t n, Workspace ws,
+                       OutSpec O, cudaStream_t s) {
+    switch (P.policy) {
+    case P_CL32_ALL: return launch_dot_t<ClassicalU32<CL_ALL>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
+    case P_CL32_THREAD: return launch_dot_t<ClassicalU32<CL_THREAD>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
+    case P_CL32_OVF: return launch_dot_t<ClassicalU32<CL_OVERFLOW>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
+    case P_CL16_ALL: return launch_dot_t<ClassicalU16<CL_ALL>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
+    case P_CL16_THREAD: return launch_dot_t<ClassicalU16<CL_THREAD>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
+    case P_MONT1: return launch_dot_t<Montgomery<1>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
+    case P_MONT2: return launch_dot_t<Montgomery<2>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
+    case P_MONT4: return launch_dot_t<Montgomery<4>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
+    case P_FP_THREAD: return launch_dot_t<Fp64<0>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
+    case P_FP_K1: return launch_dot_t<Fp64<1>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
+    case P_FP_K2: return launch_dot_t<Fp64<2>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
+    case P_ZS_ALL: return launch_dot_t<Zech<true, true>, kZechNT, kZechU>(P, K, a, b, n, ws, O, s);
+    case P_ZS_THREAD: return launch_dot_t<Zech<true, false>, kZechNT, kZechU>(P, K, a, b, n, ws, O, s);
+    case P_ZL_ALL: return launch_dot_t<Zech<false, true>, kZechNT, kZechU>(P, K, a, b, n, ws, O, s);
+    case P_ZL_THREAD: return launch_dot_t<Zech<false, false>, kZechNT, kZechU>(P, K, a, b, n, ws, O, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+static size_t elem_size(int dt) { return dt == GFP_U16 ? 2 : (dt == GFP_U32 ? 4 : 8); }
+
+gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const void *b, int64_t n, DotPlan *P) {
+    const size_t es = elem_size(I.dtype);
+    const uint64_t pm1 = I.p - 1;
+    const u128 q2 = (u128)pm1 * pm1;
+    const u128 max64 = ~(u128)0 >> 64;
+    const size_t smem = I.rep == GFP_REP_ZECH ? (size_t)K.antilog_entries * 2 : 0;
+
+    // provisional policy (the mode refinement below only depends on per-thread counts)
+    int pol = 0;
+    switch (I.rep) {
+    case GFP_REP_CLASSICAL: pol = I.dtype == GFP_U16 ? P_CL16_THREAD : P_CL32_THREAD; break;
+    case GFP_REP_MONTGOMERY: pol = I.mont_kr >= 4 ? P_MONT4 : (I.mont_kr >= 2 ? P_MONT2 : P_MONT1); break;
+    case GFP_REP_FP64: pol = I.k >= 2 ? P_FP_K2 : P_FP_K1; break;
+    case GFP_REP_ZECH: pol = zech_small_layout(I.p) ? P_ZS_ALL : P_ZL_ALL; break;
+    }
+    const int NT = policy_block(pol), U = policy_unroll(pol), W = policy_width(pol);
+    const uintptr_t pa = (uintptr_t)a, pb = (uintptr_t)b;
+    int64_t head = n;
+    if (pa % 16 == pb % 16) head = std::min<int64_t>(n, (int64_t)(((16 - pa % 16) % 16) / es));
+    const int64_t nvec = (n - head) / W;
+    const int dev_sms = [] {
+        int d = 0;
+        cudaGetDevice(&d);
+        return num_sms(d);
+    }();
+    const int bps = policy_occupancy(pol, smem);
+    int64_t want = std::max<int64_t>((nvec + (int64_t)NT * U - 1) / ((int64_t)NT * U), (head + NT - 1) / NT);
+    int64_t grid = std::min<int64_t>({(int64_t)dev_sms * bps, std::max<int64_t>(want, 1), (int64_t)kMaxGrid});
+    const int64_t threads = grid * NT;
+    const int64_t iters = (nvec + threads * U - 1) / (threads * U);
+    const u128 per_thread = (u128)iters * U * W + (head + threads - 1) / threads + 1;
+
+    int acc = GFP_ACC_DELAYED;
+    switch (I.rep) {
+    case GFP_REP_CLASSICAL:
+        if ((u128)n * q2 <= max64)
+            pol = I.dtype == GFP_U16 ? P_CL16_ALL : P_CL32_ALL;  // Eq. (1): k > n, one final remainder
+        else if (per_thread * q2 <= max64)
+            pol = I.dtype == GFP_U16 ? P_CL16_THREAD : P_CL32_THREAD;
+        else {
+            pol = P_CL32_OVF;  // sec. 3.3 overflow detection (u16 products never need it)
+            acc = GFP_ACC_OVERFLOW;
+        }
+        break;
+    case GFP_REP_MONTGOMERY:
+        acc = GFP_ACC_BLOCKED;
+        break;
+    case GFP_REP_FP64:
+        if (per_thread * q2 < ((u128)1 << 53))
+            pol = P_FP_THREAD;
+        else
+            acc = GFP_ACC_BLOCKED;
+        break;
+    case GFP_REP_ZECH: {
+        const bool small = zech_small_layout(I.p);
+        if ((u128)n * pm1 <= max64)
+            pol = small ? P_ZS_ALL : P_ZL_ALL;
+        else
+            pol = small ? P_ZS_THREAD : P_ZL_THREAD;
+        break;
+    }
+    }
+    P->policy = pol;
+    P->grid = (int)grid;
+    P->block = NT;
+    P->smem = smem;
+    P->head = head;
+    P->acc = acc;
+    return GFP_OK;
+}
+
+cudaError_t launch_finalize(const KParams &K, const uint64_t *summed, int count, OutSpec O, cudaStream_t s) {
+    finalize_kernel<<<1, 32, 0, s>>>(summed, count, K, O);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ batch launch
+template <class R, int NT, int U>
+static cudaError_t launch_batch_t(const KParams &K, const void *A, int64_t lda, const void *x, int64_t rows,
+                                  int64_t n, bool vec, OutSpec O, cudaStream_t s) {
+    using E = typename R::elem;
+    const size_t smem = R::kTable ? (size_t)K.antilog_entries * 2 : 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int64_t wpb = NT / 32;
+    if (vec) {
+        auto kern = batch_kernel<R, NT, U, true>;
+        int bps = occupancy(kern, NT, smem);
+        int64_t grid = std::min<int64_t>((rows + wpb - 1) / wpb, (int64_t)num_sms(dev) * bps);
+        kern<<<(int)std::max<int64_t>(grid, 1), NT, smem, s>>>((const E *)A, lda, (const E *)x, rows, n, K, O);
+    } else {
+        auto kern = batch_kernel<R, NT, U, false>;
+        int bps = occupancy(kern, NT, smem);
+        int64_t grid = std::min<int64_t>((rows + wpb - 1) / wpb, (int64_t)num_sms(dev) * bps);
+        kern<<<(int)std::max<int64_t>(grid, 1), NT, smem, s>>>((const E *)A, lda, (const E *)x, rows, n, K, O);
+    }
+    count_launch();
+    return cudaGetLastError();
+}
+
+gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int64_t lda, const void *x, int64_t rows,
+                        int64_t n, OutSpec O, cudaStream_t s, cudaError_t *err) {
+    const size_t es = elem_size(I.dtype);
+    const bool vec = ((uintptr_t)A % 16 == 0) && ((uintptr_t)x % 16 == 0) && ((lda * (int64_t)es) % 16 == 0);
+    const uint64_t pm1 = I.p - 1;
+    const u128 q2 = (u128)pm1 * pm1, max64 = ~(u128)0 >> 64;
+    const u128 per_lane = (u128)(n + 31) / 32 + 16;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    *err = cudaSuccess;
+    switch (I.rep) {
+    case GFP_REP_CLASSICAL:
+        if (I.dtype == GFP_U16) {
+            if (vec && (u128)n * q2 <= max64 && n <= 96 * 1024) {
+                constexpr int NT = 256, U = 8;
+                auto kern = batch_cl16_kernel<NT, U>;
+                const size_t smem = (size_t)(((n + 1) / 2 + 3) & ~int64_t(3)) * 4;
+                int bps = occupancy(kern, NT, smem);
+                int64_t grid = std::min<int64_t>((rows + NT / 32 - 1) / (NT / 32), (int64_t)num_sms(dev) * bps);
+                kern<<<(int)std::max<int64_t>(grid, 1), NT, smem, s>>>((const uint16_t *)A, lda, (const uint16_t *)x,
+                                                                       rows, n, K, O);
+                count_launch();
+                *err = cudaGetLastError();
+            } else if (per_lane * q2 <= max64) {
+                *err = (u128)n * q2 <= max64
+                           ? launch_batch_t<ClassicalU16<CL_ALL>, 256, 4>(K, A, lda, x, rows, n, vec, O, s)
+                           : launch_batch_t<ClassicalU16<CL_THREAD>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+            } else {
+                return GFP_E_UNSUPPORTED;
+            }
+        } else {
+            if ((u128)n * q2 <= max64)
+                *err = launch_batch_t<ClassicalU32<CL_ALL>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+            else if (per_lane * q2 <= max64)
+                *err = launch_batch_t<ClassicalU32<CL_THREAD>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+            else
+                *err = launch_batch_t<ClassicalU32<CL_OVERFLOW>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+        }
+        break;
+    case GFP_REP_MONTGOMERY:
+        if (I.mont_kr >= 4)
+            *err = launch_batch_t<Montgomery<4>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+        else if (I.mont_kr >= 2)
+            *err = launch_batch_t<Montgomery<2>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+        else
+            *err = launch_batch_t<Montgomery<1>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+        break;
+    case GFP_REP_FP64:
+        if (per_lane * q2 < ((u128)1 << 53))
+            *err = launch_batch_t<Fp64<0>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+        else if (I.k >= 2)
+            *err = launch_batch_t<Fp64<2>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+        else
+            *err = launch_batch_t<Fp64<1>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+        break;
+    case GFP_REP_ZECH:
+        if (zech_small_layout(I.p))
+            *err = launch_batch_t<Zech<true, false>, 1024, 2>(K, A, lda, x, rows, n, vec, O, s);
+        else
+            *err = launch_batch_t<Zech<false, false>, 1024, 2>(K, A, lda, x, rows, n, vec, O, s);
+        break;
+    }
+    return *err == cudaSuccess ? GFP_OK : GFP_E_CUDA;
+}
+
+// ------------------------------------------------------------------------------ conversion launch
+template <int OP, typename TI, typename TO>
+static cudaError_t launch_conv_t(const KParams &K, const void *in, void *out, int64_t n, const uint16_t *table,
+                                 uint32_t entries, cudaStream_t s) {
+    constexpr int NT = 256;
+    const size_t smem = table ? (size_t)entries * 2 : 0;
+    auto kern = convert_kernel<OP, TI, TO, NT>;
+    int bps = occupancy(kern, NT, smem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const bool vec = ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0);
+    int64_t want = (n / 8 + NT - 1) / NT + 1;
+    int64_t grid = std::min<int64_t>(std::max<int64_t>(want, 1), (int64_t)num_sms(dev) * bps);
+    kern<<<(int)grid, NT, smem, s>>>((const TI *)in, (TO *)out, n, vec, K, table, entries);
+    count_launch();
+    return cudaGetLastError();
+}
+
+gfp_status launch_convert(const gfp_info &I, const KParams &K, int dir, gfp_dtype in_dt, const void *in,
+                          gfp_dtype out_dt, void *out, int64_t n, cudaStream_t s, cudaError_t *err) {
+    // residues side must be integer; representation side must be the rep's dtype
+    const gfp_dtype res_dt = dir == 0 ? in_dt : out_dt, rep_dt = dir == 0 ? out_dt : in_dt;
+    if (res_dt == GFP_F64 || rep_dt != (gfp_dtype)I.dtype) return GFP_E_UNSUPPORTED;
+    if (res_dt == GFP_U16 && I.p > 65536) return GFP_E_UNSUPPORTED;
+    *err = cudaSuccess;
+    const bool in16 = in_dt == GFP_U16, out16 = out_dt == GFP_U16;
+    switch (I.rep) {
+    case GFP_REP_CLASSICAL:  // residues are the representation: a dtype cast
+        if (in16 && out16) *err = launch_conv_t<C_CAST, uint16_t, uint16_t>(K, in, out, n, nullptr, 0, s);
+        else if (in16) *err = launch_conv_t<C_CAST, uint16_t, uint32_t>(K, in, out, n, nullptr, 0, s);
+        else if (out16) *err = launch_conv_t<C_CAST, uint32_t, uint16_t>(K, in, out, n, nullptr, 0, s);
+        else *err = launch_conv_t<C_CAST, uint32_t, uint32_t>(K, in, out, n, nullptr, 0, s);
+        break;
+    case GFP_REP_FP64:  // exact integer <-> binary64 casts
+        if (dir == 0)
+            *err = in16 ? launch_conv_t<C_CAST, uint16_t, double>(K, in, out, n, nullptr, 0, s)
+                        : launch_conv_t<C_CAST, uint32_t, double>(K, in, out, n, nullptr, 0, s);
+        else
+            *err = out16 ? launch_conv_t<C_CAST, double, uint16_t>(K, in, out, n, nullptr, 0, s)
+                         : launch_conv_t<C_CAST, double, uint32_t>(K, in, out, n, nullptr, 0, s);
+        break;
+    case GFP_REP_MONTGOMERY:
+        if (in_dt != GFP_U32 || out_dt != GFP_U32) return GFP_E_UNSUPPORTED;
+        *err = dir == 0 ? launch_conv_t<C_TO_MONT, uint32_t, uint32_t>(K, in, out, n, nullptr, 0, s)
+                        : launch_conv_t<C_FROM_MONT, uint32_t, uint32_t>(K, in, out, n, nullptr, 0, s);
+        break;
+    case GFP_REP_ZECH: {
+        const uint32_t log_entries = (uint32_t)((I.p + 7) & ~7ull);
+        if (dir == 0) {
+            *err = in16 ? launch_conv_t<C_TO_ZECH, uint16_t, uint16_t>(K, in, out, n, K.logt, log_entries, s)
+                        : launch_conv_t<C_TO_ZECH, uint32_t, uint16_t>(K, in, out, n, K.logt, log_entries, s);
+        } else if (zech_small_layout(I.p)) {
+            *err = out16 ? launch_conv_t<C_FROM_ZECH_SMALL, uint16_t, uint16_t>(K, in, out, n, K.antilog,
+                                                                                  K.antilog_entries, s)
+                         : launch_conv_t<C_FROM_ZECH_SMALL, uint16_t, uint32_t>(K, in, out, n, K.antilog,
+                                                                                  K.antilog_entries, s);
+        } else {
+            *err = out16 ? launch_conv_t<C_FROM_ZECH_LARGE, uint16_t, uint16_t>(K, in, out, n, K.antilog,
+                                                                                  K.antilog_entries, s)
+                         : launch_conv_t<C_FROM_ZECH_LARGE, uint16_t, uint32_t>(K, in, out, n, K.antilog,
+                                                                                  K.antilog_entries, s);
+        }
+        break;
+    }
+    }
+    return *err == cudaSuccess ? GFP_OK : GFP_E_CUDA;
+}
+
+}  // namespace gfp

@@ -1,0 +1,23 @@
+// params.h -- the kernel-constant block shared by host launchers and device code (plain C++).
+#pragma once
+#include <cstdint>
+
+namespace gfp {
+namespace dev {
+
+struct KParams {
+    uint64_t p;
+    uint64_t mu;        // floor((2^64 - 1) / p): Barrett constant for the final reductions
+    uint64_t corr;      // 2^64 mod p (sec. 3.3 CORR)
+    double pd;          // p as binary64
+    double inv_p;       // RN(1/p)
+    uint64_t r2;        // Montgomery B^2 mod p
+    uint32_t n_im;      // -p^{-1} mod 2^32
+    uint32_t qbar;      // Zech q - 1
+    const uint16_t *antilog;  // Zech antilog table (global; staged to shared memory by the kernel)
+    const uint16_t *logt;     // Zech log table (global; read once by the finaliser)
+    uint32_t antilog_entries;
+};
+
+}  // namespace dev
+}  // namespace gfp

@@ -1,0 +1,155 @@
+"""Host-side checks of libgfp (no GPU needed): exported symbols, gfp_query constants and bounds,
+argument validation that returns before any device work.
+
+Constants are recomputed here with Python integers (independent of numtheory.cpp); bounds are checked
+against the paper's printed primes (tests/golden/paper_constants.json) and the next prime above.
+"""
+import ctypes
+import json
+import os
+import re
+
+import pytest
+
+import oracle
+from oracle import bruteforce as bf
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PAPER = json.load(open(os.path.join(ROOT, "tests", "golden", "paper_constants.json")))
+
+gfp = pytest.importorskip("paper_cs_0404008_b200")
+
+OK, E_INVAL, E_NOT_PRIME, E_BOUND, E_UNSUPPORTED = 0, 1, 2, 3, 4
+CL, MO, FP, ZE = gfp.CLASSICAL, gfp.MONTGOMERY, gfp.FP64, gfp.ZECH
+U16, U32, F64 = 0, 1, 2
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "gfp.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gfp_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported():
+    names = header_functions()
+    assert len(names) >= 13
+    for name in names:
+        assert hasattr(gfp.lib, name), name
+
+
+def q(p, rep, dt):
+    info = gfp.GfpInfo()
+    st = gfp.lib.gfp_query(p, rep, dt, ctypes.byref(info))
+    return st, info
+
+
+def next_prime(p):
+    p += 1
+    while not bf.is_prime(p) if p < 10 ** 6 else not oracle.is_prime(p):
+        p += 1
+    return p
+
+
+@pytest.mark.parametrize("rep,dt,key", [
+    (CL, U16, "classical_unsigned_32"), (CL, U32, "classical_unsigned_64"), (MO, U32, "montgomery_B32")])
+def test_bounds_at_paper_primes(rep, dt, key):
+    p = PAPER[key]["value"]
+    st, info = q(p, rep, dt)
+    assert st == OK and info.bound == p
+    assert q(next_prime(p), rep, dt)[0] in (E_BOUND,)
+
+
+def test_fp64_and_zech_bounds():
+    # fp64: largest prime with p(p-1) < 2^53 (Eq. (1) at m = 53, k >= 1)
+    p = 94906249
+    assert oracle.is_prime(p) and p * (p - 1) < 2 ** 53
+    nxt = next_prime(p)
+    assert nxt * (nxt - 1) >= 2 ** 53
+    assert q(p, FP, F64)[0] == OK and q(nxt, FP, F64)[0] == E_BOUND
+    assert q(65521, ZE, U16)[0] == OK and q(65537, ZE, U16)[0] == E_BOUND
+
+
+def test_rejections():
+    assert q(65535, CL, U16)[0] == E_NOT_PRIME
+    assert q(1, CL, U16)[0] == E_NOT_PRIME
+    assert q(0, CL, U32)[0] == E_NOT_PRIME
+    assert q(2, MO, U32)[0] == E_BOUND  # Montgomery needs odd p (gcd(p, B) = 1)
+    assert q(7, MO, U16)[0] == E_UNSUPPORTED
+    assert q(7, FP, U32)[0] == E_UNSUPPORTED
+    assert q(7, ZE, U32)[0] == E_UNSUPPORTED
+    assert q(7, 9, U32)[0] == E_INVAL
+    with pytest.raises(gfp.GfpError):
+        gfp.query(65535, CL)
+
+
+PRIMES = [2, 3, 5, 7, 101, 1009, 2897, 32749, 40009, 40499, 46337, 65521, 67108859, 94906249,
+          2 ** 31 - 1, 2654435761, 4294967291]
+
+
+@pytest.mark.parametrize("p", PRIMES)
+def test_query_constants(p):
+    for rep, dt in [(CL, U16), (CL, U32), (MO, U32), (FP, F64), (ZE, U16)]:
+        st, I = q(p, rep, dt)
+        if st != OK:
+            continue
+        m = 53 if rep == FP else 64
+        assert I.acc_bits == m
+        k = I.k
+        # Eq. (1) with a carried residue (reading G7), tight
+        if m == 64:
+            assert k * (p - 1) ** 2 + (p - 1) <= 2 ** 64 - 1 or p == 2
+            assert (k + 1) * (p - 1) ** 2 + (p - 1) > 2 ** 64 - 1 or p == 2
+        else:
+            assert k * (p - 1) ** 2 + (p - 1) < 2 ** 53 or p == 2
+            assert (k + 1) * (p - 1) ** 2 + (p - 1) >= 2 ** 53 or p == 2
+        assert I.corr == 2 ** 64 % p
+        assert I.b_mod_p == 2 ** 32 % p
+        assert I.inv_p == 1.0 / p  # Python float division is IEEE round-to-nearest
+        if rep == MO:
+            assert (I.n_im * p) % 2 ** 32 == 2 ** 32 - 1  # n_im = -p^{-1} mod B
+            assert I.r2 == 2 ** 64 % p
+            kr = I.mont_kr
+            B = 2 ** 32
+            assert kr * (p - 1) ** 2 <= p * B and kr * (p - 1) ** 2 + (B - 1) * p <= 2 ** 64 - 1
+            assert kr == 1000000 or (kr + 1) * (p - 1) ** 2 > p * B or \
+                (kr + 1) * (p - 1) ** 2 + (B - 1) * p > 2 ** 64 - 1  # capped at 10^6 (gfp.h)
+        if rep == ZE:
+            assert I.g == oracle.primitive_root(p)
+            assert I.qbar == p - 1
+            assert I.table_bytes == (131072 if 2 * (p - 1) <= 65534 else 2 * p)
+
+
+def test_config_constants_match_survey():
+    """SURVEY.md 8(a) per-config constants."""
+    i = gfp.query(65521, CL, __import__("torch").uint32)
+    assert i["k"] == 4297065216
+    i = gfp.query(67108859, FP)
+    assert i["k"] == 2 and i["inv_p"].hex() == "0x1.0000014000019p-26"
+    i = gfp.query(2 ** 31 - 1, MO)
+    assert (i["mont_kr"], i["n_im"], i["r2"], i["b_mod_p"], i["corr"]) == (2, 0x80000001, 4, 2, 4)
+    i = gfp.query(32749, ZE)
+    assert (i["g"], i["k"]) == (2, 17200859919)
+
+
+def test_lambda_example_via_query():
+    """at p = 40009 and 64-bit words, lambda ~ 1.15 10^10."""
+    i = gfp.query(40009, CL, __import__("torch").uint32)
+    assert f"{i['k'] / 1e10:.2f}" == "1.15"
+
+
+def test_argument_errors_before_device_work():
+    L = gfp.lib
+    fake = ctypes.c_void_p(0x10000)
+    out = ctypes.c_void_p(0x20000)
+    assert L.gfp_dot(65521, CL, U32, fake, fake, -1, out, None) == E_INVAL
+    assert L.gfp_dot(65521, CL, U32, None, fake, 5, out, None) == E_INVAL
+    assert L.gfp_dot(65521, CL, U32, fake, fake, 5, None, None) == E_INVAL
+    assert L.gfp_dot(65521, CL, U32, ctypes.c_void_p(0x10001), fake, 5, out, None) == E_INVAL
+    assert L.gfp_dot(65521, CL, 7, fake, fake, 5, out, None) == E_INVAL
+    assert L.gfp_dot_batch(65521, CL, U16, fake, 3, fake, 4, 5, out, None) == E_INVAL  # lda < n
+    assert L.gfp_dot_batch(65521, CL, U16, fake, 5, fake, 0, 5, out, None) == OK  # rows == 0: no-op
+    assert L.gfp_to_rep(7, MO, U32, fake, U32, fake, -3, None) == E_INVAL
+    assert b"n < 0" in L.gfp_last_error()
+    assert L.gfp_to_rep(7, MO, U32, fake, U32, out, 0, None) == OK  # n == 0: no-op
+    assert L.gfp_to_rep(7, MO, U16, fake, U32, fake, 4, None) == E_INVAL  # in-place needs equal dtypes
+    assert L.gfp_status_str(E_BOUND).startswith(b"GFP_E_BOUND")

@@ -1,0 +1,426 @@
+"""GPU parity: every entry point of libgfp (through the C ABI binding) against the CPU oracle, bit-exact.
+
+Tolerance is 0 everywhere: integer results compare exactly, and the fp64 representation holds exact
+integers (north_star: "the fp64 path holds integers exactly, so the tolerance there is 0"); doubles are
+compared bitwise (no -0.0).  Inputs are seeded synthetic vectors from synth/ (DESIGN.md input recipe).
+Sizes: the SPEC sweep at small n, k-boundary lengths, all-(p-1) worst cases, ragged tails,
+misaligned starts, and each BASELINE.json config at its full size (the oracle finishes each in seconds).
+"""
+import struct
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+gfp = pytest.importorskip("paper_cs_0404008_b200")
+CL, MO, FP, ZE = gfp.CLASSICAL, gfp.MONTGOMERY, gfp.FP64, gfp.ZECH
+DEV = "cuda:0"
+SEED = synth.BASE_SEED
+SWEEP_PRIMES = [2, 3, 5, 7, 101, 1009, 2897, 32749, 40009, 40499, 46337, 65521]
+SWEEP_DIMS = [0, 1, 2, 511, 512, 513, 10 ** 4]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.init()
+    yield
+    torch.cuda.synchronize()
+
+
+def cu(x: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
+
+
+def host(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy()
+
+
+def bits(x: float) -> bytes:
+    return struct.pack("<d", x)
+
+
+def result_int(t: torch.Tensor) -> int:
+    return int(t.cpu().to(torch.int64)[0]) if t.dtype != torch.float64 else t.cpu()[0].item()
+
+
+def residues(p, n, stream, dtype, seed=SEED):
+    return synth.uniform(seed, stream, 0, n, p, dtype)
+
+
+# ------------------------------------------------------------------------------ classical
+@pytest.mark.parametrize("p", SWEEP_PRIMES)
+def test_classical_sweep(p):
+    for dt in (np.uint16, np.uint32):
+        for n in SWEEP_DIMS:
+            a, b = residues(p, n, 0, dt, SEED + n), residues(p, n, 1, dt, SEED + n)
+            r = gfp.dot(cu(a), cu(b), p, CL)
+            assert r.dtype == (torch.uint16 if dt == np.uint16 else torch.uint32)
+            assert result_int(r) == oracle.dot_classical(p, a, b), (p, dt, n)
+        w = np.full(10 ** 4 + 3, p - 1, dt)  # worst case magnitudes
+        assert result_int(gfp.dot(cu(w), cu(w), p, CL)) == oracle.dot_classical(p, w, w) == (10 ** 4 + 3) % p
+
+
+def test_classical_c1_config():
+    """configs[0]: GF(65521), u32, n = 100000."""
+    p, n = 65521, 100000
+    a, b = residues(p, n, 0, np.uint32), residues(p, n, 1, np.uint32)
+    assert result_int(gfp.dot(cu(a), cu(b), p, CL)) == oracle.dot_classical(p, a, b)
+
+
+@pytest.mark.parametrize("p", [4294967291, 3037000493, 2 ** 31 - 1, 65537])
+def test_classical_u32_large_primes_overflow_path(p):
+    """k is tiny here, so the kernel takes the sec. 3.3 overflow-detection path (CORR on wrap)."""
+    info = gfp.query(p, CL, torch.uint32)
+    for n in [1, 3, 4, 5, 17, 1000, 100003, 2 ** 21 + 5]:
+        a, b = residues(p, n, 0, np.uint32, SEED + 7), residues(p, n, 1, np.uint32, SEED + 7)
+        assert result_int(gfp.dot(cu(a), cu(b), p, CL)) == oracle.dot_classical(p, a, b), (p, n)
+    w = np.full(3 * 10 ** 6 + 1, p - 1, np.uint32)  # every add wraps the u64 when (p-1)^2 ~ 2^64
+    assert result_int(gfp.dot(cu(w), cu(w), p, CL)) == (3 * 10 ** 6 + 1) % p
+    assert info["k"] >= 1
+
+
+def test_misaligned_and_ragged():
+    p = 65521
+    n = 100003
+    a, b = residues(p, n, 0, np.uint32), residues(p, n, 1, np.uint32)
+    ta, tb = cu(a), cu(b)
+    for oa, ob in [(1, 1), (2, 2), (3, 3), (1, 2), (0, 3), (5, 0)]:
+        m = n - 7
+        r = gfp.dot(ta[oa:oa + m], tb[ob:ob + m], p, CL)
+        assert result_int(r) == oracle.dot_classical(p, a[oa:oa + m], b[ob:ob + m]), (oa, ob)
+    a16, b16 = a.astype(np.uint16), b.astype(np.uint16)
+    t16a, t16b = cu(a16), cu(b16)
+    for oa, ob in [(1, 1), (7, 7), (3, 5)]:
+        m = n - 9
+        r = gfp.dot(t16a[oa:oa + m], t16b[ob:ob + m], p, CL)
+        assert result_int(r) == oracle.dot_classical(p, a16[oa:oa + m], b16[ob:ob + m])
+
+
+def test_empty_gives_zero_in_every_representation():
+    e16 = torch.empty(0, dtype=torch.uint16, device=DEV)
+    e32 = torch.empty(0, dtype=torch.uint32, device=DEV)
+    e64 = torch.empty(0, dtype=torch.float64, device=DEV)
+    assert result_int(gfp.dot(e32, e32, 65521, CL)) == 0
+    assert result_int(gfp.dot(e32, e32, 2 ** 31 - 1, MO)) == 0
+    r = gfp.dot(e64, e64, 67108859, FP)
+    assert bits(r.cpu()[0].item()) == bits(0.0)
+    assert result_int(gfp.dot(e16, e16, 32749, ZE)) == 0
+
+
+# ------------------------------------------------------------------------------ Montgomery
+MONT_PRIMES = [3, 7, 101, 40009, 40499, 65521, 2 ** 31 - 1, 2654435761]
+
+
+@pytest.mark.parametrize("p", MONT_PRIMES)
+def test_montgomery_conversion_and_dot(p):
+    kr = gfp.query(p, MO)["mont_kr"]
+    dims = sorted({0, 1, 2, 3, 4, 5, 7, 8, 511, 513, 10 ** 4 + 1, 3 * min(kr, 10) + 2})
+    for n in dims:
+        a, b = residues(p, n, 0, np.uint32, SEED + n), residues(p, n, 1, np.uint32, SEED + n)
+        am, bm = gfp.to_rep(cu(a), p, MO), gfp.to_rep(cu(b), p, MO)
+        ham = host(am)
+        want_am = np.array([oracle.to_mont(p, int(v)) for v in a[:64]], np.uint32)
+        assert np.array_equal(ham[:64], want_am)
+        r = gfp.dot(am, bm, p, MO)
+        assert result_int(r) == oracle.dot_montgomery(p, ham, host(bm)), (p, n)
+        assert np.array_equal(host(gfp.from_rep(am, p, MO)), a)  # round trip
+    w = np.full(4099, p - 1, np.uint32)
+    wm = gfp.to_rep(cu(w), p, MO)
+    assert result_int(gfp.dot(wm, wm, p, MO)) == oracle.to_mont(p, 4099 % p)
+
+
+def test_montgomery_closed_form_mersenne():
+    """p = 2^31-1, B = 2^32 = 2 mod p: to_mont(a) = 2a mod p, exhaustive on a 2^24 sample + edges."""
+    p = 2 ** 31 - 1
+    a = np.concatenate([residues(p, 1 << 24, 5, np.uint32), np.array([0, 1, 2, p - 2, p - 1], np.uint32)])
+    got = host(gfp.to_rep(cu(a), p, MO)).astype(np.uint64)
+    assert np.array_equal(got, (2 * a.astype(np.uint64)) % p)
+
+
+def test_montgomery_c3_config_full_size():
+    """configs[2]: GF(2^31-1), Montgomery B = 2^32, n = 2^28 (1 GiB per operand), converted on device."""
+    p, n = 2 ** 31 - 1, 1 << 28
+    a, b = residues(p, n, 0, np.uint32, SEED + 2), residues(p, n, 1, np.uint32, SEED + 2)
+    am, bm = gfp.to_rep(cu(a), p, MO), gfp.to_rep(cu(b), p, MO)
+    r = result_int(gfp.dot(am, bm, p, MO))
+    # oracle on the classical inputs, encoded: (sum a b mod p) * B mod p
+    assert r == oracle.to_mont(p, oracle.dot_classical(p, a, b))
+    # element-wise conversion check on a strided sample (closed form 2a mod p)
+    idx = np.arange(0, n, 4099)
+    got = host(am[torch.from_numpy(idx).to(DEV)]).astype(np.uint64)
+    assert np.array_equal(got, (2 * a[idx].astype(np.uint64)) % p)
+
+
+# ------------------------------------------------------------------------------ fp64
+FP_PRIMES = [2, 3, 101, 32749, 65521, 40009, 67108859, 94906249]
+
+
+@pytest.mark.parametrize("p", FP_PRIMES)
+def test_fp64_sweep(p):
+    k = gfp.query(p, FP)["k"]
+    dims = sorted(set(SWEEP_DIMS + [max(k - 1, 0), k, k + 1, 3 * k + 2] if k < 10 ** 6 else SWEEP_DIMS))
+    for n in dims:
+        a, b = residues(p, n, 0, np.float64, SEED + n), residues(p, n, 1, np.float64, SEED + n)
+        r = gfp.dot(cu(a), cu(b), p, FP).cpu()[0].item()
+        assert bits(r) == bits(oracle.dot_fp64(p, a, b)), (p, n)
+    for n in [1, 2, 3, 8, 1001, 2 ** 20 + 3]:
+        w = np.full(n, float(p - 1))
+        r = gfp.dot(cu(w), cu(w), p, FP).cpu()[0].item()
+        assert bits(r) == bits(float(n % p))
+
+
+def _two_term_rows(p, T):
+    """a0 b0 + a1 b1 = T with entries in [0, p): a0 = p-1, b0 = T // (p-1) capped, a1 = rest, b1 = 1."""
+    b0 = min(p - 1, T // (p - 1))
+    rest = T - (p - 1) * b0
+    assert 0 <= rest < p
+    return np.array([p - 1, rest], np.float64), np.array([b0, 1], np.float64)
+
+
+@pytest.mark.parametrize("p", [32749, 65521, 67108859, 94906249])
+def test_fp64_reduction_at_multiples_of_p(p):
+    """Two-term dots whose block sum T is k p - 1, k p, k p + 1 (and the SURVEY H4 values where the
+    floor(T * invP) estimate is off by one: 1781447353 at 32749, 1063012704 at 65521), so the NTL
+    reduction's fix-up branch runs on device; results must be exact."""
+    rng = np.random.default_rng(p)
+    tmax = (p - 1) * (p - 1) + (p - 2)
+    Ts = {1781447353 if p == 32749 else 1063012704 if p == 65521 else p}
+    for k in list(rng.integers(1, tmax // p, 300)) + [1, 2, tmax // p]:
+        for d in (-1, 0, 1):
+            T = int(k) * p + d
+            if 0 <= T <= tmax:
+                Ts.add(T)
+    for T in sorted(Ts):
+        a, b = _two_term_rows(p, T)
+        r = gfp.dot(cu(a), cu(b), p, FP).cpu()[0].item()
+        assert bits(r) == bits(float(T % p)) == bits(oracle.dot_fp64(p, a, b)), T
+
+
+def test_fp64_c2_config():
+    """configs[1]: GF(67108859), fp64, n = 10^7."""
+    p, n = 67108859, 10 ** 7
+    a, b = residues(p, n, 0, np.float64, SEED + 1), residues(p, n, 1, np.float64, SEED + 1)
+    r = gfp.dot(cu(a), cu(b), p, FP).cpu()[0].item()
+    assert bits(r) == bits(oracle.dot_fp64(p, a, b))
+
+
+def test_fp64_conversions():
+    p = 67108859
+    a = residues(p, 100001, 0, np.uint32)
+    f = gfp.to_rep(cu(a), p, FP)
+    assert f.dtype == torch.float64 and np.array_equal(host(f), a.astype(np.float64))
+    assert np.array_equal(host(gfp.from_rep(f, p, FP)), a)
+
+
+# ------------------------------------------------------------------------------ Zech
+ZECH_PRIMES = [2, 3, 7, 101, 1009, 32749, 32771, 40009, 65521]
+
+
+@pytest.mark.parametrize("p", ZECH_PRIMES)
+def test_zech_sweep(p):
+    g = gfp.query(p, ZE)["g"]
+    assert g == oracle.primitive_root(p)
+    for n in SWEEP_DIMS:
+        ca = synth.zech_codes(SEED + n, 0, 0, n, p - 1)
+        cb = synth.zech_codes(SEED + n, 1, 0, n, p - 1)
+        r = gfp.dot(cu(ca), cu(cb), p, ZE)
+        assert r.dtype == torch.uint16
+        assert result_int(r) == oracle.dot_zech(p, g, ca, cb), (p, n)
+    # geometric cycle: sum_{c=1}^{q-1} g^c = 0 -> code 0
+    a = np.arange(1, p, dtype=np.uint16)
+    one = np.full(p - 1, p - 1, np.uint16)
+    assert result_int(gfp.dot(cu(a), cu(one), p, ZE)) == 0
+
+
+@pytest.mark.parametrize("p", [7, 101, 32749, 40009, 65521])
+def test_zech_conversions_exhaustive(p):
+    g = gfp.query(p, ZE)["g"]
+    x = np.arange(p, dtype=np.uint16 if p < 65536 else np.uint32)
+    codes = host(gfp.to_rep(cu(x), p, ZE))
+    pw = oracle.zech_powers(p, g)
+    # decode with the oracle's own power list: code 0 -> 0, c -> g^c
+    dec = np.where(codes == 0, 0, pw[codes.astype(np.int64)])
+    assert np.array_equal(dec, x.astype(np.uint64))
+    assert codes[1] == p - 1 and codes[0] == 0
+    back = host(gfp.from_rep(cu(codes), p, ZE, dtype=torch.uint32))
+    assert np.array_equal(back, x.astype(np.uint32))
+
+
+def test_zech_c4_config():
+    """configs[3]: GF(32749), Zech u16, n = 2^26, 10% zeros."""
+    p, n = 32749, 1 << 26
+    ca = synth.zech_codes(SEED + 3, 0, 0, n, p - 1)
+    cb = synth.zech_codes(SEED + 3, 1, 0, n, p - 1)
+    r = result_int(gfp.dot(cu(ca), cu(cb), p, ZE))
+    assert r == oracle.dot_zech(p, 2, ca, cb)
+
+
+# ------------------------------------------------------------------------------ batch
+def test_batch_c5_config():
+    """configs[4]: 65536 x 4096 u16 matrix-vector over GF(65521)."""
+    p, rows, n = 65521, 65536, 4096
+    A = residues(p, rows * n, 2, np.uint16, SEED + 4).reshape(rows, n)
+    x = residues(p, n, 3, np.uint16, SEED + 4)
+    out = host(gfp.dot_batch(cu(A), cu(x), p, CL))
+    want = oracle.dot_batch_classical(p, A, x)
+    assert np.array_equal(out.astype(np.uint64), want)
+
+
+@pytest.mark.parametrize("shape", [(1, 4096), (7, 1), (33, 8), (100, 4097), (513, 1000), (3, 0), (2, 60000)])
+def test_batch_shapes_u16(shape):
+    p = 65521
+    rows, n = shape
+    A = residues(p, rows * n, 2, np.uint16).reshape(rows, n)
+    x = residues(p, n, 3, np.uint16)
+    out = host(gfp.dot_batch(cu(A), cu(x), p, CL))
+    assert np.array_equal(out.astype(np.uint64), oracle.dot_batch_classical(p, A, x))
+    w = np.full((rows, n), p - 1, np.uint16)
+    out = host(gfp.dot_batch(cu(w), cu(w[0] if rows else np.zeros(n, np.uint16)), p, CL))
+    assert np.all(out.astype(np.int64) == n % p)
+
+
+def test_batch_padded_and_unaligned_rows():
+    p = 40009
+    rows, n = 257, 1003
+    for lda in [1003, 1008, 1011]:
+        A = residues(p, rows * lda, 2, np.uint16)
+        x = residues(p, n, 3, np.uint16)
+        out = host(gfp.dot_batch(cu(A), cu(x), p, CL, rows=rows, n=n, lda=lda))
+        want = oracle.dot_batch_classical(p, A, x, lda=lda, rows=rows, n=n)
+        assert np.array_equal(out.astype(np.uint64), want), lda
+    # misaligned x / A start
+    A = residues(p, rows * n + 1, 2, np.uint16)
+    x = residues(p, n + 1, 3, np.uint16)
+    out = host(gfp.dot_batch(cu(A)[1:], cu(x)[1:], p, CL, rows=rows, n=n, lda=n))
+    assert np.array_equal(out.astype(np.uint64), oracle.dot_batch_classical(p, A[1:], x[1:], lda=n, rows=rows, n=n))
+
+
+@pytest.mark.parametrize("p", [65521, 2 ** 31 - 1, 4294967291])
+def test_batch_u32(p):
+    rows, n = 300, 2053
+    A = residues(p, rows * n, 2, np.uint32).reshape(rows, n)
+    x = residues(p, n, 3, np.uint32)
+    out = host(gfp.dot_batch(cu(A), cu(x), p, CL))
+    assert np.array_equal(out.astype(np.uint64), oracle.dot_batch_classical(p, A, x))
+
+
+def test_batch_other_representations():
+    rows, n = 129, 777
+    # Montgomery
+    p = 2 ** 31 - 1
+    A = residues(p, rows * n, 2, np.uint32)
+    x = residues(p, n, 3, np.uint32)
+    Am, xm = gfp.to_rep(cu(A), p, MO), gfp.to_rep(cu(x), p, MO)
+    out = host(gfp.dot_batch(Am, xm, p, MO, rows=rows, n=n))
+    want = oracle.dot_batch_classical(p, A, x, lda=n, rows=rows, n=n)
+    assert np.array_equal(out.astype(np.uint64), np.array([oracle.to_mont(p, int(v)) for v in want], np.uint64))
+    # fp64
+    p = 67108859
+    A = residues(p, rows * n, 2, np.float64)
+    x = residues(p, n, 3, np.float64)
+    out = host(gfp.dot_batch(cu(A), cu(x), p, FP, rows=rows, n=n))
+    want = oracle.dot_batch_classical(p, A.astype(np.uint64), x.astype(np.uint64), lda=n, rows=rows, n=n)
+    assert np.array_equal(out, want.astype(np.float64))
+    # Zech
+    for p in [32749, 65521]:
+        g = gfp.query(p, ZE)["g"]
+        CA = synth.zech_codes(SEED, 2, 0, rows * n, p - 1)
+        cx = synth.zech_codes(SEED, 3, 0, n, p - 1)
+        out = host(gfp.dot_batch(cu(CA), cu(cx), p, ZE, rows=rows, n=n))
+        want = [oracle.dot_zech(p, g, CA[r * n:(r + 1) * n], cx) for r in range(rows)]
+        assert np.array_equal(out.astype(np.int64), np.array(want, np.int64))
+
+
+# ------------------------------------------------------------------------------ partial / finalize / host
+@pytest.mark.parametrize("rep,p", [(CL, 65521), (MO, 2 ** 31 - 1), (FP, 67108859), (ZE, 32749)])
+def test_shard_partials_and_finalize(rep, p):
+    """dot(a, b) = finalize(sum_g partial(a_g, b_g)): the multi-GPU identity on virtual shards."""
+    n = 1_000_003
+    if rep == ZE:
+        a = synth.zech_codes(SEED, 0, 0, n, p - 1)
+        b = synth.zech_codes(SEED, 1, 0, n, p - 1)
+        want = oracle.dot_zech(p, 2, a, b)
+        ta, tb = cu(a), cu(b)
+    elif rep == FP:
+        a, b = residues(p, n, 0, np.float64), residues(p, n, 1, np.float64)
+        want = oracle.dot_fp64(p, a, b)
+        ta, tb = cu(a), cu(b)
+    else:
+        a, b = residues(p, n, 0, np.uint32), residues(p, n, 1, np.uint32)
+        ta, tb = cu(a), cu(b)
+        if rep == MO:
+            ta, tb = gfp.to_rep(ta, p, MO), gfp.to_rep(tb, p, MO)
+            want = oracle.to_mont(p, oracle.dot_classical(p, a, b))
+        else:
+            want = oracle.dot_classical(p, a, b)
+    for G in [1, 2, 3, 8]:
+        bounds = [n * g // G for g in range(G + 1)]
+        parts = [gfp.dot_partial(ta[bounds[g]:bounds[g + 1]], tb[bounds[g]:bounds[g + 1]], p, rep) for g in range(G)]
+        for pt in parts:
+            assert 0 <= int(pt.cpu()[0]) < p
+        summed = torch.stack(parts).sum(0)
+        r = gfp.finalize(summed, p, rep, ta.dtype)
+        got = r.cpu()[0].item() if rep == FP else int(r.cpu().to(torch.int64)[0])
+        assert got == want, G
+
+
+@pytest.mark.parametrize("rep,p", [(CL, 65521), (MO, 2 ** 31 - 1), (FP, 67108859), (ZE, 32749)])
+def test_dot_host_end_to_end(rep, p):
+    n = (64 << 20) // 4 * 3 + 12345  # several staging chunks and a ragged last one
+    if rep == ZE:
+        a = synth.zech_codes(SEED, 0, 0, n, p - 1)
+        b = synth.zech_codes(SEED, 1, 0, n, p - 1)
+        want = oracle.dot_zech(p, 2, a, b)
+    elif rep == FP:
+        a, b = residues(p, n, 0, np.float64), residues(p, n, 1, np.float64)
+        want = oracle.dot_fp64(p, a, b)
+    elif rep == MO:
+        a = np.array([0], np.uint32)
+        raw_a, raw_b = residues(p, n, 0, np.uint32), residues(p, n, 1, np.uint32)
+        a = host(gfp.to_rep(cu(raw_a), p, MO))
+        b = host(gfp.to_rep(cu(raw_b), p, MO))
+        want = oracle.to_mont(p, oracle.dot_classical(p, raw_a, raw_b))
+    else:
+        a, b = residues(p, n, 0, np.uint32), residues(p, n, 1, np.uint32)
+        want = oracle.dot_classical(p, a, b)
+    ta, tb = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()
+    assert gfp.dot_host(ta, tb, p, rep) == want
+    assert gfp.dot_host(torch.from_numpy(a[:1000]), torch.from_numpy(b[:1000]), p, rep) == \
+        gfp.dot(cu(a[:1000]), cu(b[:1000]), p, rep).cpu().to(torch.float64 if rep == FP else torch.int64)[0].item()
+
+
+def test_stream_and_graph_capture():
+    """Results are stream-ordered; the single-launch dot is CUDA-graph capturable after a warm call."""
+    p, n = 65521, 1 << 20
+    a, b = residues(p, n, 0, np.uint32), residues(p, n, 1, np.uint32)
+    ta, tb = cu(a), cu(b)
+    want = oracle.dot_classical(p, a, b)
+    s = torch.cuda.Stream()
+    out = torch.empty(1, dtype=torch.uint32, device=DEV)
+    with torch.cuda.stream(s):
+        gfp.dot(ta, tb, p, CL, out=out)  # warm: allocates the per-stream workspace
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        gfp.dot(ta, tb, p, CL, out=out, stream=s)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert result_int(out) == want
+
+
+def test_launch_counter():
+    p = 65521
+    a = cu(residues(p, 1000, 0, np.uint32))
+    gfp.launch_count(reset=True)
+    for _ in range(5):
+        gfp.dot(a, a, p, CL)
+    assert gfp.launch_count() == 5
