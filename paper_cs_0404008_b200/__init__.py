@@ -174,7 +174,7 @@ def dot_batch(A: torch.Tensor, x: torch.Tensor, p: int, rep: int = CLASSICAL, ou
     if A.dtype != x.dtype:
         raise ValueError("A and x must have the same dtype")
     if A.dim() == 2:
-        if A.stride(1) != 1:
+        if A.shape[1] > 1 and A.stride(1) != 1:
             raise ValueError("A must be row-major with unit column stride")
         rows = A.shape[0] if rows is None else rows
         n = A.shape[1] if n is None else n
