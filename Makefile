@@ -36,3 +36,8 @@ $(LIBGFP): $(GFP_SRCS) $(GFP_HDRS)
 
 clean:
 	rm -f synth/libsynth.so oracle/liboracle.so oracle/liboracle_san.so $(LIBGFP)
+
+# tuning harness (not the product): standalone executable timed on the GPU box
+tune: scripts/tune_dot
+scripts/tune_dot: scripts/tune_dot.cu $(CSRC)/device.cuh $(CSRC)/params.h
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -I$(CSRC) -Iinclude -o $@ $<

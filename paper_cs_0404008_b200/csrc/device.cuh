@@ -25,7 +25,7 @@ namespace dev {
 // 16-byte streaming load: read-only path, no L1 allocation (each byte is used exactly once).
 __device__ __forceinline__ uint4 ld_stream(const void *ptr) {
     uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+    asm("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(ptr));
     return r;
@@ -230,10 +230,23 @@ struct Zech {
     __device__ __forceinline__ static uint32_t pair(uint32_t x, uint32_t y, const KParams &K, const uint16_t *tab) {
         return lookup(x & 0xFFFFu, y & 0xFFFFu, K, tab) + lookup(x >> 16, y >> 16, K, tab);
     }
+    // SMALL, two terms per 32-bit word (SWAR): canonical codes are < 2^15, so i + j < 2^16 and
+    // v + 0x7FFF < 2^16 never carry across the 16-bit lanes.  Bit 15 of v + 0x7FFF is [v != 0].
+    __device__ __forceinline__ static uint32_t pair_swar(uint32_t x, uint32_t y, const uint16_t *tab) {
+        const uint32_t s = x + y;                                                  // i + j per lane
+        const uint32_t nz = (x + 0x7FFF7FFFu) & (y + 0x7FFF7FFFu) & 0x80008000u;  // both operands nonzero
+        const uint32_t keep = (nz >> 15) * 0xFFFFu;                                // lane mask
+        const uint32_t idx = s | ~keep;                                            // zero -> sentinel 0xFFFF
+        return (uint32_t)tab[idx & 0xFFFFu] + (uint32_t)tab[idx >> 16];
+    }
     __device__ __forceinline__ static void vec(Acc &A, uint4 x, uint4 y, const KParams &K, const uint16_t *tab) {
-        uint32_t s = pair(x.x, y.x, K, tab) + pair(x.y, y.y, K, tab) + pair(x.z, y.z, K, tab) +
-                     pair(x.w, y.w, K, tab);  // 8 values < 2^16: no wrap in 32 bits
-        A.s += s;
+        uint32_t s;
+        if (SMALL)
+            s = pair_swar(x.x, y.x, tab) + pair_swar(x.y, y.y, tab) + pair_swar(x.z, y.z, tab) +
+                pair_swar(x.w, y.w, tab);
+        else
+            s = pair(x.x, y.x, K, tab) + pair(x.y, y.y, K, tab) + pair(x.z, y.z, K, tab) + pair(x.w, y.w, K, tab);
+        A.s += s;  // 8 values < 2^16: no wrap in 32 bits
     }
     __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
         return ALL ? A.s : mod_p(A.s, K.p, K.mu);

@@ -183,15 +183,16 @@ __global__ void __launch_bounds__(NT) batch_cl16_kernel(const uint16_t *__restri
         const uint16_t *Ar = A + row * lda;
         const uint4 *av = reinterpret_cast<const uint4 *>(Ar);
         uint64_t tot = 0;
-        for (int64_t v0 = lane; v0 < nvec; v0 += 32 * U) {
+        int64_t v0 = lane;
+        // full chunks: U unpredicated 16-byte loads per lane in flight, then 8 DP2A per vector
+        for (; v0 + 32 * (U - 1) < nvec; v0 += 32 * U) {
             uint4 ra[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-                ra[u] = v0 + u * 32 < nvec ? ld_stream(av + v0 + u * 32) : make_uint4(0, 0, 0, 0);
+            for (int u = 0; u < U; ++u) ra[u] = ld_stream(av + v0 + u * 32);
             uint32_t lo = 0, hi = 0;  // <= 4U dp2a of < 2^25 each: no wrap for U <= 32
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const uint4 w = xv[v0 + u * 32 < nvec ? v0 + u * 32 : 0];
+                const uint4 w = xv[v0 + u * 32];
                 lo = __dp2a_lo(ra[u].x, w.x, lo);
                 hi = __dp2a_hi(ra[u].x, w.x, hi);
                 lo = __dp2a_lo(ra[u].y, w.y, lo);
@@ -201,6 +202,17 @@ __global__ void __launch_bounds__(NT) batch_cl16_kernel(const uint16_t *__restri
                 lo = __dp2a_lo(ra[u].w, w.w, lo);
                 hi = __dp2a_hi(ra[u].w, w.w, hi);
             }
+            tot += (uint64_t)lo + ((uint64_t)hi << 8);
+        }
+        for (; v0 < nvec; v0 += 32) {  // remaining vectors of the row
+            const uint4 ra = ld_stream(av + v0), w = xv[v0];
+            uint32_t lo = __dp2a_lo(ra.x, w.x, 0u), hi = __dp2a_hi(ra.x, w.x, 0u);
+            lo = __dp2a_lo(ra.y, w.y, lo);
+            hi = __dp2a_hi(ra.y, w.y, hi);
+            lo = __dp2a_lo(ra.z, w.z, lo);
+            hi = __dp2a_hi(ra.z, w.z, hi);
+            lo = __dp2a_lo(ra.w, w.w, lo);
+            hi = __dp2a_hi(ra.w, w.w, hi);
             tot += (uint64_t)lo + ((uint64_t)hi << 8);
         }
         for (int64_t j = nvec * 8 + lane; j < n; j += 32) tot += (uint64_t)Ar[j] * x[j];
@@ -435,7 +447,9 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
         return num_sms(d);
     }();
     const int bps = policy_occupancy(pol, smem);
-    int64_t want = std::max<int64_t>((nvec + (int64_t)NT * U - 1) / ((int64_t)NT * U), (head + NT - 1) / NT);
+    // at least one 16-byte vector per thread before capping at the resident grid: small inputs are
+    // latency-bound, so spread them over as many SMs as possible (one DRAM round trip per thread)
+    int64_t want = std::max<int64_t>((nvec + NT - 1) / NT, (head + NT - 1) / NT);
     int64_t grid = std::min<int64_t>({(int64_t)dev_sms * bps, std::max<int64_t>(want, 1), (int64_t)kMaxGrid});
     const int64_t threads = grid * NT;
     const int64_t iters = (nvec + threads * U - 1) / (threads * U);
@@ -524,7 +538,7 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
     case GFP_REP_CLASSICAL:
         if (I.dtype == GFP_U16) {
             if (vec && (u128)n * q2 <= max64 && n <= 96 * 1024) {
-                constexpr int NT = 256, U = 8;
+                constexpr int NT = 256, U = 16;
                 auto kern = batch_cl16_kernel<NT, U>;
                 const size_t smem = (size_t)(((n + 1) / 2 + 3) & ~int64_t(3)) * 4;
                 int bps = occupancy(kern, NT, smem);
