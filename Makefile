@@ -41,3 +41,11 @@ clean:
 tune: scripts/tune_dot
 scripts/tune_dot: scripts/tune_dot.cu $(CSRC)/device.cuh $(CSRC)/params.h
 	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -I$(CSRC) -Iinclude -o $@ $<
+tune: scripts/tune_small
+scripts/tune_small: scripts/tune_small.cu $(CSRC)/device.cuh $(CSRC)/params.h
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -I$(CSRC) -Iinclude -o $@ $<
+
+# A/B variant of the product library for tuning runs (GFP_LIBRARY=... python bench.py)
+gfp-pipe: $(PKG)/libgfp_pipe.so
+$(PKG)/libgfp_pipe.so: $(GFP_SRCS) $(GFP_HDRS)
+	$(NVCC) $(NVFLAGS) -DGFP_DOT_PIPE=1 -shared -o $@ $(GFP_SRCS) -lcudart 2> /dev/null

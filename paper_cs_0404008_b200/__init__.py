@@ -28,7 +28,7 @@ U16, U32, F64 = 0, 1, 2
 _REP_NAMES = {CLASSICAL: "classical", MONTGOMERY: "montgomery", FP64: "fp64", ZECH: "zech"}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libgfp.so")
+_LIB_PATH = os.environ.get("GFP_LIBRARY") or os.path.join(_HERE, "libgfp.so")  # override: A/B builds
 if not os.path.exists(_LIB_PATH):
     raise ImportError(f"{_LIB_PATH} is missing: build it with `make gfp` (nvcc, sm_100a). "
                       "There is no CPU fallback.")

@@ -8,8 +8,8 @@
 
 namespace gfp {
 
-// Per-(device, stream) scratch for the single-launch combine: per-CTA partials and the
-// last-CTA-done counter (self-resetting, so no memset per call).
+// Per-(device, stream) scratch for the single-launch combine: the u64 sum of CTA contributions
+// (partials[0]) and the last-CTA-done counter, both self-resetting, so no memset per call.
 struct Workspace {
     uint64_t *partials;
     unsigned int *counter;

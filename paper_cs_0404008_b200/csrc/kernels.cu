@@ -84,33 +84,69 @@ __device__ __forceinline__ void stage_table(uint16_t *dst, const uint16_t *src, 
 }
 
 // ------------------------------------------------------------------------------ single dot
-template <class R, int NT, int U>
+template <class R, int NT, int U, bool PIPE>
 __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restrict__ a,
                                                  const typename R::elem *__restrict__ b, int64_t n,
                                                  int64_t head, KParams K, Workspace ws, OutSpec O) {
     extern __shared__ __align__(16) uint16_t s_tab[];
     __shared__ uint64_t red[32];
-    __shared__ int s_last;
-    const uint16_t *tab = nullptr;
-    if constexpr (R::kTable) {
-        stage_table(s_tab, K.antilog, K.antilog_entries);
-        __syncthreads();
-        tab = s_tab;
-    }
     typename R::Acc acc;
     R::init(acc);
     const int64_t gtid = (int64_t)blockIdx.x * NT + threadIdx.x;
     const int64_t gstride = (int64_t)gridDim.x * NT;
-
-    // scalar head (the whole input when a and b are not co-aligned)
-    for (int64_t i = gtid; i < head; i += gstride) R::term(acc, a[i], b[i], K, tab);
-
-    // 16-byte vector body: U independent loads of each operand in flight per thread
     const int64_t nvec = (n - head) / R::W;
     const uint4 *av = reinterpret_cast<const uint4 *>(a + head);
     const uint4 *bv = reinterpret_cast<const uint4 *>(b + head);
     int64_t i0 = (int64_t)blockIdx.x * (NT * U) + threadIdx.x;
     const int64_t step = (int64_t)gridDim.x * (NT * U);
+    const uint16_t *tab = nullptr;
+
+    // Software-pipelined stream (PIPE): the U loads of each operand for step k+1 are in flight while
+    // step k computes, so every thread keeps between U and 2U 16-byte loads outstanding per operand.
+    // The first loads are issued before the Zech antilog table is staged, so the stream's DRAM latency
+    // overlaps the table copy from L2 into shared memory.
+    uint4 ca[U], cb[U];
+    bool have = PIPE && i0 + (U - 1) * NT < nvec;
+    if (PIPE && have) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            ca[u] = ld_stream(av + i0 + u * NT);
+            cb[u] = ld_stream(bv + i0 + u * NT);
+        }
+    }
+    if constexpr (R::kTable) {
+        stage_table(s_tab, K.antilog, K.antilog_entries);
+        __syncthreads();
+        tab = s_tab;
+    }
+    if constexpr (PIPE) {
+        while (have) {
+            const int64_t nx = i0 + step;
+            const bool more = nx + (U - 1) * NT < nvec;
+            uint4 na[U], nb[U];
+            if (more) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    na[u] = ld_stream(av + nx + u * NT);
+                    nb[u] = ld_stream(bv + nx + u * NT);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) R::vec(acc, ca[u], cb[u], K, tab);
+            i0 = nx;
+            have = more;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                ca[u] = na[u];
+                cb[u] = nb[u];
+            }
+        }
+    }
+
+    // scalar head (the whole input when a and b are not co-aligned)
+    for (int64_t i = gtid; i < head; i += gstride) R::term(acc, a[i], b[i], K, tab);
+
+    // 16-byte vector body (!PIPE): U independent loads of each operand in flight per thread
     for (; i0 + (U - 1) * NT < nvec; i0 += step) {
         uint4 xa[U], xb[U];
 #pragma unroll
@@ -129,23 +165,23 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
     // scalar tail (< W elements)
     for (int64_t i = head + nvec * R::W + gtid; i < n; i += gstride) R::term(acc, a[i], b[i], K, tab);
 
-    // combine: warp shuffle -> CTA tree -> per-CTA partial -> last CTA reduces and encodes
-    uint64_t v = block_sum(R::finish(acc, K), red);
+    // combine: warp shuffle -> CTA tree -> one u64 atomic per CTA; the CTA whose arrival on the
+    // counter is last (acq_rel orders every earlier CTA's atomic before its own read) reduces mod p
+    // once and encodes -- "A single machine remaindering is needed at the end".
+    // Exact and order-independent: integer sums, no wrap (host-checked bounds).
+    const uint64_t v = block_sum(R::finish(acc, K), red);
     if (threadIdx.x == 0) {
-        ws.partials[blockIdx.x] = v;
-        __threadfence();
-        unsigned int t = atomicAdd(ws.counter, 1u);
-        s_last = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    uint64_t s = 0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) s += (uint64_t)__ldcg(reinterpret_cast<const unsigned long long *>(ws.partials + i));
-    s = block_sum(s, red);
-    if (threadIdx.x == 0) {
-        write_result(mod_p(s, K.p, K.mu), O, K, 0);  // "A single machine remaindering ... at the end"
-        *ws.counter = 0;
+        unsigned long long *sum = reinterpret_cast<unsigned long long *>(ws.partials);
+        atomicAdd(sum, (unsigned long long)v);
+        unsigned int t;
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(ws.counter) : "memory");
+        if (t == gridDim.x - 1) {
+            unsigned long long s;
+            asm volatile("ld.relaxed.gpu.u64 %0, [%1];" : "=l"(s) : "l"(sum) : "memory");
+            write_result(mod_p(s, K.p, K.mu), O, K, 0);
+            *sum = 0;  // self-reset for the next launch on this stream
+            *ws.counter = 0;
+        }
     }
 }
 
@@ -351,25 +387,32 @@ static int occupancy(F kernel, int block, size_t smem) {
     return bps;
 }
 
-constexpr int kDotNT = 256, kDotU = 4, kZechNT = 1024, kZechU = 2;
+// Measured on B200 (scripts/ab_bench.sh, scripts/tune_*.cu): unpipelined U=4 (40 regs, 6 CTAs/SM)
+// beats the register-pipelined variant (80 regs) by 2% on C3; fp64 is best at U=2; Zech (1024
+// threads, 64-register cap) needs the pipeline to keep loads in flight across its table lookups.
+#ifndef GFP_DOT_PIPE
+#define GFP_DOT_PIPE 0
+#endif
+constexpr int kDotNT = 256, kDotU = 4, kFpU = 2, kZechNT = 1024, kZechU = 2;
+constexpr bool kPipe = GFP_DOT_PIPE != 0;
 
-template <class R, int NT, int U>
+template <class R, int NT, int U, bool PIPE>
 static cudaError_t launch_dot_t(const DotPlan &P, const KParams &K, const void *a, const void *b, int64_t n,
                                 Workspace ws, OutSpec O, cudaStream_t s) {
-    auto kern = dot_kernel<R, NT, U>;
+    auto kern = dot_kernel<R, NT, U, PIPE>;
     occupancy(kern, NT, P.smem);  // sets the smem attribute once
     kern<<<P.grid, NT, P.smem, s>>>((const typename R::elem *)a, (const typename R::elem *)b, n, P.head, K, ws, O);
     count_launch();
     return cudaGetLastError();
 }
 
-template <class R, int NT, int U>
+template <class R, int NT, int U, bool PIPE>
 static int dot_occupancy(size_t smem) {
-    return occupancy(dot_kernel<R, NT, U>, NT, smem);
+    return occupancy(dot_kernel<R, NT, U, PIPE>, NT, smem);
 }
 
 static int policy_block(int pol) { return pol >= P_ZS_ALL ? kZechNT : kDotNT; }
-static int policy_unroll(int pol) { return pol >= P_ZS_ALL ? kZechU : kDotU; }
+static int policy_unroll(int pol) { return pol >= P_ZS_ALL ? kZechU : (pol >= P_FP_THREAD ? kFpU : kDotU); }
 static int policy_width(int pol) {
     if (pol <= P_CL32_OVF || (pol >= P_MONT1 && pol <= P_MONT4)) return 4;
     if (pol >= P_FP_THREAD && pol <= P_FP_K2) return 2;
@@ -378,21 +421,21 @@ static int policy_width(int pol) {
 
 static int policy_occupancy(int pol, size_t smem) {
     switch (pol) {
-    case P_CL32_ALL: return dot_occupancy<ClassicalU32<CL_ALL>, kDotNT, kDotU>(smem);
-    case P_CL32_THREAD: return dot_occupancy<ClassicalU32<CL_THREAD>, kDotNT, kDotU>(smem);
-    case P_CL32_OVF: return dot_occupancy<ClassicalU32<CL_OVERFLOW>, kDotNT, kDotU>(smem);
-    case P_CL16_ALL: return dot_occupancy<ClassicalU16<CL_ALL>, kDotNT, kDotU>(smem);
-    case P_CL16_THREAD: return dot_occupancy<ClassicalU16<CL_THREAD>, kDotNT, kDotU>(smem);
-    case P_MONT1: return dot_occupancy<Montgomery<1>, kDotNT, kDotU>(smem);
-    case P_MONT2: return dot_occupancy<Montgomery<2>, kDotNT, kDotU>(smem);
-    case P_MONT4: return dot_occupancy<Montgomery<4>, kDotNT, kDotU>(smem);
-    case P_FP_THREAD: return dot_occupancy<Fp64<0>, kDotNT, kDotU>(smem);
-    case P_FP_K1: return dot_occupancy<Fp64<1>, kDotNT, kDotU>(smem);
-    case P_FP_K2: return dot_occupancy<Fp64<2>, kDotNT, kDotU>(smem);
-    case P_ZS_ALL: return dot_occupancy<Zech<true, true>, kZechNT, kZechU>(smem);
-    case P_ZS_THREAD: return dot_occupancy<Zech<true, false>, kZechNT, kZechU>(smem);
-    case P_ZL_ALL: return dot_occupancy<Zech<false, true>, kZechNT, kZechU>(smem);
-    case P_ZL_THREAD: return dot_occupancy<Zech<false, false>, kZechNT, kZechU>(smem);
+    case P_CL32_ALL: return dot_occupancy<ClassicalU32<CL_ALL>, kDotNT, kDotU, kPipe>(smem);
+    case P_CL32_THREAD: return dot_occupancy<ClassicalU32<CL_THREAD>, kDotNT, kDotU, kPipe>(smem);
+    case P_CL32_OVF: return dot_occupancy<ClassicalU32<CL_OVERFLOW>, kDotNT, kDotU, kPipe>(smem);
+    case P_CL16_ALL: return dot_occupancy<ClassicalU16<CL_ALL>, kDotNT, kDotU, kPipe>(smem);
+    case P_CL16_THREAD: return dot_occupancy<ClassicalU16<CL_THREAD>, kDotNT, kDotU, kPipe>(smem);
+    case P_MONT1: return dot_occupancy<Montgomery<1>, kDotNT, kDotU, kPipe>(smem);
+    case P_MONT2: return dot_occupancy<Montgomery<2>, kDotNT, kDotU, kPipe>(smem);
+    case P_MONT4: return dot_occupancy<Montgomery<4>, kDotNT, kDotU, kPipe>(smem);
+    case P_FP_THREAD: return dot_occupancy<Fp64<0>, kDotNT, kFpU, false>(smem);
+    case P_FP_K1: return dot_occupancy<Fp64<1>, kDotNT, kFpU, false>(smem);
+    case P_FP_K2: return dot_occupancy<Fp64<2>, kDotNT, kFpU, false>(smem);
+    case P_ZS_ALL: return dot_occupancy<Zech<true, true>, kZechNT, kZechU, true>(smem);
+    case P_ZS_THREAD: return dot_occupancy<Zech<true, false>, kZechNT, kZechU, true>(smem);
+    case P_ZL_ALL: return dot_occupancy<Zech<false, true>, kZechNT, kZechU, true>(smem);
+    case P_ZL_THREAD: return dot_occupancy<Zech<false, false>, kZechNT, kZechU, true>(smem);
     }
     return 1;
 }
@@ -400,21 +443,21 @@ static int policy_occupancy(int pol, size_t smem) {
 cudaError_t launch_dot(const DotPlan &P, const KParams &K, const void *a, const void *b, int64_t n, Workspace ws,
                        OutSpec O, cudaStream_t s) {
     switch (P.policy) {
-    case P_CL32_ALL: return launch_dot_t<ClassicalU32<CL_ALL>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
-    case P_CL32_THREAD: return launch_dot_t<ClassicalU32<CL_THREAD>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
-    case P_CL32_OVF: return launch_dot_t<ClassicalU32<CL_OVERFLOW>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
-    case P_CL16_ALL: return launch_dot_t<ClassicalU16<CL_ALL>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
-    case P_CL16_THREAD: return launch_dot_t<ClassicalU16<CL_THREAD>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
-    case P_MONT1: return launch_dot_t<Montgomery<1>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
-    case P_MONT2: return launch_dot_t<Montgomery<2>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
-    case P_MONT4: return launch_dot_t<Montgomery<4>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
-    case P_FP_THREAD: return launch_dot_t<Fp64<0>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
-    case P_FP_K1: return launch_dot_t<Fp64<1>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
-    case P_FP_K2: return launch_dot_t<Fp64<2>, kDotNT, kDotU>(P, K, a, b, n, ws, O, s);
-    case P_ZS_ALL: return launch_dot_t<Zech<true, true>, kZechNT, kZechU>(P, K, a, b, n, ws, O, s);
-    case P_ZS_THREAD: return launch_dot_t<Zech<true, false>, kZechNT, kZechU>(P, K, a, b, n, ws, O, s);
-    case P_ZL_ALL: return launch_dot_t<Zech<false, true>, kZechNT, kZechU>(P, K, a, b, n, ws, O, s);
-    case P_ZL_THREAD: return launch_dot_t<Zech<false, false>, kZechNT, kZechU>(P, K, a, b, n, ws, O, s);
+    case P_CL32_ALL: return launch_dot_t<ClassicalU32<CL_ALL>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
+    case P_CL32_THREAD: return launch_dot_t<ClassicalU32<CL_THREAD>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
+    case P_CL32_OVF: return launch_dot_t<ClassicalU32<CL_OVERFLOW>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
+    case P_CL16_ALL: return launch_dot_t<ClassicalU16<CL_ALL>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
+    case P_CL16_THREAD: return launch_dot_t<ClassicalU16<CL_THREAD>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
+    case P_MONT1: return launch_dot_t<Montgomery<1>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
+    case P_MONT2: return launch_dot_t<Montgomery<2>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
+    case P_MONT4: return launch_dot_t<Montgomery<4>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
+    case P_FP_THREAD: return launch_dot_t<Fp64<0>, kDotNT, kFpU, false>(P, K, a, b, n, ws, O, s);
+    case P_FP_K1: return launch_dot_t<Fp64<1>, kDotNT, kFpU, false>(P, K, a, b, n, ws, O, s);
+    case P_FP_K2: return launch_dot_t<Fp64<2>, kDotNT, kFpU, false>(P, K, a, b, n, ws, O, s);
+    case P_ZS_ALL: return launch_dot_t<Zech<true, true>, kZechNT, kZechU, true>(P, K, a, b, n, ws, O, s);
+    case P_ZS_THREAD: return launch_dot_t<Zech<true, false>, kZechNT, kZechU, true>(P, K, a, b, n, ws, O, s);
+    case P_ZL_ALL: return launch_dot_t<Zech<false, true>, kZechNT, kZechU, true>(P, K, a, b, n, ws, O, s);
+    case P_ZL_THREAD: return launch_dot_t<Zech<false, false>, kZechNT, kZechU, true>(P, K, a, b, n, ws, O, s);
     }
     return cudaErrorInvalidValue;
 }
