@@ -440,3 +440,41 @@ def test_launch_counter():
     for _ in range(5):
         gfp.dot(a, a, p, CL)
     assert gfp.launch_count() == 5
+
+
+# ------------------------------------------------------------------------------ maximum sizes
+def _full(n, value, dtype):
+    """Device vector of n copies of `value` without a host copy (int16/int32 bit patterns viewed unsigned)."""
+    if dtype == torch.uint16:
+        v = value - (1 << 16) if value >= 1 << 15 else value
+        return torch.full((n,), v, dtype=torch.int16, device=DEV).view(torch.uint16)
+    v = value - (1 << 32) if value >= 1 << 31 else value
+    return torch.full((n,), v, dtype=torch.int32, device=DEV).view(torch.uint32)
+
+
+def test_beyond_2_31_elements_closed_form():
+    """n > 2^31 exercises the 64-bit index arithmetic of every loop: all-(p-1) vectors dot to n mod p."""
+    n = (1 << 31) + 4099
+    p = 65521
+    w = _full(n, p - 1, torch.uint16)
+    assert result_int(gfp.dot(w, w, p, CL)) == n % p
+    del w
+    p = 32749
+    c = _full(n, (p - 1) // 2, torch.uint16)  # code of -1 (i_{-1} = (q-1)/2, P:139-140); (-1)(-1) = 1
+    assert result_int(gfp.dot(c, c, p, ZE)) == oracle.zech_encode(p, 2, n % p)
+    del c
+    torch.cuda.empty_cache()
+    p = 2 ** 31 - 1
+    m = _full(n, oracle.to_mont(p, p - 1), torch.uint32)
+    assert result_int(gfp.dot(m, m, p, MO)) == oracle.to_mont(p, n % p)
+    del m
+    torch.cuda.empty_cache()
+
+
+def test_batch_many_rows_closed_form():
+    """rows > 2^20 with short rows: every row of all-(p-1) dots to n mod p."""
+    p, rows, n = 65521, (1 << 21) + 3, 24
+    A = _full(rows * n, p - 1, torch.uint16).view(rows, n)
+    x = _full(n, p - 1, torch.uint16)
+    out = gfp.dot_batch(A, x, p, CL)
+    assert bool((out.to(torch.int32) == n % p).all())
