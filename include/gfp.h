@@ -92,6 +92,37 @@ typedef enum {
     GFP_ACC_OVERFLOW = 2   /* sec. 3.3: let the u64 wrap, add CORR = 2^64 mod p on wrap */
 } gfp_acc;
 
+/* The paper's accumulation algorithms (sec. 3), selectable per call through gfp_options. */
+typedef enum {
+    GFP_STRAT_AUTO = 0,     /* the library's choice (the fastest exact plan; gfp_plan reports it) */
+    GFP_STRAT_DELAYED = 1,  /* sec. 3.1 Eq. (1): no reduction before the end; needs n(p-1)^2 < 2^m */
+    GFP_STRAT_BLOCKED = 2,  /* sec. 3.2: reduce every k = floor((2^m-1-(p-1))/(p-1)^2) products (G7) */
+    GFP_STRAT_OVERFLOW = 3, /* sec. 3.3: wrap test + CORR = 2^m mod p on every product */
+    GFP_STRAT_HYBRID = 4    /* sec. 3.4 Eq. (2): one wrap test per block of lambda, lambda p(p-1) < 2^m */
+} gfp_strategy;
+
+/* Per-call options.  acc_bits: the accumulator width m of Eq. (1): 0 = default (64; 53 for fp64),
+ * 32 or 64 for classical storage (m = 32 needs p(p-1) < 2^32, i.e. p <= 65521).  Admissible
+ * combinations: classical x {all strategies} x {32, 64}; Montgomery x {AUTO, BLOCKED (REDC every
+ * k_R products, sec. 3.2.1), OVERFLOW (overflow-Montgomery, sec. 3.3)}; fp64 x {AUTO,
+ * DELAYED, BLOCKED}; Zech x {AUTO}.  Anything else: GFP_E_UNSUPPORTED; a strategy whose bound the
+ * (p, n) pair violates: GFP_E_BOUND. */
+typedef struct {
+    int32_t strategy;  /* gfp_strategy */
+    int32_t acc_bits;
+} gfp_options;
+
+/* What a call would run (gfp_plan): kernel, grid, the strategy and its block length, and per-thread
+ * bounds on terms and on reductions / wrap tests. */
+typedef struct {
+    int32_t strategy, acc_bits;
+    uint64_t block;              /* products per reduction or per wrap test; 0 = none before the end */
+    int32_t grid, threads_per_block;
+    int64_t terms_per_thread;    /* upper bound */
+    int64_t reductions_per_thread; /* upper bound: remainders, REDCs or wrap tests */
+    char kernel[64];
+} gfp_plan_info;
+
 /* Host-side description of a field/representation (gfp_query). */
 typedef struct {
     uint64_t p;
@@ -153,6 +184,18 @@ gfp_status gfp_dot_partial(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a,
                            int64_t n, uint64_t *partial, void *stream);
 gfp_status gfp_finalize(uint64_t p, gfp_rep rep, gfp_dtype dt, const uint64_t *summed, void *out,
                         void *stream);
+
+/* gfp_dot / gfp_dot_batch with explicit options (NULL = defaults): the paper's strategies side by
+ * side, exact in every admissible combination.  Same pointers, streams and errors as gfp_dot. */
+gfp_status gfp_dot_ex(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
+                      const gfp_options *opt, void *out, void *stream);
+gfp_status gfp_dot_batch_ex(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *A, int64_t lda, const void *x,
+                            int64_t rows, int64_t n, const gfp_options *opt, void *out, void *stream);
+
+/* host: the plan gfp_dot_ex would use for n terms with 16-byte aligned operands on the current
+ * device (no device work besides querying its SM count and kernel occupancy). */
+gfp_status gfp_plan(uint64_t p, gfp_rep rep, gfp_dtype dt, int64_t n, const gfp_options *opt,
+                    gfp_plan_info *info);
 
 /* End-to-end convenience: a, b, out are HOST pointers (pinned memory gives
  * overlapped copies; pageable works but copies synchronously).  Streams the

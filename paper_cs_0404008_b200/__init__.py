@@ -18,13 +18,16 @@ import os
 import torch
 
 __all__ = [
-    "CLASSICAL", "MONTGOMERY", "FP64", "ZECH", "GfpError", "lib", "query", "dot", "dot_batch",
+    "CLASSICAL", "MONTGOMERY", "FP64", "ZECH", "AUTO", "DELAYED", "BLOCKED", "OVERFLOW", "HYBRID",
+    "GfpError", "lib", "query", "plan", "dot", "dot_ex", "dot_batch", "dot_batch_ex",
     "dot_partial", "finalize", "to_rep", "from_rep", "dot_host", "launch_count", "release_caches",
     "rep_dtype",
 ]
 
 CLASSICAL, MONTGOMERY, FP64, ZECH = 0, 1, 2, 3
 U16, U32, F64 = 0, 1, 2
+AUTO, DELAYED, BLOCKED, OVERFLOW, HYBRID = 0, 1, 2, 3, 4  # gfp_strategy (paper sec. 3)
+_STRAT_NAMES = {AUTO: "auto", DELAYED: "delayed", BLOCKED: "blocked", OVERFLOW: "overflow", HYBRID: "hybrid"}
 _REP_NAMES = {CLASSICAL: "classical", MONTGOMERY: "montgomery", FP64: "fp64", ZECH: "zech"}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -43,6 +46,17 @@ class GfpInfo(ctypes.Structure):
                 ("table_bytes", ctypes.c_uint64)]
 
 
+class GfpOptions(ctypes.Structure):
+    _fields_ = [("strategy", ctypes.c_int32), ("acc_bits", ctypes.c_int32)]
+
+
+class GfpPlanInfo(ctypes.Structure):
+    _fields_ = [("strategy", ctypes.c_int32), ("acc_bits", ctypes.c_int32), ("block", ctypes.c_uint64),
+                ("grid", ctypes.c_int32), ("threads_per_block", ctypes.c_int32),
+                ("terms_per_thread", ctypes.c_int64), ("reductions_per_thread", ctypes.c_int64),
+                ("kernel", ctypes.c_char * 64)]
+
+
 lib = ctypes.CDLL(_LIB_PATH)
 _u64, _i64, _int, _vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
 _SIGS = {
@@ -54,6 +68,9 @@ _SIGS = {
     "gfp_dot_partial": [_u64, _int, _int, _vp, _vp, _i64, _vp, _vp],
     "gfp_finalize": [_u64, _int, _int, _vp, _vp, _vp],
     "gfp_dot_host": [_u64, _int, _int, _vp, _vp, _i64, _vp, _vp],
+    "gfp_dot_ex": [_u64, _int, _int, _vp, _vp, _i64, ctypes.POINTER(GfpOptions), _vp, _vp],
+    "gfp_dot_batch_ex": [_u64, _int, _int, _vp, _i64, _vp, _i64, _i64, ctypes.POINTER(GfpOptions), _vp, _vp],
+    "gfp_plan": [_u64, _int, _int, _i64, ctypes.POINTER(GfpOptions), ctypes.POINTER(GfpPlanInfo)],
 }
 for _name, _args in _SIGS.items():
     getattr(lib, _name).argtypes = _args
@@ -140,6 +157,36 @@ def dot(a: torch.Tensor, b: torch.Tensor, p: int, rep: int = CLASSICAL, out: tor
     return out
 
 
+def _opts(strategy, acc_bits):
+    return ctypes.byref(GfpOptions(strategy, acc_bits))
+
+
+def plan(p: int, rep: int, n: int, dtype: torch.dtype | None = None, strategy: int = AUTO,
+         acc_bits: int = 0) -> dict:
+    """What gfp_dot_ex would run for n terms: kernel, grid, strategy, block length, per-thread bounds."""
+    info = GfpPlanInfo()
+    dt = _TORCH_DT[dtype if dtype is not None else rep_dtype(rep, p)]
+    _check(lib.gfp_plan(p, rep, dt, n, _opts(strategy, acc_bits), ctypes.byref(info)))
+    d = {f: getattr(info, f) for f, _ in GfpPlanInfo._fields_}
+    d["kernel"] = info.kernel.decode()
+    d["strategy_name"] = _STRAT_NAMES.get(info.strategy, "?")
+    return d
+
+
+def dot_ex(a: torch.Tensor, b: torch.Tensor, p: int, rep: int = CLASSICAL, strategy: int = AUTO, acc_bits: int = 0,
+           out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """dot with an explicit accumulation strategy of the paper (sec. 3) and accumulator width m."""
+    a, b = _flat_cuda(a, "a"), _flat_cuda(b, "b")
+    if a.numel() != b.numel() or a.dtype != b.dtype or a.device != b.device:
+        raise ValueError("a and b must have the same length, dtype and device")
+    if out is None:
+        out = torch.empty(1, dtype=a.dtype, device=a.device)
+    with torch.cuda.device(a.device):
+        _check(lib.gfp_dot_ex(p, rep, _dt(a), a.data_ptr(), b.data_ptr(), a.numel(), _opts(strategy, acc_bits),
+                              out.data_ptr(), _stream(a, stream)))
+    return out
+
+
 def dot_partial(a: torch.Tensor, b: torch.Tensor, p: int, rep: int = CLASSICAL, out: torch.Tensor | None = None,
                 stream=None) -> torch.Tensor:
     """This shard's partial residue (int64 device tensor of 1 element) for a later all-reduce + finalize."""
@@ -190,6 +237,27 @@ def dot_batch(A: torch.Tensor, x: torch.Tensor, p: int, rep: int = CLASSICAL, ou
     with torch.cuda.device(A.device):
         _check(lib.gfp_dot_batch(p, rep, _dt(A), A.data_ptr(), lda, x.data_ptr(), rows, n, out.data_ptr(),
                                  _stream(A, stream)))
+    return out
+
+
+def dot_batch_ex(A: torch.Tensor, x: torch.Tensor, p: int, rep: int = CLASSICAL, strategy: int = AUTO,
+                 acc_bits: int = 0, out: torch.Tensor | None = None, rows: int | None = None, n: int | None = None,
+                 lda: int | None = None, stream=None) -> torch.Tensor:
+    """dot_batch with an explicit accumulation strategy (sec. 3) and accumulator width."""
+    if not (A.is_cuda and x.is_cuda) or A.dtype != x.dtype:
+        raise ValueError("A and x must be CUDA tensors of the same dtype")
+    if A.dim() == 2:
+        rows = A.shape[0] if rows is None else rows
+        n = A.shape[1] if n is None else n
+        lda = A.stride(0) if lda is None else lda
+    elif rows is None or n is None:
+        raise ValueError("flat A needs rows and n")
+    lda = n if lda is None else lda
+    if out is None:
+        out = torch.empty(rows, dtype=A.dtype, device=A.device)
+    with torch.cuda.device(A.device):
+        _check(lib.gfp_dot_batch_ex(p, rep, _dt(A), A.data_ptr(), lda, x.data_ptr(), rows, n,
+                                    _opts(strategy, acc_bits), out.data_ptr(), _stream(A, stream)))
     return out
 
 

@@ -95,6 +95,8 @@ gfp_status get_ctx(uint64_t p, gfp_rep rep, gfp_dtype dt, Ctx **out) {
     K.r2 = c->info.r2;
     K.n_im = c->info.n_im;
     K.qbar = (uint32_t)c->info.qbar;
+    K.corr32 = (uint32_t)((((u128)1) << 32) % p);
+    K.mu32 = (uint32_t)(0xFFFFFFFFull / p);
     if (rep == GFP_REP_ZECH) {
         std::vector<uint16_t> logt, anti;
         zech_tables(p, c->info.g, logt, anti);
@@ -155,8 +157,16 @@ gfp_status check_dot_args(gfp_dtype dt, const void *a, const void *b, int64_t n,
     return GFP_OK;
 }
 
+gfp_status plan_fail(gfp_status st) {
+    switch (st) {
+    case GFP_E_BOUND: return fail(st, "(p, n) violates the bound of the requested strategy / accumulator width");
+    case GFP_E_UNSUPPORTED: return fail(st, "strategy or accumulator width not offered for this representation");
+    default: return fail(st, "invalid options");
+    }
+}
+
 gfp_status dot_common(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n, void *out,
-                      int mode, cudaStream_t s) {
+                      int mode, cudaStream_t s, const gfp_options *opt = nullptr) {
     gfp_status st = check_dot_args(dt, a, b, n, out, mode == OUT_ENCODE ? dtype_size(dt) : 8);
     if (st != GFP_OK) return st;
     Ctx *c;
@@ -164,7 +174,7 @@ gfp_status dot_common(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, cons
     Workspace ws;
     if ((st = get_ws(s, &ws)) != GFP_OK) return st;
     DotPlan plan;
-    if ((st = plan_dot(c->info, c->K, a, b, n, &plan)) != GFP_OK) return st;
+    if ((st = plan_dot(c->info, c->K, a, b, n, opt, &plan)) != GFP_OK) return plan_fail(st);
     OutSpec o{out, (int)rep, (int)dt, mode};
     cudaError_t e = launch_dot(plan, c->K, a, b, n, ws, o, s);
     return e == cudaSuccess ? GFP_OK : cuda_fail(e, "dot launch");
@@ -206,8 +216,8 @@ gfp_status gfp_finalize(uint64_t p, gfp_rep rep, gfp_dtype dt, const uint64_t *s
     return e == cudaSuccess ? GFP_OK : cuda_fail(e, "finalize launch");
 }
 
-gfp_status gfp_dot_batch(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *A, int64_t lda, const void *x,
-                         int64_t rows, int64_t n, void *out, void *stream) {
+static gfp_status batch_common(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *A, int64_t lda, const void *x,
+                               int64_t rows, int64_t n, const gfp_options *opt, void *out, void *stream) {
     if ((int)dt < 0 || (int)dt > 2) return fail(GFP_E_INVAL, "unknown dtype");
     if (rows < 0 || n < 0 || lda < n) return fail(GFP_E_INVAL, "need rows >= 0, n >= 0, lda >= n");
     if (rows == 0) return GFP_OK;
@@ -219,9 +229,48 @@ gfp_status gfp_dot_batch(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *A, i
     if (st != GFP_OK) return st;
     OutSpec o{out, (int)rep, (int)dt, OUT_ENCODE};
     cudaError_t e = cudaSuccess;
-    st = launch_batch(c->info, c->K, A, lda, x, rows, n, o, (cudaStream_t)stream, &e);
+    st = launch_batch(c->info, c->K, A, lda, x, rows, n, opt, o, (cudaStream_t)stream, &e);
     if (st == GFP_E_CUDA) return cuda_fail(e, "batch launch");
-    if (st != GFP_OK) return fail(st, "batch: unsupported size for this representation");
+    if (st != GFP_OK) return plan_fail(st);
+    return GFP_OK;
+}
+
+gfp_status gfp_dot_batch(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *A, int64_t lda, const void *x,
+                         int64_t rows, int64_t n, void *out, void *stream) {
+    return batch_common(p, rep, dt, A, lda, x, rows, n, nullptr, out, stream);
+}
+
+gfp_status gfp_dot_batch_ex(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *A, int64_t lda, const void *x,
+                            int64_t rows, int64_t n, const gfp_options *opt, void *out, void *stream) {
+    return batch_common(p, rep, dt, A, lda, x, rows, n, opt, out, stream);
+}
+
+gfp_status gfp_dot_ex(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
+                      const gfp_options *opt, void *out, void *stream) {
+    return dot_common(p, rep, dt, a, b, n, out, OUT_ENCODE, (cudaStream_t)stream, opt);
+}
+
+gfp_status gfp_plan(uint64_t p, gfp_rep rep, gfp_dtype dt, int64_t n, const gfp_options *opt, gfp_plan_info *info) {
+    if (info == nullptr || n < 0) return fail(GFP_E_INVAL, "info is NULL or n < 0");
+    gfp_info I;
+    gfp_status st = gfp_query(p, rep, dt, &I);
+    if (st != GFP_OK) return st;
+    dev::KParams K;  // planning needs only the table size (no device tables are built here)
+    memset(&K, 0, sizeof(K));
+    K.p = p;
+    K.antilog_entries = (uint32_t)((I.table_bytes / 2 + 7) & ~uint64_t(7));
+    DotPlan plan;
+    const void *aligned_ptr = (const void *)(uintptr_t)4096;
+    if ((st = plan_dot(I, K, aligned_ptr, aligned_ptr, n, opt, &plan)) != GFP_OK) return plan_fail(st);
+    memset(info, 0, sizeof(*info));
+    info->strategy = plan.strategy;
+    info->acc_bits = plan.acc_bits;
+    info->block = plan.kblk;
+    info->grid = plan.grid;
+    info->threads_per_block = plan.block;
+    info->terms_per_thread = plan.per_thread;
+    info->reductions_per_thread = plan.reductions;
+    snprintf(info->kernel, sizeof(info->kernel), "%s", plan.name);
     return GFP_OK;
 }
 
@@ -306,8 +355,9 @@ gfp_status gfp_dot_host(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, co
         if (e == cudaSuccess) e = cudaStreamWaitEvent(s, S->copied[slot], 0);
         if (e != cudaSuccess) break;
         DotPlan plan;
-        if ((st = plan_dot(c->info, c->K, S->buf[slot][0], S->buf[slot][1], std::max<int64_t>(len, 0), &plan)) != GFP_OK)
-            return st;
+        if ((st = plan_dot(c->info, c->K, S->buf[slot][0], S->buf[slot][1], std::max<int64_t>(len, 0), nullptr,
+                           &plan)) != GFP_OK)
+            return plan_fail(st);
         OutSpec o{S->d_partial, (int)rep, (int)dt, ci == 0 ? OUT_PARTIAL : OUT_ACCUMULATE};
         e = launch_dot(plan, c->K, S->buf[slot][0], S->buf[slot][1], std::max<int64_t>(len, 0), ws, o, s);
         if (e == cudaSuccess) e = cudaEventRecord(S->consumed[slot], s);

@@ -41,6 +41,15 @@ __device__ __forceinline__ uint64_t mod_p(uint64_t x, uint64_t p, uint64_t mu) {
     return r;
 }
 
+// x mod p for a 32-bit x (p < 2^16 in the m = 32 strategies): q = floor(x mu32 / 2^32) >= floor(x/p) - 2.
+__device__ __forceinline__ uint32_t mod_p32(uint32_t x, uint32_t p, uint32_t mu32) {
+    uint32_t q = __umulhi(x, mu32);
+    uint32_t r = x - q * p;
+    r = r >= p ? r - p : r;
+    r = r >= p ? r - p : r;
+    return r;
+}
+
 // Montgomery reduction (sec. 2.2) with B = 2^32: U = T n_im mod B, returns (T + U p) / B,
 // which is T B^{-1} mod p up to a multiple of p.  The caller guarantees T + U p < 2^64.
 __device__ __forceinline__ uint32_t redc(uint64_t T, uint32_t p, uint32_t n_im) {
@@ -250,6 +259,115 @@ struct Zech {
     }
     __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
         return ALL ? A.s : mod_p(A.s, K.p, K.mu);
+    }
+};
+
+
+// ------------------------------------------------------------------------------ explicit strategies
+// The paper's section-3 accumulation algorithms, selectable through gfp_dot_ex / gfp_dot_batch_ex for
+// classical storage E (u16 / u32) with an m-bit accumulator ACC (u32 or u64).  Every variant is exact;
+// the host checks (p-1)^2 < 2^m and each strategy's bound.  Per thread (the paper's loop is per dot):
+//   S_DELAYED  sec. 3.1, Eq. (1): no reduction until the end (host: the whole dot has n <= k terms)
+//   S_BLOCKED  sec. 3.2 listing P:361-370: reduce every K.kblk = k products (reading G1/G7)
+//   S_OVERFLOW sec. 3.3 listing P:414-422: sum += product; if (sum < product) sum += CORR
+//   S_HYBRID   sec. 3.4, Eq. (2): one wrap test per block of K.kblk = lambda products,
+//              lambda p (p-1) < 2^m; the block sum cannot wrap twice nor re-wrap after CORR
+enum Strategy { S_DELAYED = 1, S_BLOCKED = 2, S_OVERFLOW = 3, S_HYBRID = 4 };
+
+template <typename ACC, typename E, int STRAT>
+struct ClassicalS {
+    using elem = E;
+    static constexpr int W = 16 / sizeof(E);
+    static constexpr bool kTable = false;
+    struct Acc {
+        ACC s, base;
+        uint32_t cnt;
+    };
+    __device__ __forceinline__ static void init(Acc &A) {
+        A.s = 0;
+        A.base = 0;
+        A.cnt = 0;
+    }
+    __device__ __forceinline__ static ACC corr(const KParams &K) {
+        return sizeof(ACC) == 4 ? (ACC)K.corr32 : (ACC)K.corr;
+    }
+    __device__ __forceinline__ static ACC reduce(ACC s, const KParams &K) {
+        if constexpr (sizeof(ACC) == 4)
+            return mod_p32(s, (uint32_t)K.p, K.mu32);
+        else
+            return mod_p(s, K.p, K.mu);
+    }
+    __device__ __forceinline__ static void term(Acc &A, uint32_t x, uint32_t y, const KParams &K,
+                                                const uint16_t * = nullptr) {
+        const ACC prod = (ACC)x * (ACC)y;
+        if (STRAT == S_DELAYED) {
+            A.s += prod;
+        } else if (STRAT == S_BLOCKED) {
+            if (A.cnt == K.kblk) {
+                A.s = reduce(A.s, K);  // res %= P after each block (G1)
+                A.cnt = 0;
+            }
+            A.s += prod;
+            ++A.cnt;
+        } else if (STRAT == S_OVERFLOW) {
+            A.s += prod;
+            if (A.s < prod) A.s += corr(K);
+        } else {  // S_HYBRID
+            A.s += prod;
+            if (++A.cnt == K.kblk) {
+                if (A.s < A.base) A.s += corr(K);
+                A.base = A.s;
+                A.cnt = 0;
+            }
+        }
+    }
+    __device__ __forceinline__ static void vec(Acc &A, uint4 x, uint4 y, const KParams &K, const uint16_t *) {
+        if constexpr (sizeof(E) == 4) {
+            term(A, x.x, y.x, K);
+            term(A, x.y, y.y, K);
+            term(A, x.z, y.z, K);
+            term(A, x.w, y.w, K);
+        } else {
+            const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                term(A, xs[i] & 0xFFFFu, ys[i] & 0xFFFFu, K);
+                term(A, xs[i] >> 16, ys[i] >> 16, K);
+            }
+        }
+    }
+    __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
+        if (STRAT == S_HYBRID && A.s < A.base) A.s += corr(K);  // the last, partial block
+        return (uint64_t)reduce(A.s, K);
+    }
+};
+
+// Overflow-Montgomery (sec. 3.3): the products x~ y~ = ab B^2 are summed with the
+// overflow trick (CORR = 2^64 mod p); each thread then reduces its sum mod p and applies ONE REDC
+// to return to B^1 scale ("one reduction ... to mod out the result, and an additional one to divide
+// the element by B").  The result is the Montgomery form of the dot, like Montgomery<KR>.
+struct MontgomeryOverflow {
+    using elem = uint32_t;
+    static constexpr int W = 4;
+    static constexpr bool kTable = false;
+    struct Acc { uint64_t S; };
+    __device__ __forceinline__ static void init(Acc &A) { A.S = 0; }
+    __device__ __forceinline__ static void term(Acc &A, uint32_t x, uint32_t y, const KParams &K,
+                                                const uint16_t * = nullptr) {
+        const uint64_t prod = (uint64_t)x * y;
+        A.S += prod;
+        if (A.S < prod) A.S += K.corr;
+    }
+    __device__ __forceinline__ static void vec(Acc &A, uint4 x, uint4 y, const KParams &K, const uint16_t *) {
+        term(A, x.x, y.x, K);
+        term(A, x.y, y.y, K);
+        term(A, x.z, y.z, K);
+        term(A, x.w, y.w, K);
+    }
+    __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
+        const uint32_t p = (uint32_t)K.p;
+        const uint32_t r = redc(mod_p(A.S, K.p, K.mu), p, K.n_im);  // T < p <= pB: r <= p
+        return r >= p ? r - p : r;
     }
 };
 

@@ -31,17 +31,23 @@ struct DotPlan {
     size_t smem;
     int64_t head;   // scalar elements before the first 16-byte aligned vector (== n if unaligned)
     int acc;        // gfp_acc reported for the plan
+    int strategy;   // gfp_strategy actually used
+    int acc_bits;   // m of the accumulator
+    uint64_t kblk;  // products per reduction / per wrap test (0: none before the end)
+    int64_t per_thread, reductions;  // bounds per thread
+    const char *name;
 };
 
 // Build a plan: chooses grid, the accumulation policy and its mode for n elements.
 gfp_status plan_dot(const gfp_info &info, const dev::KParams &K, const void *a, const void *b, int64_t n,
-                    DotPlan *plan);
+                    const gfp_options *opt, DotPlan *plan);
 cudaError_t launch_dot(const DotPlan &plan, const dev::KParams &K, const void *a, const void *b, int64_t n,
                        Workspace ws, OutSpec out, cudaStream_t s);
 cudaError_t launch_finalize(const dev::KParams &K, const uint64_t *summed, int count, OutSpec out,
                             cudaStream_t s);
 gfp_status launch_batch(const gfp_info &info, const dev::KParams &K, const void *A, int64_t lda, const void *x,
-                        int64_t rows, int64_t n, OutSpec out, cudaStream_t s, cudaError_t *err);
+                        int64_t rows, int64_t n, const gfp_options *opt, OutSpec out, cudaStream_t s,
+                        cudaError_t *err);
 // dir: 0 = to_rep, 1 = from_rep
 gfp_status launch_convert(const gfp_info &info, const dev::KParams &K, int dir, gfp_dtype in_dt, const void *in,
                           gfp_dtype out_dt, void *out, int64_t n, cudaStream_t s, cudaError_t *err);

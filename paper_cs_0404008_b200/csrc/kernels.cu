@@ -28,8 +28,12 @@ enum Policy {
     P_MONT1, P_MONT2, P_MONT4,
     P_FP_THREAD, P_FP_K1, P_FP_K2,
     P_ZS_ALL, P_ZS_THREAD, P_ZL_ALL, P_ZL_THREAD,
+    // explicit strategies (gfp_dot_ex): P_CS + 8*acc64 + 4*elem32 + (strategy - 1)
+    P_CS = 32, P_CS_END = P_CS + 16,
+    P_MONT_OVF = 64,
     P_COUNT
 };
+constexpr int cs_policy(bool acc64, bool e32, int strat) { return P_CS + 8 * acc64 + 4 * e32 + (strat - 1); }
 
 static thread_local uint64_t t_launches = 0;
 void count_launch() { ++t_launches; }
@@ -411,13 +415,37 @@ static int dot_occupancy(size_t smem) {
     return occupancy(dot_kernel<R, NT, U, PIPE>, NT, smem);
 }
 
-static int policy_block(int pol) { return pol >= P_ZS_ALL ? kZechNT : kDotNT; }
-static int policy_unroll(int pol) { return pol >= P_ZS_ALL ? kZechU : (pol >= P_FP_THREAD ? kFpU : kDotU); }
+static bool is_zech(int pol) { return pol >= P_ZS_ALL && pol <= P_ZL_THREAD; }
+static int policy_block(int pol) { return is_zech(pol) ? kZechNT : kDotNT; }
+static int policy_unroll(int pol) {
+    return is_zech(pol) ? kZechU : ((pol >= P_FP_THREAD && pol <= P_FP_K2) ? kFpU : kDotU);
+}
 static int policy_width(int pol) {
-    if (pol <= P_CL32_OVF || (pol >= P_MONT1 && pol <= P_MONT4)) return 4;
+    if (pol >= P_CS && pol < P_CS_END) return ((pol - P_CS) & 4) ? 4 : 8;
+    if (pol <= P_CL32_OVF || (pol >= P_MONT1 && pol <= P_MONT4) || pol == P_MONT_OVF) return 4;
     if (pol >= P_FP_THREAD && pol <= P_FP_K2) return 2;
     return 8;
 }
+
+// explicit-strategy policy type for (acc64, e32, strategy)
+#define GFP_CS_CASES(M)                                                                     \
+    M(cs_policy(0, 0, 1), ClassicalS<uint32_t, uint16_t, S_DELAYED>)                        \
+    M(cs_policy(0, 0, 2), ClassicalS<uint32_t, uint16_t, S_BLOCKED>)                        \
+    M(cs_policy(0, 0, 3), ClassicalS<uint32_t, uint16_t, S_OVERFLOW>)                       \
+    M(cs_policy(0, 0, 4), ClassicalS<uint32_t, uint16_t, S_HYBRID>)                         \
+    M(cs_policy(0, 1, 1), ClassicalS<uint32_t, uint32_t, S_DELAYED>)                        \
+    M(cs_policy(0, 1, 2), ClassicalS<uint32_t, uint32_t, S_BLOCKED>)                        \
+    M(cs_policy(0, 1, 3), ClassicalS<uint32_t, uint32_t, S_OVERFLOW>)                       \
+    M(cs_policy(0, 1, 4), ClassicalS<uint32_t, uint32_t, S_HYBRID>)                         \
+    M(cs_policy(1, 0, 1), ClassicalS<uint64_t, uint16_t, S_DELAYED>)                        \
+    M(cs_policy(1, 0, 2), ClassicalS<uint64_t, uint16_t, S_BLOCKED>)                        \
+    M(cs_policy(1, 0, 3), ClassicalS<uint64_t, uint16_t, S_OVERFLOW>)                       \
+    M(cs_policy(1, 0, 4), ClassicalS<uint64_t, uint16_t, S_HYBRID>)                         \
+    M(cs_policy(1, 1, 1), ClassicalS<uint64_t, uint32_t, S_DELAYED>)                        \
+    M(cs_policy(1, 1, 2), ClassicalS<uint64_t, uint32_t, S_BLOCKED>)                        \
+    M(cs_policy(1, 1, 3), ClassicalS<uint64_t, uint32_t, S_OVERFLOW>)                       \
+    M(cs_policy(1, 1, 4), ClassicalS<uint64_t, uint32_t, S_HYBRID>)                         \
+    M(P_MONT_OVF, MontgomeryOverflow)
 
 static int policy_occupancy(int pol, size_t smem) {
     switch (pol) {
@@ -436,12 +464,18 @@ static int policy_occupancy(int pol, size_t smem) {
     case P_ZS_THREAD: return dot_occupancy<Zech<true, false>, kZechNT, kZechU, true>(smem);
     case P_ZL_ALL: return dot_occupancy<Zech<false, true>, kZechNT, kZechU, true>(smem);
     case P_ZL_THREAD: return dot_occupancy<Zech<false, false>, kZechNT, kZechU, true>(smem);
+#define GFP_OCC(pol, ...) \
+    case pol: return dot_occupancy<__VA_ARGS__, kDotNT, kDotU, false>(smem);
+        GFP_CS_CASES(GFP_OCC)
+#undef GFP_OCC
     }
     return 1;
 }
 
-cudaError_t launch_dot(const DotPlan &P, const KParams &K, const void *a, const void *b, int64_t n, Workspace ws,
+cudaError_t launch_dot(const DotPlan &P, const KParams &K0, const void *a, const void *b, int64_t n, Workspace ws,
                        OutSpec O, cudaStream_t s) {
+    KParams K = K0;
+    K.kblk = P.kblk;
     switch (P.policy) {
     case P_CL32_ALL: return launch_dot_t<ClassicalU32<CL_ALL>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
     case P_CL32_THREAD: return launch_dot_t<ClassicalU32<CL_THREAD>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
@@ -458,13 +492,101 @@ cudaError_t launch_dot(const DotPlan &P, const KParams &K, const void *a, const 
     case P_ZS_THREAD: return launch_dot_t<Zech<true, false>, kZechNT, kZechU, true>(P, K, a, b, n, ws, O, s);
     case P_ZL_ALL: return launch_dot_t<Zech<false, true>, kZechNT, kZechU, true>(P, K, a, b, n, ws, O, s);
     case P_ZL_THREAD: return launch_dot_t<Zech<false, false>, kZechNT, kZechU, true>(P, K, a, b, n, ws, O, s);
+#define GFP_LAUNCH(pol, ...) \
+    case pol: return launch_dot_t<__VA_ARGS__, kDotNT, kDotU, false>(P, K, a, b, n, ws, O, s);
+        GFP_CS_CASES(GFP_LAUNCH)
+#undef GFP_LAUNCH
     }
     return cudaErrorInvalidValue;
 }
 
 static size_t elem_size(int dt) { return dt == GFP_U16 ? 2 : (dt == GFP_U32 ? 4 : 8); }
 
-gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const void *b, int64_t n, DotPlan *P) {
+// Explicit strategy (gfp_options) -> policy and block length; GFP_OK or the reason it is not admissible.
+static gfp_status resolve_strategy(const gfp_info &I, int64_t n, const gfp_options *opt, int *pol, uint64_t *kblk,
+                                   int *acc_bits) {
+    const int strat = opt ? opt->strategy : GFP_STRAT_AUTO;
+    const int bits = opt ? opt->acc_bits : 0;
+    *kblk = 0;
+    *acc_bits = I.acc_bits;
+    if (strat < GFP_STRAT_AUTO || strat > GFP_STRAT_HYBRID) return GFP_E_INVAL;
+    if (strat == GFP_STRAT_AUTO && bits == 0) return GFP_OK;
+    const uint64_t pm1 = I.p - 1;
+    const u128 q2 = (u128)pm1 * pm1;
+    switch (I.rep) {
+    case GFP_REP_CLASSICAL: {
+        if (bits != 0 && bits != 32 && bits != 64) return GFP_E_INVAL;
+        const int m = bits ? bits : 64;
+        const u128 wmax = m == 64 ? (~(u128)0 >> 64) : (((u128)1 << 32) - 1);  // 2^m - 1
+        if (q2 + pm1 > wmax) return GFP_E_BOUND;  // an AXPY must fit the m-bit word
+        const int s = strat == GFP_STRAT_AUTO ? GFP_STRAT_BLOCKED : strat;
+        if (s == GFP_STRAT_DELAYED && (u128)n * q2 > wmax) return GFP_E_BOUND;  // Eq. (1): n <= k
+        if (s == GFP_STRAT_BLOCKED) *kblk = q2 == 0 ? UINT64_MAX : (uint64_t)std::min<u128>((wmax - pm1) / q2, UINT64_MAX);
+        if (s == GFP_STRAT_HYBRID) {
+            const u128 pp = (u128)I.p * pm1;  // Eq. (2): lambda p (p-1) < 2^m
+            *kblk = (uint64_t)std::min<u128>(wmax / pp, UINT64_MAX);
+            if (*kblk == 0) return GFP_E_BOUND;
+        }
+        *pol = cs_policy(m == 64, I.dtype == GFP_U32, s);
+        *acc_bits = m;
+        return GFP_OK;
+    }
+    case GFP_REP_MONTGOMERY:
+        if (bits != 0 && bits != 64) return GFP_E_INVAL;
+        if (strat == GFP_STRAT_OVERFLOW) *pol = P_MONT_OVF;
+        else if (strat != GFP_STRAT_AUTO && strat != GFP_STRAT_BLOCKED) return GFP_E_UNSUPPORTED;
+        return GFP_OK;
+    case GFP_REP_FP64:
+        if (bits != 0 && bits != 53) return GFP_E_INVAL;
+        if (strat == GFP_STRAT_DELAYED) {
+            if ((u128)n * q2 >= ((u128)1 << 53)) return GFP_E_BOUND;
+            *pol = P_FP_THREAD;
+        } else if (strat == GFP_STRAT_BLOCKED) {
+            *pol = I.k >= 2 ? P_FP_K2 : P_FP_K1;
+        } else if (strat != GFP_STRAT_AUTO) {
+            return GFP_E_UNSUPPORTED;
+        }
+        return GFP_OK;
+    case GFP_REP_ZECH:
+        return (strat == GFP_STRAT_AUTO && (bits == 0 || bits == 64)) ? GFP_OK : GFP_E_UNSUPPORTED;
+    }
+    return GFP_E_INVAL;
+}
+
+static const char *policy_name(int pol) {
+    switch (pol) {
+    case P_CL32_ALL: return "dot_kernel<ClassicalU32<ALL>>";
+    case P_CL32_THREAD: return "dot_kernel<ClassicalU32<THREAD>>";
+    case P_CL32_OVF: return "dot_kernel<ClassicalU32<OVERFLOW>>";
+    case P_CL16_ALL: return "dot_kernel<ClassicalU16<ALL>>";
+    case P_CL16_THREAD: return "dot_kernel<ClassicalU16<THREAD>>";
+    case P_MONT1: return "dot_kernel<Montgomery<1>>";
+    case P_MONT2: return "dot_kernel<Montgomery<2>>";
+    case P_MONT4: return "dot_kernel<Montgomery<4>>";
+    case P_FP_THREAD: return "dot_kernel<Fp64<0>>";
+    case P_FP_K1: return "dot_kernel<Fp64<1>>";
+    case P_FP_K2: return "dot_kernel<Fp64<2>>";
+    case P_ZS_ALL: return "dot_kernel<Zech<SMALL,ALL>>";
+    case P_ZS_THREAD: return "dot_kernel<Zech<SMALL,THREAD>>";
+    case P_ZL_ALL: return "dot_kernel<Zech<LARGE,ALL>>";
+    case P_ZL_THREAD: return "dot_kernel<Zech<LARGE,THREAD>>";
+    case P_MONT_OVF: return "dot_kernel<MontgomeryOverflow>";
+    }
+    if (pol >= P_CS && pol < P_CS_END) {
+        static const char *names[16] = {
+            "ClassicalS<u32acc,u16,DELAYED>", "ClassicalS<u32acc,u16,BLOCKED>", "ClassicalS<u32acc,u16,OVERFLOW>",
+            "ClassicalS<u32acc,u16,HYBRID>", "ClassicalS<u32acc,u32,DELAYED>", "ClassicalS<u32acc,u32,BLOCKED>",
+            "ClassicalS<u32acc,u32,OVERFLOW>", "ClassicalS<u32acc,u32,HYBRID>", "ClassicalS<u64acc,u16,DELAYED>",
+            "ClassicalS<u64acc,u16,BLOCKED>", "ClassicalS<u64acc,u16,OVERFLOW>", "ClassicalS<u64acc,u16,HYBRID>",
+            "ClassicalS<u64acc,u32,DELAYED>", "ClassicalS<u64acc,u32,BLOCKED>", "ClassicalS<u64acc,u32,OVERFLOW>",
+            "ClassicalS<u64acc,u32,HYBRID>"};
+        return names[pol - P_CS];
+    }
+    return "?";
+}
+
+gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const void *b, int64_t n,
+                    const gfp_options *opt, DotPlan *P) {
     const size_t es = elem_size(I.dtype);
     const uint64_t pm1 = I.p - 1;
     const u128 q2 = (u128)pm1 * pm1;
@@ -479,6 +601,11 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
     case GFP_REP_FP64: pol = I.k >= 2 ? P_FP_K2 : P_FP_K1; break;
     case GFP_REP_ZECH: pol = zech_small_layout(I.p) ? P_ZS_ALL : P_ZL_ALL; break;
     }
+    int xpol = -1, acc_bits = I.acc_bits;
+    uint64_t kblk = 0;
+    gfp_status st = resolve_strategy(I, n, opt, &xpol, &kblk, &acc_bits);
+    if (st != GFP_OK) return st;
+    if (xpol >= 0) pol = xpol;
     const int NT = policy_block(pol), U = policy_unroll(pol), W = policy_width(pol);
     const uintptr_t pa = (uintptr_t)a, pb = (uintptr_t)b;
     int64_t head = n;
@@ -498,35 +625,60 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
     const int64_t iters = (nvec + threads * U - 1) / (threads * U);
     const u128 per_thread = (u128)iters * U * W + (head + threads - 1) / threads + 1;
 
-    int acc = GFP_ACC_DELAYED;
-    switch (I.rep) {
-    case GFP_REP_CLASSICAL:
-        if ((u128)n * q2 <= max64)
-            pol = I.dtype == GFP_U16 ? P_CL16_ALL : P_CL32_ALL;  // Eq. (1): k > n, one final remainder
-        else if (per_thread * q2 <= max64)
-            pol = I.dtype == GFP_U16 ? P_CL16_THREAD : P_CL32_THREAD;
-        else {
-            pol = P_CL32_OVF;  // sec. 3.3 overflow detection (u16 products never need it)
-            acc = GFP_ACC_OVERFLOW;
-        }
-        break;
-    case GFP_REP_MONTGOMERY:
-        acc = GFP_ACC_BLOCKED;
-        break;
-    case GFP_REP_FP64:
-        if (per_thread * q2 < ((u128)1 << 53))
-            pol = P_FP_THREAD;
-        else
+    int acc = GFP_ACC_DELAYED, strat = GFP_STRAT_DELAYED;
+    int64_t reductions = 1;  // per thread, bound (delayed: the one final reduction)
+    if (xpol < 0) {
+        switch (I.rep) {
+        case GFP_REP_CLASSICAL:
+            if ((u128)n * q2 <= max64) {
+                pol = I.dtype == GFP_U16 ? P_CL16_ALL : P_CL32_ALL;  // Eq. (1): k > n, one final remainder
+                reductions = 0;
+            } else if (per_thread * q2 <= max64) {
+                pol = I.dtype == GFP_U16 ? P_CL16_THREAD : P_CL32_THREAD;
+            } else {
+                pol = P_CL32_OVF;  // sec. 3.3 overflow detection (u16 products never need it)
+                acc = GFP_ACC_OVERFLOW;
+                strat = GFP_STRAT_OVERFLOW;
+                reductions = (int64_t)per_thread;  // one wrap test per term
+            }
+            break;
+        case GFP_REP_MONTGOMERY:
             acc = GFP_ACC_BLOCKED;
-        break;
-    case GFP_REP_ZECH: {
-        const bool small = zech_small_layout(I.p);
-        if ((u128)n * pm1 <= max64)
-            pol = small ? P_ZS_ALL : P_ZL_ALL;
-        else
-            pol = small ? P_ZS_THREAD : P_ZL_THREAD;
-        break;
-    }
+            strat = GFP_STRAT_BLOCKED;
+            kblk = pol == P_MONT4 ? 4 : (pol == P_MONT2 ? 2 : 1);
+            reductions = (int64_t)(per_thread / kblk) + 1;  // REDCs
+            break;
+        case GFP_REP_FP64:
+            if (per_thread * q2 < ((u128)1 << 53)) {
+                pol = P_FP_THREAD;
+            } else {
+                acc = GFP_ACC_BLOCKED;
+                strat = GFP_STRAT_BLOCKED;
+                kblk = pol == P_FP_K2 ? 2 : 1;
+                reductions = (int64_t)(per_thread / kblk) + 1;
+            }
+            break;
+        case GFP_REP_ZECH: {
+            const bool small = zech_small_layout(I.p);
+            if ((u128)n * pm1 <= max64) {
+                pol = small ? P_ZS_ALL : P_ZL_ALL;
+                reductions = 0;
+            } else {
+                pol = small ? P_ZS_THREAD : P_ZL_THREAD;
+            }
+            break;
+        }
+        }
+    } else {
+        strat = (pol >= P_CS && pol < P_CS_END) ? ((pol - P_CS) & 3) + 1
+                : (pol == P_MONT_OVF ? GFP_STRAT_OVERFLOW : (opt ? opt->strategy : GFP_STRAT_AUTO));
+        if (strat == GFP_STRAT_AUTO) strat = GFP_STRAT_BLOCKED;
+        acc = strat == GFP_STRAT_OVERFLOW || strat == GFP_STRAT_HYBRID ? GFP_ACC_OVERFLOW
+              : (strat == GFP_STRAT_BLOCKED ? GFP_ACC_BLOCKED : GFP_ACC_DELAYED);
+        if (pol == P_FP_K2 || pol == P_FP_K1) kblk = pol == P_FP_K2 ? 2 : 1;
+        if (strat == GFP_STRAT_OVERFLOW) reductions = (int64_t)per_thread;
+        else if (strat == GFP_STRAT_BLOCKED || strat == GFP_STRAT_HYBRID)
+            reductions = (int64_t)(kblk ? per_thread / kblk : 0) + 1;
     }
     P->policy = pol;
     P->grid = (int)grid;
@@ -534,6 +686,12 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
     P->smem = smem;
     P->head = head;
     P->acc = acc;
+    P->strategy = strat;
+    P->acc_bits = acc_bits;
+    P->kblk = kblk;
+    P->per_thread = (int64_t)per_thread;
+    P->reductions = reductions;
+    P->name = policy_name(pol);
     return GFP_OK;
 }
 
@@ -568,7 +726,7 @@ static cudaError_t launch_batch_t(const KParams &K, const void *A, int64_t lda, 
 }
 
 gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int64_t lda, const void *x, int64_t rows,
-                        int64_t n, OutSpec O, cudaStream_t s, cudaError_t *err) {
+                        int64_t n, const gfp_options *opt, OutSpec O, cudaStream_t s, cudaError_t *err) {
     const size_t es = elem_size(I.dtype);
     const bool vec = ((uintptr_t)A % 16 == 0) && ((uintptr_t)x % 16 == 0) && ((lda * (int64_t)es) % 16 == 0);
     const uint64_t pm1 = I.p - 1;
@@ -577,6 +735,27 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
     int dev = 0;
     cudaGetDevice(&dev);
     *err = cudaSuccess;
+    {  // explicit strategy (gfp_dot_batch_ex): the generic warp-per-row kernel with that policy
+        int xpol = -1, acc_bits = 0;
+        uint64_t kblk = 0;
+        gfp_status st = resolve_strategy(I, n, opt, &xpol, &kblk, &acc_bits);
+        if (st != GFP_OK) return st;
+        if (xpol >= 0) {
+            KParams K2 = K;
+            K2.kblk = kblk;
+            switch (xpol) {
+#define GFP_BATCH(pol, ...) \
+    case pol: *err = launch_batch_t<__VA_ARGS__, 256, 4>(K2, A, lda, x, rows, n, vec, O, s); break;
+                GFP_CS_CASES(GFP_BATCH)
+#undef GFP_BATCH
+            case P_FP_THREAD: *err = launch_batch_t<Fp64<0>, 256, 4>(K2, A, lda, x, rows, n, vec, O, s); break;
+            case P_FP_K2: *err = launch_batch_t<Fp64<2>, 256, 4>(K2, A, lda, x, rows, n, vec, O, s); break;
+            case P_FP_K1: *err = launch_batch_t<Fp64<1>, 256, 4>(K2, A, lda, x, rows, n, vec, O, s); break;
+            default: return GFP_E_UNSUPPORTED;
+            }
+            return *err == cudaSuccess ? GFP_OK : GFP_E_CUDA;
+        }
+    }
     switch (I.rep) {
     case GFP_REP_CLASSICAL:
         if (I.dtype == GFP_U16) {

@@ -17,6 +17,10 @@ struct KParams {
     const uint16_t *antilog;  // Zech antilog table (global; staged to shared memory by the kernel)
     const uint16_t *logt;     // Zech log table (global; read once by the finaliser)
     uint32_t antilog_entries;
+    // explicit-strategy kernels (gfp_dot_ex): block length for BLOCKED / HYBRID, 32-bit constants
+    uint64_t kblk;
+    uint32_t corr32;    // 2^32 mod p
+    uint32_t mu32;      // floor((2^32 - 1) / p)
 };
 
 }  // namespace dev

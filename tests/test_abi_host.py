@@ -153,3 +153,50 @@ def test_argument_errors_before_device_work():
     assert L.gfp_to_rep(7, MO, U32, fake, U32, out, 0, None) == OK  # n == 0: no-op
     assert L.gfp_to_rep(7, MO, U16, fake, U32, fake, 4, None) == E_INVAL  # in-place needs equal dtypes
     assert L.gfp_status_str(E_BOUND).startswith(b"GFP_E_BOUND")
+
+
+# ------------------------------------------------------------------------------ explicit strategies (F2)
+def test_plan_block_lengths_match_the_paper():
+    """m = 32 accumulators at DIM = 512 (sec. 3.4): the blocked k (Eq. (1), reading G7)
+    is >= 512 up to p = 2897 and below from the next prime; the hybrid lambda of Eq. (2),
+    lambda p(p-1) < 2^32, is >= 512 up to 2887 (reading G4)."""
+    P = gfp.plan
+    assert P(2897, CL, 512, strategy=gfp.BLOCKED, acc_bits=32)["block"] == 512
+    assert P(2903, CL, 512, strategy=gfp.BLOCKED, acc_bits=32)["block"] == 509
+    assert P(2887, CL, 512, strategy=gfp.HYBRID, acc_bits=32)["block"] >= 512
+    assert P(2897, CL, 512, strategy=gfp.HYBRID, acc_bits=32)["block"] == 511
+    for p in [3, 101, 2897, 40009, 65521]:
+        for m in (32, 64):
+            k = P(p, CL, 512, strategy=gfp.BLOCKED, acc_bits=m)["block"]
+            assert k * (p - 1) ** 2 + (p - 1) <= 2 ** m - 1 < (k + 1) * (p - 1) ** 2 + (p - 1)
+            lam = P(p, CL, 512, strategy=gfp.HYBRID, acc_bits=m)["block"]
+            assert lam * p * (p - 1) < 2 ** m <= (lam + 1) * p * (p - 1)
+    assert P(40009, CL, 10 ** 6, strategy=gfp.DELAYED)["kernel"].endswith("DELAYED>")
+    assert P(65521, CL, 10 ** 6, strategy=gfp.OVERFLOW, acc_bits=32)["reductions_per_thread"] >= 1
+
+
+def test_plan_rejections():
+    P = gfp.plan
+    with pytest.raises(gfp.GfpError) as e:
+        P(65537, CL, 10, dtype=__import__("torch").uint32, strategy=gfp.BLOCKED, acc_bits=32)
+    assert e.value.status == E_BOUND  # (p-1)^2 + (p-1) >= 2^32
+    with pytest.raises(gfp.GfpError) as e:
+        P(65521, CL, 2, strategy=gfp.DELAYED, acc_bits=32)  # 2 (p-1)^2 > 2^32: Eq. (1) violated
+    assert e.value.status == E_BOUND
+    with pytest.raises(gfp.GfpError) as e:
+        P(4294967291, CL, 3, strategy=gfp.DELAYED)
+    assert e.value.status == E_BOUND
+    with pytest.raises(gfp.GfpError) as e:
+        P(2 ** 31 - 1, MO, 10, strategy=gfp.HYBRID)
+    assert e.value.status == E_UNSUPPORTED
+    with pytest.raises(gfp.GfpError) as e:
+        P(32749, ZE, 10, strategy=gfp.BLOCKED)
+    assert e.value.status == E_UNSUPPORTED
+    with pytest.raises(gfp.GfpError) as e:
+        P(67108859, FP, 10, strategy=gfp.OVERFLOW)
+    assert e.value.status == E_UNSUPPORTED
+    with pytest.raises(gfp.GfpError) as e:
+        P(65521, CL, 10, strategy=gfp.BLOCKED, acc_bits=48)
+    assert e.value.status == E_INVAL
+    assert P(2 ** 31 - 1, MO, 10, strategy=gfp.OVERFLOW)["kernel"] == "dot_kernel<MontgomeryOverflow>"
+    assert P(67108859, FP, 2, strategy=gfp.DELAYED)["kernel"] == "dot_kernel<Fp64<0>>"
