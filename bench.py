@@ -339,6 +339,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--oracle-budget", type=float, default=12.0, help="seconds of oracle work per sample")
+    ap.add_argument("--sweep", default=None, metavar="OUT.jsonl",
+                    help="SURVEY 8(f) F1: paper-shaped prime sweep of DIM=512 batched dots per strategy, "
+                         "written to OUT.jsonl (one GPU)")
+    ap.add_argument("--sweep-rows", type=int, default=1 << 19)
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.warmup < 3 and args.impl == "ours":
@@ -348,6 +352,8 @@ def main():
 
     if args.impl == "reference":
         return reference_arm(args, cfg, world, rank)
+    if args.sweep:
+        return prime_sweep(args)
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -544,6 +550,96 @@ def secondary_table(gfp, args, dev, stream, exclude):
         del d, reps, step, ev, out, g
         torch.cuda.empty_cache()
     return table
+
+
+def sweep_primes(gfp):
+    """~48 log-spaced primes in [3, 65521] + the paper's landmarks, and word-size primes for u32 storage.
+    Primality from the library's own gfp_query (GFP_E_NOT_PRIME)."""
+    def prime(q):
+        try:
+            gfp.query(q, gfp.CLASSICAL, torch.uint32)
+            return True
+        except gfp.GfpError:
+            return False
+
+    def prev_prime(x):
+        while x > 2 and not prime(x):
+            x -= 1
+        return x
+    small = sorted({prev_prime(int(round(3 * (65521 / 3) ** (i / 47)))) for i in range(48)} |
+                   {3, 2887, 2897, 2903, 32749, 40009, 40499, 46337, 65521})
+    large = [65537, prev_prime(1 << 20), prev_prime(1 << 24), prev_prime(1 << 28), 2 ** 31 - 1, 3037000493,
+             4294967291]
+    return small, large
+
+
+def prime_sweep(args):
+    """F1: many independent length-512 dots (gfp_dot_batch_ex, classical) per prime and per strategy of the
+    paper, with 32-bit accumulators where admissible (the m of Figs. 7-8) and 64-bit ones.  Each cell is
+    timed by CUDA-graph replay over >= 3x L2 of rows and checked bit-for-bit against the library's
+    default plan (itself oracle-checked in tests/)."""
+    import paper_cs_0404008_b200 as gfp
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(device=dev)
+    small, large = sweep_primes(gfp)
+    rows, n = args.sweep_rows, 512
+    peak, _ = peak_hbm()
+    strategies = [("auto", gfp.AUTO, 0), ("blocked32", gfp.BLOCKED, 32), ("overflow32", gfp.OVERFLOW, 32),
+                  ("hybrid32", gfp.HYBRID, 32), ("blocked64", gfp.BLOCKED, 64), ("overflow64", gfp.OVERFLOW, 64),
+                  ("hybrid64", gfp.HYBRID, 64)]
+    cells = []
+    out = open(args.sweep, "w")
+    for p in small + large:
+        dt_np, dt_t = (np.uint16, torch.uint16) if p <= 65521 else (np.uint32, torch.uint32)
+        A = torch.from_numpy(synth.uniform(synth.BASE_SEED + 5, synth.STREAM_MAT, 0, rows * n, p, dt_np)).to(dev)
+        x = torch.from_numpy(synth.uniform(synth.BASE_SEED + 5, synth.STREAM_X, 0, n, p, dt_np)).to(dev)
+        A = A.view(rows, n)
+        torch.cuda.synchronize()
+        ref = gfp.dot_batch(A, x, p, gfp.CLASSICAL)
+        nbytes = A.numel() * A.element_size() + n * A.element_size() + rows * A.element_size()
+        for name, strat, m in strategies:
+            try:
+                pl = gfp.plan(p, gfp.CLASSICAL, n, dtype=dt_t, strategy=strat, acc_bits=m)
+            except gfp.GfpError:
+                continue
+            o = torch.empty(rows, dtype=dt_t, device=dev)
+            with torch.cuda.stream(stream):
+                gfp.dot_batch_ex(A, x, p, gfp.CLASSICAL, strategy=strat, acc_bits=m, out=o, stream=stream)
+                stream.synchronize()
+                ok = bool(torch.equal(o, ref))
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for _ in range(4):
+                        gfp.dot_batch_ex(A, x, p, gfp.CLASSICAL, strategy=strat, acc_bits=m, out=o, stream=stream)
+                g.replay()
+                stream.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(5):
+                    g.replay()
+                e1.record(stream)
+                stream.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / 20
+            blk = pl["block"] if pl["block"] else None
+            cell = {"p": p, "strategy": name, "acc_bits": pl["acc_bits"], "block_k": blk,
+                    "reductions_per_dim512_sequential": (None if not blk else -(-n // blk)) if name != "auto" else 1,
+                    "terms_per_lane": n // 32,
+                    "reductions_per_lane": (None if not blk else -(-(n // 32) // blk)),
+                    "us": us, "terms_per_s": rows * n / (us / 1e6), "GB/s": nbytes / (us / 1e6) / 1e9,
+                    "frac_of_measured_hbm": nbytes / (us / 1e6) / 1e9 / peak, "equal_to_default": ok}
+            cells.append(cell)
+            out.write(json.dumps(cell) + "\n")
+            out.flush()
+        del A, x, ref
+        torch.cuda.empty_cache()
+    out.close()
+    bad = [c for c in cells if not c["equal_to_default"]]
+    summary = {"sweep": args.sweep, "cells": len(cells), "primes": len(small) + len(large), "dim": n, "rows": rows,
+               "all_equal_to_default": not bad,
+               "min_terms_per_s": min(c["terms_per_s"] for c in cells),
+               "max_terms_per_s": max(c["terms_per_s"] for c in cells)}
+    print(json.dumps(summary), flush=True)
 
 
 def reference_arm(args, cfg, world, rank):
