@@ -321,7 +321,42 @@ struct ClassicalS {
             }
         }
     }
+    __device__ __forceinline__ static void raw(Acc &A, uint4 x, uint4 y) {
+        if constexpr (sizeof(E) == 4) {
+            A.s += (ACC)x.x * (ACC)y.x;
+            A.s += (ACC)x.y * (ACC)y.y;
+            A.s += (ACC)x.z * (ACC)y.z;
+            A.s += (ACC)x.w * (ACC)y.w;
+        } else {
+            const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                A.s += (ACC)(xs[i] & 0xFFFFu) * (ACC)(ys[i] & 0xFFFFu);
+                A.s += (ACC)(xs[i] >> 16) * (ACC)(ys[i] >> 16);
+            }
+        }
+    }
     __device__ __forceinline__ static void vec(Acc &A, uint4 x, uint4 y, const KParams &K, const uint16_t *) {
+        if ((STRAT == S_BLOCKED || STRAT == S_HYBRID) && K.kblk >= (uint64_t)W) {
+            // block bookkeeping once per 16-byte vector: close the block first if W more products
+            // would exceed k (BLOCKED: reduce; HYBRID: the one wrap test of the block)
+            if (A.cnt + W > K.kblk) {
+                if (STRAT == S_BLOCKED) {
+                    A.s = reduce(A.s, K);
+                } else {
+                    if (A.s < A.base) A.s += corr(K);
+                    A.base = A.s;
+                }
+                A.cnt = 0;
+            }
+            raw(A, x, y);
+            A.cnt += W;
+            return;
+        }
+        if (STRAT == S_DELAYED) {
+            raw(A, x, y);
+            return;
+        }
         if constexpr (sizeof(E) == 4) {
             term(A, x.x, y.x, K);
             term(A, x.y, y.y, K);

@@ -203,7 +203,17 @@ __global__ void finalize_kernel(const uint64_t *summed, int count, KParams K, Ou
 // packed pair of A entries  dp2a_lo(A2, w) = a0 x0_lo + a1 x1_lo  and  dp2a_hi(A2, w) = a0 x0_hi + a1 x1_hi,
 // each < 2^25.  Row value = sum lo + 256 * sum hi, accumulated in u64 per lane (no reduction, the
 // row total n (p-1)^2 < 2^64 is host-checked; Eq. (1)), then one mod p per row.
-template <int NT, int U>
+// Segmented sum over aligned groups of L lanes (L a power of two <= 32).
+template <int L>
+__device__ __forceinline__ uint64_t group_sum(uint64_t v) {
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+
+// LPR lanes per row (32: a warp per long row; 8: four short rows per warp, so DIM = 512 rows still
+// keep 8 vectors per lane in flight and pay a 3-step instead of a 5-step shuffle per row).
+template <int NT, int U, int LPR>
 __global__ void __launch_bounds__(NT) batch_cl16_kernel(const uint16_t *__restrict__ A, int64_t lda,
                                                         const uint16_t *__restrict__ x, int64_t rows, int64_t n,
                                                         KParams K, OutSpec O) {
@@ -215,56 +225,62 @@ __global__ void __launch_bounds__(NT) batch_cl16_kernel(const uint16_t *__restri
         s_xw[j] = (x0 & 0xFFu) | ((x1 & 0xFFu) << 8) | ((x0 >> 8) << 16) | ((x1 >> 8) << 24);
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31;
+    constexpr int RPW = 32 / LPR;  // rows per warp
+    const int lane = threadIdx.x & 31, g = lane % LPR;
     const int64_t nvec = n / 8;
     const uint4 *xv = reinterpret_cast<const uint4 *>(s_xw);
-    for (int64_t row = (int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); row < rows;
-         row += (int64_t)gridDim.x * (NT / 32)) {
-        const uint16_t *Ar = A + row * lda;
+    const int64_t warp0 = (int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
+    const int64_t wstride = (int64_t)gridDim.x * (NT / 32);
+    for (int64_t rbase = warp0 * RPW; rbase < rows; rbase += wstride * RPW) {
+        const int64_t row = rbase + lane / LPR;
+        const bool valid = row < rows;
+        const uint16_t *Ar = A + (valid ? row : 0) * lda;
         const uint4 *av = reinterpret_cast<const uint4 *>(Ar);
         uint64_t tot = 0;
-        int64_t v0 = lane;
-        // full chunks: U unpredicated 16-byte loads per lane in flight, then 8 DP2A per vector
-        for (; v0 + 32 * (U - 1) < nvec; v0 += 32 * U) {
-            uint4 ra[U];
+        int64_t v0 = g;
+        if (valid) {
+            // full chunks: U unpredicated 16-byte loads per lane in flight, then 8 DP2A per vector
+            for (; v0 + LPR * (U - 1) < nvec; v0 += LPR * U) {
+                uint4 ra[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) ra[u] = ld_stream(av + v0 + u * 32);
-            uint32_t lo = 0, hi = 0;  // <= 4U dp2a of < 2^25 each: no wrap for U <= 32
+                for (int u = 0; u < U; ++u) ra[u] = ld_stream(av + v0 + u * LPR);
+                uint32_t lo = 0, hi = 0;  // <= 4U dp2a of < 2^25 each: no wrap for U <= 32
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint4 w = xv[v0 + u * 32];
-                lo = __dp2a_lo(ra[u].x, w.x, lo);
-                hi = __dp2a_hi(ra[u].x, w.x, hi);
-                lo = __dp2a_lo(ra[u].y, w.y, lo);
-                hi = __dp2a_hi(ra[u].y, w.y, hi);
-                lo = __dp2a_lo(ra[u].z, w.z, lo);
-                hi = __dp2a_hi(ra[u].z, w.z, hi);
-                lo = __dp2a_lo(ra[u].w, w.w, lo);
-                hi = __dp2a_hi(ra[u].w, w.w, hi);
+                for (int u = 0; u < U; ++u) {
+                    const uint4 w = xv[v0 + u * LPR];
+                    lo = __dp2a_lo(ra[u].x, w.x, lo);
+                    hi = __dp2a_hi(ra[u].x, w.x, hi);
+                    lo = __dp2a_lo(ra[u].y, w.y, lo);
+                    hi = __dp2a_hi(ra[u].y, w.y, hi);
+                    lo = __dp2a_lo(ra[u].z, w.z, lo);
+                    hi = __dp2a_hi(ra[u].z, w.z, hi);
+                    lo = __dp2a_lo(ra[u].w, w.w, lo);
+                    hi = __dp2a_hi(ra[u].w, w.w, hi);
+                }
+                tot += (uint64_t)lo + ((uint64_t)hi << 8);
             }
-            tot += (uint64_t)lo + ((uint64_t)hi << 8);
+            for (; v0 < nvec; v0 += LPR) {  // remaining vectors of the row
+                const uint4 ra = ld_stream(av + v0), w = xv[v0];
+                uint32_t lo = __dp2a_lo(ra.x, w.x, 0u), hi = __dp2a_hi(ra.x, w.x, 0u);
+                lo = __dp2a_lo(ra.y, w.y, lo);
+                hi = __dp2a_hi(ra.y, w.y, hi);
+                lo = __dp2a_lo(ra.z, w.z, lo);
+                hi = __dp2a_hi(ra.z, w.z, hi);
+                lo = __dp2a_lo(ra.w, w.w, lo);
+                hi = __dp2a_hi(ra.w, w.w, hi);
+                tot += (uint64_t)lo + ((uint64_t)hi << 8);
+            }
+            for (int64_t j = nvec * 8 + g; j < n; j += LPR) tot += (uint64_t)Ar[j] * x[j];
         }
-        for (; v0 < nvec; v0 += 32) {  // remaining vectors of the row
-            const uint4 ra = ld_stream(av + v0), w = xv[v0];
-            uint32_t lo = __dp2a_lo(ra.x, w.x, 0u), hi = __dp2a_hi(ra.x, w.x, 0u);
-            lo = __dp2a_lo(ra.y, w.y, lo);
-            hi = __dp2a_hi(ra.y, w.y, hi);
-            lo = __dp2a_lo(ra.z, w.z, lo);
-            hi = __dp2a_hi(ra.z, w.z, hi);
-            lo = __dp2a_lo(ra.w, w.w, lo);
-            hi = __dp2a_hi(ra.w, w.w, hi);
-            tot += (uint64_t)lo + ((uint64_t)hi << 8);
-        }
-        for (int64_t j = nvec * 8 + lane; j < n; j += 32) tot += (uint64_t)Ar[j] * x[j];
-        tot = warp_sum(tot);
-        if (lane == 0) write_result(mod_p(tot, K.p, K.mu), O, K, row);
+        tot = group_sum<LPR>(tot);
+        if (valid && g == 0) write_result(mod_p(tot, K.p, K.mu), O, K, row);
     }
 }
 
 // ------------------------------------------------------------------------------ batch: generic
 // Warp per row with policy R.  x read through the read-only path (L1-resident, reused by every
 // row).  VEC: rows and x are 16-byte aligned (A, lda*sizeof, x) -> 16-byte loads.
-template <class R, int NT, int U, bool VEC>
+template <class R, int NT, int U, bool VEC, int LPR>
 __global__ void __launch_bounds__(NT) batch_kernel(const typename R::elem *__restrict__ A, int64_t lda,
                                                    const typename R::elem *__restrict__ x, int64_t rows,
                                                    int64_t n, KParams K, OutSpec O) {
@@ -275,31 +291,37 @@ __global__ void __launch_bounds__(NT) batch_kernel(const typename R::elem *__res
         __syncthreads();
         tab = s_tab;
     }
-    const int lane = threadIdx.x & 31;
-    for (int64_t row = (int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); row < rows;
-         row += (int64_t)gridDim.x * (NT / 32)) {
-        const typename R::elem *Ar = A + row * lda;
+    constexpr int RPW = 32 / LPR;
+    const int lane = threadIdx.x & 31, g = lane % LPR;
+    const int64_t warp0 = (int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
+    const int64_t wstride = (int64_t)gridDim.x * (NT / 32);
+    for (int64_t rbase = warp0 * RPW; rbase < rows; rbase += wstride * RPW) {
+        const int64_t row = rbase + lane / LPR;
+        const bool valid = row < rows;
+        const typename R::elem *Ar = A + (valid ? row : 0) * lda;
         typename R::Acc acc;
         R::init(acc);
-        int64_t done = 0;
-        if (VEC) {
-            const int64_t nvec = n / R::W;
-            const uint4 *av = reinterpret_cast<const uint4 *>(Ar);
-            const uint4 *xv = reinterpret_cast<const uint4 *>(x);
-            for (int64_t v0 = lane; v0 < nvec; v0 += 32 * U) {
-                uint4 ra[U];
+        if (valid) {
+            int64_t done = 0;
+            if (VEC) {
+                const int64_t nvec = n / R::W;
+                const uint4 *av = reinterpret_cast<const uint4 *>(Ar);
+                const uint4 *xv = reinterpret_cast<const uint4 *>(x);
+                int64_t v0 = g;
+                for (; v0 + LPR * (U - 1) < nvec; v0 += LPR * U) {
+                    uint4 ra[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u)
-                    ra[u] = v0 + u * 32 < nvec ? ld_stream(av + v0 + u * 32) : make_uint4(0, 0, 0, 0);
+                    for (int u = 0; u < U; ++u) ra[u] = ld_stream(av + v0 + u * LPR);
 #pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (v0 + u * 32 < nvec) R::vec(acc, ra[u], __ldg(xv + v0 + u * 32), K, tab);
+                    for (int u = 0; u < U; ++u) R::vec(acc, ra[u], __ldg(xv + v0 + u * LPR), K, tab);
+                }
+                for (; v0 < nvec; v0 += LPR) R::vec(acc, ld_stream(av + v0), __ldg(xv + v0), K, tab);
+                done = nvec * R::W;
             }
-            done = nvec * R::W;
+            for (int64_t j = done + g; j < n; j += LPR) R::term(acc, Ar[j], x[j], K, tab);
         }
-        for (int64_t j = done + lane; j < n; j += 32) R::term(acc, Ar[j], x[j], K, tab);
-        uint64_t v = warp_sum(R::finish(acc, K));
-        if (lane == 0) write_result(mod_p(v, K.p, K.mu), O, K, row);
+        uint64_t v = group_sum<LPR>(valid ? R::finish(acc, K) : 0);
+        if (valid && g == 0) write_result(mod_p(v, K.p, K.mu), O, K, row);
     }
 }
 
@@ -702,27 +724,28 @@ cudaError_t launch_finalize(const KParams &K, const uint64_t *summed, int count,
 }
 
 // ------------------------------------------------------------------------------ batch launch
-template <class R, int NT, int U>
-static cudaError_t launch_batch_t(const KParams &K, const void *A, int64_t lda, const void *x, int64_t rows,
-                                  int64_t n, bool vec, OutSpec O, cudaStream_t s) {
+template <class R, int NT, int U, int LPR>
+static cudaError_t launch_batch_lpr(const KParams &K, const void *A, int64_t lda, const void *x, int64_t rows,
+                                   int64_t n, bool vec, OutSpec O, cudaStream_t s) {
     using E = typename R::elem;
     const size_t smem = R::kTable ? (size_t)K.antilog_entries * 2 : 0;
     int dev = 0;
     cudaGetDevice(&dev);
-    const int64_t wpb = NT / 32;
-    if (vec) {
-        auto kern = batch_kernel<R, NT, U, true>;
-        int bps = occupancy(kern, NT, smem);
-        int64_t grid = std::min<int64_t>((rows + wpb - 1) / wpb, (int64_t)num_sms(dev) * bps);
-        kern<<<(int)std::max<int64_t>(grid, 1), NT, smem, s>>>((const E *)A, lda, (const E *)x, rows, n, K, O);
-    } else {
-        auto kern = batch_kernel<R, NT, U, false>;
-        int bps = occupancy(kern, NT, smem);
-        int64_t grid = std::min<int64_t>((rows + wpb - 1) / wpb, (int64_t)num_sms(dev) * bps);
-        kern<<<(int)std::max<int64_t>(grid, 1), NT, smem, s>>>((const E *)A, lda, (const E *)x, rows, n, K, O);
-    }
+    const int64_t rpb = (NT / 32) * (32 / LPR);  // rows per CTA per sweep
+    auto kern = vec ? batch_kernel<R, NT, U, true, LPR> : batch_kernel<R, NT, U, false, LPR>;
+    int bps = occupancy(kern, NT, smem);
+    int64_t grid = std::min<int64_t>((rows + rpb - 1) / rpb, (int64_t)num_sms(dev) * bps);
+    kern<<<(int)std::max<int64_t>(grid, 1), NT, smem, s>>>((const E *)A, lda, (const E *)x, rows, n, K, O);
     count_launch();
     return cudaGetLastError();
+}
+
+// Lanes per row: a full warp for long rows, 8 lanes (4 rows per warp) when a row has < 256 vectors.
+template <class R, int NT, int U>
+static cudaError_t launch_batch_t(const KParams &K, const void *A, int64_t lda, const void *x, int64_t rows,
+                                  int64_t n, bool vec, OutSpec O, cudaStream_t s) {
+    if (n / R::W >= 256 || R::kTable) return launch_batch_lpr<R, NT, U, 32>(K, A, lda, x, rows, n, vec, O, s);
+    return launch_batch_lpr<R, NT, U, 8>(K, A, lda, x, rows, n, vec, O, s);
 }
 
 gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int64_t lda, const void *x, int64_t rows,
@@ -760,11 +783,13 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
     case GFP_REP_CLASSICAL:
         if (I.dtype == GFP_U16) {
             if (vec && (u128)n * q2 <= max64 && n <= 96 * 1024) {
-                constexpr int NT = 256, U = 16;
-                auto kern = batch_cl16_kernel<NT, U>;
+                constexpr int NT = 256;
+                const bool long_rows = n / 8 >= 256;
+                auto kern = long_rows ? batch_cl16_kernel<NT, 16, 32> : batch_cl16_kernel<NT, 8, 8>;
+                const int64_t rpb = long_rows ? NT / 32 : NT / 8;  // rows per CTA per sweep
                 const size_t smem = (size_t)(((n + 1) / 2 + 3) & ~int64_t(3)) * 4;
                 int bps = occupancy(kern, NT, smem);
-                int64_t grid = std::min<int64_t>((rows + NT / 32 - 1) / (NT / 32), (int64_t)num_sms(dev) * bps);
+                int64_t grid = std::min<int64_t>((rows + rpb - 1) / rpb, (int64_t)num_sms(dev) * bps);
                 kern<<<(int)std::max<int64_t>(grid, 1), NT, smem, s>>>((const uint16_t *)A, lda, (const uint16_t *)x,
                                                                        rows, n, K, O);
                 count_launch();
