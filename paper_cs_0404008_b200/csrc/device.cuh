@@ -303,7 +303,7 @@ struct ClassicalS {
         if (STRAT == S_DELAYED) {
             A.s += prod;
         } else if (STRAT == S_BLOCKED) {
-            if (A.cnt == K.kblk) {
+            if (A.cnt >= K.kblk) {
                 A.s = reduce(A.s, K);  // res %= P after each block (G1)
                 A.cnt = 0;
             }
@@ -312,13 +312,14 @@ struct ClassicalS {
         } else if (STRAT == S_OVERFLOW) {
             A.s += prod;
             if (A.s < prod) A.s += corr(K);
-        } else {  // S_HYBRID
-            A.s += prod;
-            if (++A.cnt == K.kblk) {
+        } else {  // S_HYBRID: close the block (its one wrap test) before it would exceed lambda products
+            if (A.cnt >= K.kblk) {
                 if (A.s < A.base) A.s += corr(K);
                 A.base = A.s;
                 A.cnt = 0;
             }
+            A.s += prod;
+            ++A.cnt;
         }
     }
     __device__ __forceinline__ static void raw(Acc &A, uint4 x, uint4 y) {
