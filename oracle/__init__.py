@@ -49,6 +49,10 @@ def _load():
             "oracle_zech_decode_one": (i64, [u64, u64, u64]),
             "oracle_zech_encode_one": (u64, [u64, u64, u64]),
             "oracle_dot_zech": (u64, [u64, u64, vp, vp, i64, vp, ctypes.POINTER(i64)]),
+            "oracle_zech_tplus1": (None, [u64, u64, vp, vp]),
+            "oracle_zech_mul": (u64, [u64, u64, u64]),
+            "oracle_zech_add": (u64, [u64, vp, u64, u64]),
+            "oracle_dot_zech_tplus1": (u64, [u64, u64, vp, vp, i64, vp, vp, ctypes.POINTER(i64)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -144,6 +148,39 @@ def dot_zech(p: int, g: int, a: np.ndarray, b: np.ndarray) -> int:
     bad = ctypes.c_int64(-1)
     r = int(_load().oracle_dot_zech(p, g, a.ctypes.data, b.ctypes.data, a.size, pw.ctypes.data,
                                     ctypes.byref(bad)))
+    if bad.value >= 0:
+        raise ValueError(f"element {bad.value} is not a Zech code for p={p}")
+    return r
+
+
+def zech_tplus1(p: int, g: int) -> np.ndarray:
+    """t_plus1[k], k = 0 .. q-1: the code of 1 + g^k (sec. 2.4; 0 when 1 + g^k = 0)."""
+    t = np.empty(p, dtype=np.uint64)
+    lg = np.empty(p, dtype=np.uint64)
+    _load().oracle_zech_tplus1(p, g, t.ctypes.data, lg.ctypes.data)
+    return t
+
+
+def zech_mul(p: int, i: int, j: int) -> int:
+    """Table 1 multiplication of Zech codes: i + j (- qbar)."""
+    return int(_load().oracle_zech_mul(p, i, j))
+
+
+def zech_add(p: int, t: np.ndarray, i: int, j: int) -> int:
+    """Table 1 addition of Zech codes: k = j - i (+ qbar); i + t_plus1[k] (- qbar)."""
+    return int(_load().oracle_zech_add(p, t.ctypes.data, i, j))
+
+
+def dot_zech_tplus1(p: int, g: int, a: np.ndarray, b: np.ndarray) -> int:
+    """Pure-Zech dot: Table 1 product and t_plus1 addition per term, result a code."""
+    a, b = _c(a.astype(np.uint16, copy=False)), _c(b.astype(np.uint16, copy=False))
+    if a.shape != b.shape:
+        raise ValueError("length mismatch")
+    t = np.empty(p, dtype=np.uint64)
+    lg = np.empty(p, dtype=np.uint64)
+    bad = ctypes.c_int64(-1)
+    r = int(_load().oracle_dot_zech_tplus1(p, g, a.ctypes.data, b.ctypes.data, a.size, t.ctypes.data,
+                                           lg.ctypes.data, ctypes.byref(bad)))
     if bad.value >= 0:
         raise ValueError(f"element {bad.value} is not a Zech code for p={p}")
     return r

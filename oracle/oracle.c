@@ -240,3 +240,82 @@ uint64_t oracle_dot_zech(uint64_t p, uint64_t g, const uint16_t *a, const uint16
     }
     return oracle_zech_encode_one(p, g, acc);
 }
+
+/* ----------------------------- Zech arithmetic of Table 1 (sec 2.4, F3) */
+/* The paper's own addition of discrete-log codes (Table 1),
+ * written out step by step in the table's order and notation.  Codes follow
+ * P:126-131 (0 -> 0, 1 -> qbar = q-1, g^i -> i); all of [1, qbar] are the
+ * nonzero codes, code qbar standing for g^0 = 1.  These functions give the
+ * same unique field element as oracle_dot_zech (the sum is unique); they
+ * exist so the pure-Zech accumulation has its algorithm in the oracle too. */
+
+/* t_plus1[k] for k = 0 .. q-1 (a table "of size q"): the code h of
+ * 1 + g^k, i.e. g^h = 1 + g^k, with h = 0 when 1 + g^k = 0 (k = (q-1)/2,
+ * g^((q-1)/2) = -1).  t[q-1] = t[0] since g^(q-1) = g^0.  The log
+ * map is built by enumerating the powers g^c (no table shared with anything).
+ * lg must hold p entries of scratch. */
+void oracle_zech_tplus1(uint64_t p, uint64_t g, uint64_t *t, uint64_t *lg)
+{
+    uint64_t q = p, qbar = q - 1, x = 1 % p;
+    for (uint64_t c = 0; c < p; ++c) lg[c] = 0;
+    /* lg[g^c] = c for c = 1 .. qbar-1; lg[1] = qbar; lg[0] = 0 */
+    for (uint64_t c = 1; c < qbar; ++c) {
+        x = (uint64_t)(((u128)x * g) % p);
+        lg[x] = c;
+    }
+    lg[1 % p] = qbar;
+    lg[0] = 0;
+    x = 1 % p; /* g^k */
+    for (uint64_t k = 0; k < qbar; ++k) {
+        t[k] = lg[(x + 1) % p];
+        x = (uint64_t)(((u128)x * g) % p);
+    }
+    t[qbar] = t[0];
+}
+
+/* Table 1 row "Multiplication": g^i * g^j -> i + j (- qbar).  Zero operands
+ * (code 0) give zero (reading G13). */
+uint64_t oracle_zech_mul(uint64_t p, uint64_t i, uint64_t j)
+{
+    uint64_t qbar = p - 1;
+    if (i == 0 || j == 0) return 0;
+    uint64_t s = i + j;
+    if (s > qbar) s -= qbar; /* the "(- qbar)" test */
+    return s;
+}
+
+/* Table 1 row "Addition": g^i + g^j -> k = j - i (+ qbar); i + t_plus1[k] (- qbar).
+ * A zero operand returns the other one; t_plus1[k] = 0 (1 + g^k = 0) gives zero. */
+uint64_t oracle_zech_add(uint64_t p, const uint64_t *t, uint64_t i, uint64_t j)
+{
+    int64_t qbar = (int64_t)p - 1;
+    if (i == 0) return j;
+    if (j == 0) return i;
+    int64_t k = (int64_t)j - (int64_t)i;
+    if (k < 0) k += qbar; /* the "(+ qbar)" test */
+    uint64_t h = t[k];
+    if (h == 0) return 0; /* g^i (1 + g^k) = 0 */
+    uint64_t r = i + h;
+    if (r > (uint64_t)qbar) r -= (uint64_t)qbar; /* the "(- qbar)" test */
+    return r;
+}
+
+/* Pure-Zech dot (reading G11's alternative): every product and
+ * every partial sum stays a Zech code; acc starts at the zero code and absorbs
+ * one Table-1 product per term with one Table-1 addition.  t, lg: scratch of p
+ * entries each.  *bad = first invalid code index or -1. */
+uint64_t oracle_dot_zech_tplus1(uint64_t p, uint64_t g, const uint16_t *a, const uint16_t *b, int64_t n,
+                                uint64_t *t, uint64_t *lg, int64_t *bad)
+{
+    uint64_t q = p, acc = 0;
+    *bad = -1;
+    oracle_zech_tplus1(p, g, t, lg);
+    for (int64_t i = 0; i < n; ++i) {
+        if (a[i] > q - 1 || b[i] > q - 1) {
+            *bad = i;
+            return UINT64_MAX;
+        }
+        acc = oracle_zech_add(p, t, acc, oracle_zech_mul(p, a[i], b[i]));
+    }
+    return acc;
+}

@@ -314,3 +314,74 @@ def test_bilinearity_symmetry_additivity(p):
     assert d(sa, b) == d(a, b) * s % p
     for cut in [0, 1, 1000, n - 1, n]:
         assert (d(a[:cut], b[:cut]) + d(a[cut:], b[cut:])) % p == d(a, b)
+
+
+# ------------------------------------------------------------------ Zech Table 1 (F3)
+def _zech_maps(p, g):
+    """decode list and encode dict from the literal P:128-130 cases (bruteforce.py, Python pow)."""
+    dec = [bf.zech_decode(p, g, c) for c in range(p)]
+    enc = {x: c for c, x in enumerate(dec)}
+    assert len(enc) == p  # bijection onto GF(p)
+    return dec, enc
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 7, 11, 13, 101, 257])
+def test_zech_table1_mul_add_exhaustive(p):
+    """Pins oracle_zech_mul / oracle_zech_add / t_plus1 (sec. 2.4 Table 1): every pair of
+    codes gives the code of the field product / sum computed with Python integers."""
+    g = bf.primitive_root(p)
+    dec, enc = _zech_maps(p, g)
+    t = oracle.zech_tplus1(p, g)
+    assert t.size == p  # "a table of size q" (P:143)
+    for i in range(p):
+        for j in range(p):
+            assert oracle.zech_mul(p, i, j) == enc[dec[i] * dec[j] % p], (i, j)
+            assert oracle.zech_add(p, t, i, j) == enc[(dec[i] + dec[j]) % p], (i, j)
+
+
+@pytest.mark.parametrize("p", [32749, 40009, 65521])
+def test_zech_tplus1_identities(p):
+    """t_plus1 against facts independent of how it is built: its definition g^h = 1 + g^k on sampled
+    k (Python pow), the zero at k = qbar/2 (g^(qbar/2) = -1), and Zech's reflection identity
+    Z(-k) = Z(k) - k (mod qbar), from 1 + g^-k = g^-k (1 + g^k)."""
+    g = oracle.primitive_root(p)
+    qbar = p - 1
+    t = [int(v) for v in oracle.zech_tplus1(p, g)]
+    assert t[qbar // 2] == 0 and t[qbar] == t[0]
+    assert pow(g, t[0], p) == 2
+    rng = random.Random(p)
+    for k in rng.sample(range(qbar), 2000):
+        if k == qbar // 2:
+            continue
+        assert pow(g, t[k], p) == (1 + pow(g, k, p)) % p
+        assert 1 <= t[k] <= qbar
+    for k in range(1, qbar):
+        if k == qbar // 2:
+            continue
+        assert (t[qbar - k] - (t[k] - k)) % qbar == 0, k
+    assert t.count(0) == 1  # 1 + g^k = 0 only at k = qbar/2
+
+
+@pytest.mark.parametrize("p", [3, 7, 101, 1009, 32749, 40009, 65521])
+def test_dot_zech_tplus1_unique_result(p):
+    """The pure-Zech accumulation reaches the unique field element: equal to the integer-decoded
+    dot (oracle_dot_zech) and, on tiny inputs, to Python-integer brute force; zero-heavy inputs
+    and sums that cancel to zero are included."""
+    g = oracle.primitive_root(p)
+    rng = random.Random(p + 7)
+    for n in [0, 1, 2, 3, 64, 513, 5000]:
+        ca = np.array([0 if rng.random() < 0.1 else rng.randrange(1, p) for _ in range(n)], np.uint16)
+        cb = np.array([0 if rng.random() < 0.1 else rng.randrange(1, p) for _ in range(n)], np.uint16)
+        r = oracle.dot_zech_tplus1(p, g, ca, cb)
+        assert r == oracle.dot_zech(p, g, ca, cb)
+        if n <= 64:
+            want = bf.dot(p, [bf.zech_decode(p, g, int(c)) for c in ca], [bf.zech_decode(p, g, int(c)) for c in cb])
+            assert r == bf.zech_encode(p, g, want)
+    # x + (-x) = 0: the code of -1 is qbar/2 (P:138-139), so [c, c] . [qbar, qbar/2] cancels
+    c = np.array([1, 1], np.uint16)
+    assert oracle.dot_zech_tplus1(p, g, c, np.array([p - 1, (p - 1) // 2], np.uint16)) == 0
+    # all-ones of length p (code qbar) sums to p = 0
+    ones = np.full(p, p - 1, np.uint16)
+    assert oracle.dot_zech_tplus1(p, g, ones, ones) == 0
+    with pytest.raises(ValueError):
+        oracle.dot_zech_tplus1(p, g, np.array([p], np.uint32), np.array([1], np.uint32))
