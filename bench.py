@@ -47,6 +47,10 @@ CONFIGS = {
             dtype=np.uint16, n=1 << 26, bpt=4, kind="dot"),
     4: dict(name="C5", workload="configs[4]: GF(65521) classical u16 matrix-vector 65536x4096, rows sharded",
             p=65521, rep=0, dtype=np.uint16, rows=65536, n=4096, bpt=2, kind="batch"),
+    # configs[3] again with the paper's own Zech accumulation: t_plus1 additions, no
+    # integer accumulator (gfp_dot_ex, GFP_STRAT_ZECH_ADD = 5)
+    5: dict(name="C4-zech_add", workload="configs[3] with pure-Zech t_plus1 accumulation (sec. 2.4 Table 1)",
+            p=32749, rep=3, dtype=np.uint16, n=1 << 26, bpt=4, kind="dot", strategy=5, inputs_of=3),
 }
 REP_NAMES = {0: "classical", 1: "montgomery", 2: "fp64", 3: "zech"}
 DTYPE_NAMES = {np.dtype(np.uint16): "u16", np.dtype(np.uint32): "u32", np.dtype(np.float64): "f64"}
@@ -137,7 +141,8 @@ def shard(n, rank, world):
 def host_inputs(cfg, rank, world, limit=None):
     """Host arrays of this rank's shard, in the representation's *input* form (classical residues for
     Montgomery, which is converted on device; Zech codes; fp64 integers; classical residues)."""
-    seed = synth.BASE_SEED + [k for k, v in CONFIGS.items() if v is cfg][0]
+    idx = [k for k, v in CONFIGS.items() if v is cfg][0]
+    seed = synth.BASE_SEED + cfg.get("inputs_of", idx)
     p = cfg["p"]
     if cfg["kind"] == "batch":
         r0, r1 = shard(cfg["rows"], rank, world)
@@ -234,7 +239,9 @@ def make_step(gfp, cfg, reps, world, group, stream):
         if record:
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record(stream)
-        if world == 1:
+        if world == 1 and cfg.get("strategy"):
+            gfp.dot_ex(a, b, p, rep, strategy=cfg["strategy"], out=out, stream=stream)
+        elif world == 1:
             gfp.dot(a, b, p, rep, out=out, stream=stream)
         else:
             gfp.dot_partial(a, b, p, rep, out=partial, stream=stream)
@@ -410,7 +417,10 @@ def main():
             got = gfp.dot_batch(d["A"][:m], d["x"], cfg["p"], cfg["rep"]).cpu().numpy().astype(np.uint64)
             parity = bool(np.array_equal(got, ores))
         else:
-            r = gfp.dot(d["a"][:m], d["b"][:m], cfg["p"], cfg["rep"])
+            if cfg.get("strategy"):
+                r = gfp.dot_ex(d["a"][:m], d["b"][:m], cfg["p"], cfg["rep"], strategy=cfg["strategy"])
+            else:
+                r = gfp.dot(d["a"][:m], d["b"][:m], cfg["p"], cfg["rep"])
             got = r.cpu()[0].item() if cfg["rep"] == 2 else int(r.cpu().to(torch.int64)[0])
             parity = got == ores
         cpu["parity_checked_terms"] = int(m) if cfg["kind"] == "dot" else int(m) * cfg["n"]
@@ -435,7 +445,7 @@ def main():
                                                            cfg["kind"] == "dot" else ""),
                        "l2": "inputs larger than L2: %.0f MiB per rank x %d rotating copies vs 126 MB L2"
                              % (local_bytes / 2 ** 20, len(reps)),
-                       "seed": synth.BASE_SEED + args.config},
+                       "seed": synth.BASE_SEED + cfg.get("inputs_of", args.config)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_timed,
             "clocks": clk.summary(), "parity_vs_oracle": parity, "phases": phases,

@@ -18,7 +18,7 @@ import os
 import torch
 
 __all__ = [
-    "CLASSICAL", "MONTGOMERY", "FP64", "ZECH", "AUTO", "DELAYED", "BLOCKED", "OVERFLOW", "HYBRID",
+    "CLASSICAL", "MONTGOMERY", "FP64", "ZECH", "AUTO", "DELAYED", "BLOCKED", "OVERFLOW", "HYBRID", "ZECH_ADD",
     "GfpError", "lib", "query", "plan", "dot", "dot_ex", "dot_batch", "dot_batch_ex",
     "dot_partial", "finalize", "to_rep", "from_rep", "dot_host", "launch_count", "release_caches",
     "rep_dtype",
@@ -27,7 +27,9 @@ __all__ = [
 CLASSICAL, MONTGOMERY, FP64, ZECH = 0, 1, 2, 3
 U16, U32, F64 = 0, 1, 2
 AUTO, DELAYED, BLOCKED, OVERFLOW, HYBRID = 0, 1, 2, 3, 4  # gfp_strategy (paper sec. 3)
-_STRAT_NAMES = {AUTO: "auto", DELAYED: "delayed", BLOCKED: "blocked", OVERFLOW: "overflow", HYBRID: "hybrid"}
+ZECH_ADD = 5  # pure discrete-log accumulation through t_plus1 (sec. 2.4 Table 1), Zech only
+_STRAT_NAMES = {AUTO: "auto", DELAYED: "delayed", BLOCKED: "blocked", OVERFLOW: "overflow", HYBRID: "hybrid",
+                ZECH_ADD: "zech_add"}
 _REP_NAMES = {CLASSICAL: "classical", MONTGOMERY: "montgomery", FP64: "fp64", ZECH: "zech"}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))

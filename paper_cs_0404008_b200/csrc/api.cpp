@@ -39,7 +39,7 @@ size_t dtype_size(int dt) { return dt == GFP_U16 ? 2 : (dt == GFP_U32 ? 4 : 8); 
 struct Ctx {
     gfp_info info;
     dev::KParams K;
-    uint16_t *d_antilog = nullptr, *d_log = nullptr;
+    uint16_t *d_antilog = nullptr, *d_log = nullptr, *d_zplus1 = nullptr;
 };
 
 std::mutex g_mu;
@@ -98,23 +98,30 @@ gfp_status get_ctx(uint64_t p, gfp_rep rep, gfp_dtype dt, Ctx **out) {
     K.corr32 = (uint32_t)((((u128)1) << 32) % p);
     K.mu32 = (uint32_t)(0xFFFFFFFFull / p);
     if (rep == GFP_REP_ZECH) {
-        std::vector<uint16_t> logt, anti;
+        std::vector<uint16_t> logt, anti, delta;
         zech_tables(p, c->info.g, logt, anti);
+        zech_plus1_delta(p, logt, delta);
         logt.resize((logt.size() + 7) & ~size_t(7), 0);
         anti.resize((anti.size() + 7) & ~size_t(7), 0);
+        delta.resize((delta.size() + 7) & ~size_t(7), 0);
         cudaError_t e = cudaMalloc(&c->d_log, logt.size() * 2);
         if (e == cudaSuccess) e = cudaMalloc(&c->d_antilog, anti.size() * 2);
+        if (e == cudaSuccess) e = cudaMalloc(&c->d_zplus1, delta.size() * 2);
         if (e == cudaSuccess) e = cudaMemcpy(c->d_log, logt.data(), logt.size() * 2, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(c->d_antilog, anti.data(), anti.size() * 2, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(c->d_zplus1, delta.data(), delta.size() * 2, cudaMemcpyHostToDevice);
         if (e != cudaSuccess) {
             cudaFree(c->d_log);
             cudaFree(c->d_antilog);
+            cudaFree(c->d_zplus1);
             delete c;
             return cuda_fail(e, "Zech table upload");
         }
         K.antilog = c->d_antilog;
         K.logt = c->d_log;
         K.antilog_entries = (uint32_t)anti.size();
+        K.zplus1 = c->d_zplus1;
+        K.zplus1_entries = (uint32_t)delta.size();
     }
     g_ctx[key] = c;
     *out = c;
@@ -259,6 +266,7 @@ gfp_status gfp_plan(uint64_t p, gfp_rep rep, gfp_dtype dt, int64_t n, const gfp_
     memset(&K, 0, sizeof(K));
     K.p = p;
     K.antilog_entries = (uint32_t)((I.table_bytes / 2 + 7) & ~uint64_t(7));
+    K.zplus1_entries = (uint32_t)((p + 7) & ~uint64_t(7));  // qbar + 1 = p entries
     DotPlan plan;
     const void *aligned_ptr = (const void *)(uintptr_t)4096;
     if ((st = plan_dot(I, K, aligned_ptr, aligned_ptr, n, opt, &plan)) != GFP_OK) return plan_fail(st);
@@ -394,6 +402,7 @@ void gfp_release_caches(void) {
     for (auto &kv : g_ctx) {
         cudaFree(kv.second->d_antilog);
         cudaFree(kv.second->d_log);
+        cudaFree(kv.second->d_zplus1);
         delete kv.second;
     }
     g_ctx.clear();

@@ -263,6 +263,43 @@ struct Zech {
 };
 
 
+// Pure-Zech arithmetic (sec. 2.4, Table 1).  Values live in
+// "u space": a nonzero element g^e with code e in [1, qbar] (code qbar = g^0) is held as
+// u = e - 1 in [0, qbar), and the zero element as kZ.  Then
+//   multiplication  g^i * g^j:  u = i + j - 1 (- qbar)                       (Table 1 row 1)
+//   addition        g^(s+1) + g^(c+1) = g^(s+1) (1 + g^k),  k = c - s (+ qbar),
+//                   u = s + delta[k] (- qbar), delta[k] = log(1 + g^k)        (Table 1 "Addition")
+// with delta the t_plus1 table in exponent form (numtheory.h), kZechDeltaZero where 1 + g^k = 0.
+// Each "(+/- qbar)" test is one unsigned min: v = min(v, v - qbar) folds [0, 2 qbar) into [0, qbar).
+namespace zadd {
+constexpr uint32_t kZ = 0xFFFFFFFFu;   // the zero element
+constexpr uint32_t kDZero = 0xFFFFu;  // delta sentinel: 1 + g^k = 0
+
+__device__ __forceinline__ uint32_t fold(uint32_t v, uint32_t qbar) { return min(v, v - qbar); }
+
+// product of two codes -> u space (a zero operand gives kZ)
+__device__ __forceinline__ uint32_t mul(uint32_t ci, uint32_t cj, uint32_t qbar) {
+    const uint32_t u = fold(ci + cj - 1u, qbar);
+    return (ci == 0 || cj == 0) ? kZ : u;
+}
+
+// s + c in u space, either operand possibly kZ.  The table index stays in [0, qbar] in every case
+// (s = kZ: k = c + 1 <= qbar; c = kZ: k = qbar - 1 - s), so the lookup never leaves the table.
+__device__ __forceinline__ uint32_t add(uint32_t s, uint32_t c, uint32_t qbar, const uint16_t *delta) {
+    uint32_t k = c - s;
+    k = min(k, k + qbar);
+    const uint32_t d = delta[k];
+    uint32_t r = fold(s + d, qbar);
+    r = d == kDZero ? kZ : r;  // g^(s+1) (1 + g^k) = 0
+    r = s == kZ ? c : r;
+    r = c == kZ ? s : r;
+    return r;
+}
+
+// u space -> Zech code: zero -> 0, u -> u + 1
+__device__ __forceinline__ uint32_t to_code(uint32_t u) { return u == kZ ? 0u : u + 1u; }
+}  // namespace zadd
+
 // ------------------------------------------------------------------------------ explicit strategies
 // The paper's section-3 accumulation algorithms, selectable through gfp_dot_ex / gfp_dot_batch_ex for
 // classical storage E (u16 / u32) with an m-bit accumulator ACC (u32 or u64).  Every variant is exact;

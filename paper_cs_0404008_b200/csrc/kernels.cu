@@ -31,6 +31,7 @@ enum Policy {
     // explicit strategies (gfp_dot_ex): P_CS + 8*acc64 + 4*elem32 + (strategy - 1)
     P_CS = 32, P_CS_END = P_CS + 16,
     P_MONT_OVF = 64,
+    P_ZECH_ADD = 65,  // pure-Zech accumulation (F3)
     P_COUNT
 };
 constexpr int cs_policy(bool acc64, bool e32, int strat) { return P_CS + 8 * acc64 + 4 * e32 + (strat - 1); }
@@ -186,6 +187,145 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
             *sum = 0;  // self-reset for the next launch on this stream
             *ws.counter = 0;
         }
+    }
+}
+
+// ------------------------------------------------------------------------------ pure-Zech dot (F3)
+// Every product and every partial sum stays in the discrete-log representation (sec. 2.4, Table 1):
+// a product is an index addition, a sum one lookup in the t_plus1 table (staged in shared memory).
+// Eight independent Zech accumulators per thread (one per u16 lane of a 16-byte vector) hide the
+// lookup latency of the dependent additions; they are merged by Zech additions in the thread, the
+// warp (shuffles) and the CTA, and each CTA's merged value goes to the workspace, where the last CTA
+// to arrive on the counter merges them all and encodes.  No integer sum, no remainder anywhere.
+__device__ __forceinline__ uint32_t zech_warp_merge(uint32_t v, uint32_t qbar, const uint16_t *D) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = zadd::add(v, __shfl_xor_sync(0xFFFFFFFFu, v, o), qbar, D);
+    return v;
+}
+
+// Merge over the CTA; valid in thread 0.
+__device__ __forceinline__ uint32_t zech_block_merge(uint32_t v, uint32_t *red, uint32_t qbar, const uint16_t *D) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = zech_warp_merge(v, qbar, D);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    v = zadd::kZ;
+    if (warp == 0) v = zech_warp_merge(lane < nw ? red[lane] : zadd::kZ, qbar, D);
+    return v;
+}
+
+__device__ __forceinline__ void zech_add_pair(uint32_t (&acc)[8], int j, uint32_t x, uint32_t y, uint32_t qbar,
+                                              const uint16_t *D) {
+    acc[2 * j] = zadd::add(acc[2 * j], zadd::mul(x & 0xFFFFu, y & 0xFFFFu, qbar), qbar, D);
+    acc[2 * j + 1] = zadd::add(acc[2 * j + 1], zadd::mul(x >> 16, y >> 16, qbar), qbar, D);
+}
+
+template <int NT, int U>
+__global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__restrict__ a,
+                                                          const uint16_t *__restrict__ b, int64_t n, int64_t head,
+                                                          KParams K, Workspace ws, OutSpec O) {
+    extern __shared__ __align__(16) uint16_t s_delta[];
+    __shared__ uint32_t red[32];
+    __shared__ int s_last;
+    const uint32_t qbar = K.qbar;
+    const int64_t gtid = (int64_t)blockIdx.x * NT + threadIdx.x;
+    const int64_t gstride = (int64_t)gridDim.x * NT;
+    const int64_t nvec = (n - head) / 8;
+    const uint4 *av = reinterpret_cast<const uint4 *>(a + head);
+    const uint4 *bv = reinterpret_cast<const uint4 *>(b + head);
+    int64_t i0 = (int64_t)blockIdx.x * (NT * U) + threadIdx.x;
+    const int64_t step = (int64_t)gridDim.x * (NT * U);
+
+    // first loads in flight while the table is staged from L2
+    uint4 ca[U], cb[U];
+    bool have = i0 + (U - 1) * NT < nvec;
+    if (have) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            ca[u] = ld_stream(av + i0 + u * NT);
+            cb[u] = ld_stream(bv + i0 + u * NT);
+        }
+    }
+    stage_table(s_delta, K.zplus1, K.zplus1_entries);
+    __syncthreads();
+    const uint16_t *D = s_delta;
+
+    uint32_t acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = zadd::kZ;
+    while (have) {
+        const int64_t nx = i0 + step;
+        const bool more = nx + (U - 1) * NT < nvec;
+        uint4 na[U], nb[U];
+        if (more) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                na[u] = ld_stream(av + nx + u * NT);
+                nb[u] = ld_stream(bv + nx + u * NT);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            zech_add_pair(acc, 0, ca[u].x, cb[u].x, qbar, D);
+            zech_add_pair(acc, 1, ca[u].y, cb[u].y, qbar, D);
+            zech_add_pair(acc, 2, ca[u].z, cb[u].z, qbar, D);
+            zech_add_pair(acc, 3, ca[u].w, cb[u].w, qbar, D);
+        }
+        i0 = nx;
+        have = more;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            ca[u] = na[u];
+            cb[u] = nb[u];
+        }
+    }
+    // ragged vectors (< U per thread), scalar head and tail
+    for (int u = 0; u < U; ++u) {
+        if (i0 + u * NT < nvec) {
+            const uint4 x = ld_stream(av + i0 + u * NT), y = ld_stream(bv + i0 + u * NT);
+            zech_add_pair(acc, 0, x.x, y.x, qbar, D);
+            zech_add_pair(acc, 1, x.y, y.y, qbar, D);
+            zech_add_pair(acc, 2, x.z, y.z, qbar, D);
+            zech_add_pair(acc, 3, x.w, y.w, qbar, D);
+        }
+    }
+    for (int64_t i = gtid; i < head; i += gstride) acc[0] = zadd::add(acc[0], zadd::mul(a[i], b[i], qbar), qbar, D);
+    for (int64_t i = head + nvec * 8 + gtid; i < n; i += gstride)
+        acc[1] = zadd::add(acc[1], zadd::mul(a[i], b[i], qbar), qbar, D);
+
+    // merge: thread (tree over its 8 accumulators) -> warp -> CTA -> workspace -> last CTA
+    acc[0] = zadd::add(acc[0], acc[1], qbar, D);
+    acc[2] = zadd::add(acc[2], acc[3], qbar, D);
+    acc[4] = zadd::add(acc[4], acc[5], qbar, D);
+    acc[6] = zadd::add(acc[6], acc[7], qbar, D);
+    acc[0] = zadd::add(acc[0], acc[2], qbar, D);
+    acc[4] = zadd::add(acc[4], acc[6], qbar, D);
+    uint32_t v = zech_block_merge(zadd::add(acc[0], acc[4], qbar, D), red, qbar, D);
+    if (threadIdx.x == 0) {
+        ws.partials[1 + blockIdx.x] = v;
+        unsigned int t;
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(ws.counter) : "memory");
+        s_last = t == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    v = zadd::kZ;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) {
+        unsigned long long w;
+        asm volatile("ld.relaxed.gpu.u64 %0, [%1];" : "=l"(w) : "l"(ws.partials + 1 + i) : "memory");
+        v = zadd::add(v, (uint32_t)w, qbar, D);
+    }
+    v = zech_block_merge(v, red, qbar, D);
+    if (threadIdx.x == 0) {
+        if (O.mode == OUT_ENCODE) {
+            ((uint16_t *)O.out)[0] = (uint16_t)zadd::to_code(v);  // already a Zech code: no log lookup
+        } else {  // additive (classical) form for the multi-GPU sum: g^(v+1) from the antilog table
+            const uint64_t r = v == zadd::kZ ? 0 : K.antilog[v + 1];
+            if (O.mode == OUT_PARTIAL) ((uint64_t *)O.out)[0] = r;
+            else ((uint64_t *)O.out)[0] += r;
+        }
+        *ws.counter = 0;
     }
 }
 
@@ -419,7 +559,7 @@ static int occupancy(F kernel, int block, size_t smem) {
 #ifndef GFP_DOT_PIPE
 #define GFP_DOT_PIPE 0
 #endif
-constexpr int kDotNT = 256, kDotU = 4, kFpU = 2, kZechNT = 1024, kZechU = 2;
+constexpr int kDotNT = 256, kDotU = 4, kFpU = 2, kZechNT = 1024, kZechU = 2, kZaddNT = 512, kZaddU = 2;
 constexpr bool kPipe = GFP_DOT_PIPE != 0;
 
 template <class R, int NT, int U, bool PIPE>
@@ -438,8 +578,9 @@ static int dot_occupancy(size_t smem) {
 }
 
 static bool is_zech(int pol) { return pol >= P_ZS_ALL && pol <= P_ZL_THREAD; }
-static int policy_block(int pol) { return is_zech(pol) ? kZechNT : kDotNT; }
+static int policy_block(int pol) { return pol == P_ZECH_ADD ? kZaddNT : (is_zech(pol) ? kZechNT : kDotNT); }
 static int policy_unroll(int pol) {
+    if (pol == P_ZECH_ADD) return kZaddU;
     return is_zech(pol) ? kZechU : ((pol >= P_FP_THREAD && pol <= P_FP_K2) ? kFpU : kDotU);
 }
 static int policy_width(int pol) {
@@ -490,6 +631,7 @@ static int policy_occupancy(int pol, size_t smem) {
     case pol: return dot_occupancy<__VA_ARGS__, kDotNT, kDotU, false>(smem);
         GFP_CS_CASES(GFP_OCC)
 #undef GFP_OCC
+    case P_ZECH_ADD: return occupancy(zech_add_dot_kernel<kZaddNT, kZaddU>, kZaddNT, smem);
     }
     return 1;
 }
@@ -518,6 +660,13 @@ cudaError_t launch_dot(const DotPlan &P, const KParams &K0, const void *a, const
     case pol: return launch_dot_t<__VA_ARGS__, kDotNT, kDotU, false>(P, K, a, b, n, ws, O, s);
         GFP_CS_CASES(GFP_LAUNCH)
 #undef GFP_LAUNCH
+    case P_ZECH_ADD: {
+        auto kern = zech_add_dot_kernel<kZaddNT, kZaddU>;
+        occupancy(kern, kZaddNT, P.smem);
+        kern<<<P.grid, kZaddNT, P.smem, s>>>((const uint16_t *)a, (const uint16_t *)b, n, P.head, K, ws, O);
+        count_launch();
+        return cudaGetLastError();
+    }
     }
     return cudaErrorInvalidValue;
 }
@@ -531,7 +680,12 @@ static gfp_status resolve_strategy(const gfp_info &I, int64_t n, const gfp_optio
     const int bits = opt ? opt->acc_bits : 0;
     *kblk = 0;
     *acc_bits = I.acc_bits;
-    if (strat < GFP_STRAT_AUTO || strat > GFP_STRAT_HYBRID) return GFP_E_INVAL;
+    if (strat < GFP_STRAT_AUTO || strat > GFP_STRAT_ZECH_ADD) return GFP_E_INVAL;
+    if (strat == GFP_STRAT_ZECH_ADD) {
+        if (I.rep != GFP_REP_ZECH || (bits != 0 && bits != 64)) return GFP_E_UNSUPPORTED;
+        *pol = P_ZECH_ADD;
+        return GFP_OK;
+    }
     if (strat == GFP_STRAT_AUTO && bits == 0) return GFP_OK;
     const uint64_t pm1 = I.p - 1;
     const u128 q2 = (u128)pm1 * pm1;
@@ -593,6 +747,7 @@ static const char *policy_name(int pol) {
     case P_ZL_ALL: return "dot_kernel<Zech<LARGE,ALL>>";
     case P_ZL_THREAD: return "dot_kernel<Zech<LARGE,THREAD>>";
     case P_MONT_OVF: return "dot_kernel<MontgomeryOverflow>";
+    case P_ZECH_ADD: return "zech_add_dot_kernel";
     }
     if (pol >= P_CS && pol < P_CS_END) {
         static const char *names[16] = {
@@ -613,7 +768,7 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
     const uint64_t pm1 = I.p - 1;
     const u128 q2 = (u128)pm1 * pm1;
     const u128 max64 = ~(u128)0 >> 64;
-    const size_t smem = I.rep == GFP_REP_ZECH ? (size_t)K.antilog_entries * 2 : 0;
+    size_t smem = I.rep == GFP_REP_ZECH ? (size_t)K.antilog_entries * 2 : 0;
 
     // provisional policy (the mode refinement below only depends on per-thread counts)
     int pol = 0;
@@ -628,6 +783,7 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
     gfp_status st = resolve_strategy(I, n, opt, &xpol, &kblk, &acc_bits);
     if (st != GFP_OK) return st;
     if (xpol >= 0) pol = xpol;
+    if (pol == P_ZECH_ADD) smem = (size_t)K.zplus1_entries * 2;
     const int NT = policy_block(pol), U = policy_unroll(pol), W = policy_width(pol);
     const uintptr_t pa = (uintptr_t)a, pb = (uintptr_t)b;
     int64_t head = n;
@@ -642,7 +798,9 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
     // at least one 16-byte vector per thread before capping at the resident grid: small inputs are
     // latency-bound, so spread them over as many SMs as possible (one DRAM round trip per thread)
     int64_t want = std::max<int64_t>((nvec + NT - 1) / NT, (head + NT - 1) / NT);
-    int64_t grid = std::min<int64_t>({(int64_t)dev_sms * bps, std::max<int64_t>(want, 1), (int64_t)kMaxGrid});
+    // (the pure-Zech kernel keeps one workspace slot per CTA after slot 0)
+    int64_t grid = std::min<int64_t>({(int64_t)dev_sms * bps, std::max<int64_t>(want, 1),
+                                      (int64_t)kMaxGrid - (pol == P_ZECH_ADD ? 1 : 0)});
     const int64_t threads = grid * NT;
     const int64_t iters = (nvec + threads * U - 1) / (threads * U);
     const u128 per_thread = (u128)iters * U * W + (head + threads - 1) / threads + 1;
@@ -695,11 +853,15 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
         strat = (pol >= P_CS && pol < P_CS_END) ? ((pol - P_CS) & 3) + 1
                 : (pol == P_MONT_OVF ? GFP_STRAT_OVERFLOW : (opt ? opt->strategy : GFP_STRAT_AUTO));
         if (strat == GFP_STRAT_AUTO) strat = GFP_STRAT_BLOCKED;
+        if (pol == P_ZECH_ADD) strat = GFP_STRAT_ZECH_ADD;  // no integer accumulator at all
+
         acc = strat == GFP_STRAT_OVERFLOW || strat == GFP_STRAT_HYBRID ? GFP_ACC_OVERFLOW
               : (strat == GFP_STRAT_BLOCKED ? GFP_ACC_BLOCKED : GFP_ACC_DELAYED);
         if (pol == P_FP_K2 || pol == P_FP_K1) kblk = pol == P_FP_K2 ? 2 : 1;
-        if (strat == GFP_STRAT_OVERFLOW) reductions = (int64_t)per_thread;
-        else if (strat == GFP_STRAT_BLOCKED || strat == GFP_STRAT_HYBRID)
+        if (strat == GFP_STRAT_OVERFLOW || strat == GFP_STRAT_ZECH_ADD) {
+            reductions = (int64_t)per_thread;  // one wrap test / one Zech addition (table lookup) per term
+            if (pol == P_ZECH_ADD) acc_bits = 0;
+        } else if (strat == GFP_STRAT_BLOCKED || strat == GFP_STRAT_HYBRID)
             reductions = (int64_t)(kblk ? per_thread / kblk : 0) + 1;
     }
     P->policy = pol;

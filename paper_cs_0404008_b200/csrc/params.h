@@ -17,6 +17,8 @@ struct KParams {
     const uint16_t *antilog;  // Zech antilog table (global; staged to shared memory by the kernel)
     const uint16_t *logt;     // Zech log table (global; read once by the finaliser)
     uint32_t antilog_entries;
+    const uint16_t *zplus1;   // Zech t_plus1 table in exponent form (numtheory.h zech_plus1_delta), global
+    uint32_t zplus1_entries;  // qbar + 1, padded to a multiple of 8
     // explicit-strategy kernels (gfp_dot_ex): block length for BLOCKED / HYBRID, 32-bit constants
     uint64_t kblk;
     uint32_t corr32;    // 2^32 mod p

@@ -200,3 +200,19 @@ def test_plan_rejections():
     assert e.value.status == E_INVAL
     assert P(2 ** 31 - 1, MO, 10, strategy=gfp.OVERFLOW)["kernel"] == "dot_kernel<MontgomeryOverflow>"
     assert P(67108859, FP, 2, strategy=gfp.DELAYED)["kernel"] == "dot_kernel<Fp64<0>>"
+
+
+def test_plan_zech_add():
+    """Pure-Zech accumulation (F3): Zech only, one table lookup per term, no integer accumulator."""
+    P = gfp.plan
+    d = P(32749, ZE, 2 ** 26, strategy=gfp.ZECH_ADD)
+    assert d["kernel"] == "zech_add_dot_kernel" and d["strategy_name"] == "zech_add"
+    assert d["acc_bits"] == 0 and d["reductions_per_thread"] >= d["terms_per_thread"] > 0
+    assert P(65521, ZE, 10, strategy=gfp.ZECH_ADD)["kernel"] == "zech_add_dot_kernel"
+    for rep, p in [(CL, 65521), (MO, 2 ** 31 - 1), (FP, 67108859)]:
+        with pytest.raises(gfp.GfpError) as e:
+            P(p, rep, 10, strategy=gfp.ZECH_ADD)
+        assert e.value.status == E_UNSUPPORTED
+    with pytest.raises(gfp.GfpError) as e:
+        P(32749, ZE, 10, strategy=gfp.ZECH_ADD, acc_bits=32)
+    assert e.value.status == E_UNSUPPORTED
