@@ -39,7 +39,7 @@ size_t dtype_size(int dt) { return dt == GFP_U16 ? 2 : (dt == GFP_U32 ? 4 : 8); 
 struct Ctx {
     gfp_info info;
     dev::KParams K;
-    uint16_t *d_antilog = nullptr, *d_log = nullptr, *d_zplus1 = nullptr;
+    uint16_t *d_antilog = nullptr, *d_log = nullptr, *d_zplus1 = nullptr, *d_zplus1s = nullptr;
 };
 
 std::mutex g_mu;
@@ -104,9 +104,21 @@ gfp_status get_ctx(uint64_t p, gfp_rep rep, gfp_dtype dt, Ctx **out) {
         logt.resize((logt.size() + 7) & ~size_t(7), 0);
         anti.resize((anti.size() + 7) & ~size_t(7), 0);
         delta.resize((delta.size() + 7) & ~size_t(7), 0);
+        // byte-scaled, doubled copy for the fast S = 2 kernel (small fields): index e in [0, 2 qbar] holds
+        // 2 delta[e mod qbar], index 2 qbar + 1 the "add nothing" 0
+        const bool scaled = zech_small_layout(p);
+        const uint64_t qbar = p - 1;
+        std::vector<uint16_t> delta2(scaled ? ((2 * qbar + 2 + 7) & ~uint64_t(7)) : 0, 0);
+        for (uint64_t e = 0; scaled && e <= 2 * qbar; ++e) {
+            const uint16_t v = delta[e % qbar];
+            delta2[e] = v == kZechDeltaZero ? v : (uint16_t)(2 * v);
+        }
         cudaError_t e = cudaMalloc(&c->d_log, logt.size() * 2);
         if (e == cudaSuccess) e = cudaMalloc(&c->d_antilog, anti.size() * 2);
         if (e == cudaSuccess) e = cudaMalloc(&c->d_zplus1, delta.size() * 2);
+        if (e == cudaSuccess && scaled) e = cudaMalloc(&c->d_zplus1s, delta2.size() * 2);
+        if (e == cudaSuccess && scaled)
+            e = cudaMemcpy(c->d_zplus1s, delta2.data(), delta2.size() * 2, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(c->d_log, logt.data(), logt.size() * 2, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(c->d_antilog, anti.data(), anti.size() * 2, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(c->d_zplus1, delta.data(), delta.size() * 2, cudaMemcpyHostToDevice);
@@ -114,6 +126,7 @@ gfp_status get_ctx(uint64_t p, gfp_rep rep, gfp_dtype dt, Ctx **out) {
             cudaFree(c->d_log);
             cudaFree(c->d_antilog);
             cudaFree(c->d_zplus1);
+            cudaFree(c->d_zplus1s);
             delete c;
             return cuda_fail(e, "Zech table upload");
         }
@@ -121,6 +134,8 @@ gfp_status get_ctx(uint64_t p, gfp_rep rep, gfp_dtype dt, Ctx **out) {
         K.logt = c->d_log;
         K.antilog_entries = (uint32_t)anti.size();
         K.zplus1 = c->d_zplus1;
+        K.zplus1s = c->d_zplus1s;
+        K.zplus1s_entries = (uint32_t)delta2.size();
         K.zplus1_entries = (uint32_t)delta.size();
     }
     g_ctx[key] = c;
@@ -266,7 +281,8 @@ gfp_status gfp_plan(uint64_t p, gfp_rep rep, gfp_dtype dt, int64_t n, const gfp_
     memset(&K, 0, sizeof(K));
     K.p = p;
     K.antilog_entries = (uint32_t)((I.table_bytes / 2 + 7) & ~uint64_t(7));
-    K.zplus1_entries = (uint32_t)((p + 7) & ~uint64_t(7));  // qbar + 1 = p entries
+    K.zplus1_entries = (uint32_t)((p + 1 + 7) & ~uint64_t(7));  // qbar + 2 = p + 1 entries
+    K.zplus1s_entries = (uint32_t)((2 * (p - 1) + 2 + 7) & ~uint64_t(7));
     DotPlan plan;
     const void *aligned_ptr = (const void *)(uintptr_t)4096;
     if ((st = plan_dot(I, K, aligned_ptr, aligned_ptr, n, opt, &plan)) != GFP_OK) return plan_fail(st);
@@ -403,6 +419,7 @@ void gfp_release_caches(void) {
         cudaFree(kv.second->d_antilog);
         cudaFree(kv.second->d_log);
         cudaFree(kv.second->d_zplus1);
+        cudaFree(kv.second->d_zplus1s);
         delete kv.second;
     }
     g_ctx.clear();

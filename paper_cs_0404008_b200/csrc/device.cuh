@@ -263,41 +263,52 @@ struct Zech {
 };
 
 
-// Pure-Zech arithmetic (sec. 2.4, Table 1).  Values live in
-// "u space": a nonzero element g^e with code e in [1, qbar] (code qbar = g^0) is held as
-// u = e - 1 in [0, qbar), and the zero element as kZ.  Then
-//   multiplication  g^i * g^j:  u = i + j - 1 (- qbar)                       (Table 1 row 1)
-//   addition        g^(s+1) + g^(c+1) = g^(s+1) (1 + g^k),  k = c - s (+ qbar),
-//                   u = s + delta[k] (- qbar), delta[k] = log(1 + g^k)        (Table 1 "Addition")
-// with delta the t_plus1 table in exponent form (numtheory.h), kZechDeltaZero where 1 + g^k = 0.
-// Each "(+/- qbar)" test is one unsigned min: v = min(v, v - qbar) folds [0, 2 qbar) into [0, qbar).
+// Pure-Zech arithmetic (sec. 2.4, Table 1).  A nonzero element
+// g^e is held as v = S e with e in [0, qbar] (e = qbar is g^0 again: the code qbar of P:126-131), the
+// zero element as kZ.  S = 2 makes v a byte offset into the u16 table (one register + the table base
+// per address); S = 1 when 2 qbar does not fit the u16 entries.  With q = S qbar:
+//   multiplication  g^i * g^j:  v = S (i + j) (- q)                           (Table 1 row 1)
+//   addition        g^s + g^c = g^s (1 + g^(c - s)),  k = c - s (+ q),
+//                   v = s + delta[k] (- q), delta[k] = S log(1 + g^k)           (Table 1 "Addition")
+// with delta the t_plus1 table in scaled exponent form (numtheory.h), 0xFFFF where 1 + g^k = 0.
+// Each "(+/- q)" test is one unsigned min: v = min(v, v - q) or min(k, k + q).
 namespace zadd {
-constexpr uint32_t kZ = 0xFFFFFFFFu;   // the zero element
-constexpr uint32_t kDZero = 0xFFFFu;  // delta sentinel: 1 + g^k = 0
+template <int S>
+struct Ops {
+    static constexpr uint32_t kZ = 0u - (uint32_t)S;  // the zero element (-S: index math stays in the table)
+    static constexpr uint32_t kDZero = 0xFFFFu;        // delta sentinel: 1 + g^k = 0 (odd: never a scaled delta)
 
-__device__ __forceinline__ uint32_t fold(uint32_t v, uint32_t qbar) { return min(v, v - qbar); }
+    __device__ __forceinline__ static uint32_t fold(uint32_t v, uint32_t q) { return min(v, v - q); }
+    __device__ __forceinline__ static uint32_t lookup(const uint16_t *delta, uint32_t k) {
+        return *reinterpret_cast<const uint16_t *>(reinterpret_cast<const char *>(delta) + k * (2 / S));
+    }
 
-// product of two codes -> u space (a zero operand gives kZ)
-__device__ __forceinline__ uint32_t mul(uint32_t ci, uint32_t cj, uint32_t qbar) {
-    const uint32_t u = fold(ci + cj - 1u, qbar);
-    return (ci == 0 || cj == 0) ? kZ : u;
-}
+    // product of two codes (each in [0, qbar]); a zero operand gives kZ.  Result in [0, q].
+    __device__ __forceinline__ static uint32_t mul(uint32_t ci, uint32_t cj, uint32_t q) {
+        const uint32_t v = fold((uint32_t)S * (ci + cj), q);
+        return (ci == 0 || cj == 0) ? kZ : v;
+    }
 
-// s + c in u space, either operand possibly kZ.  The table index stays in [0, qbar] in every case
-// (s = kZ: k = c + 1 <= qbar; c = kZ: k = qbar - 1 - s), so the lookup never leaves the table.
-__device__ __forceinline__ uint32_t add(uint32_t s, uint32_t c, uint32_t qbar, const uint16_t *delta) {
-    uint32_t k = c - s;
-    k = min(k, k + qbar);
-    const uint32_t d = delta[k];
-    uint32_t r = fold(s + d, qbar);
-    r = d == kDZero ? kZ : r;  // g^(s+1) (1 + g^k) = 0
-    r = s == kZ ? c : r;
-    r = c == kZ ? s : r;
-    return r;
-}
+    // s + c, either operand possibly kZ, values in [0, q].  The index stays in [0, q] in every case
+    // (s = kZ: k = c + S; c = kZ: k = q - S - s), so the lookup never leaves the table.
+    __device__ __forceinline__ static uint32_t add(uint32_t s, uint32_t c, uint32_t q, const uint16_t *delta) {
+        uint32_t k = c - s;
+        k = min(k, k + q);
+        const uint32_t d = lookup(delta, k);
+        uint32_t r = fold(s + d, q);
+        r = d == kDZero ? kZ : r;  // g^s (1 + g^k) = 0
+        r = s == kZ ? c : r;
+        r = c == kZ ? s : r;
+        return r;
+    }
 
-// u space -> Zech code: zero -> 0, u -> u + 1
-__device__ __forceinline__ uint32_t to_code(uint32_t u) { return u == kZ ? 0u : u + 1u; }
+    // exponent in [1, qbar] (qbar for g^0) of a nonzero value: the Zech code of P:126-131
+    __device__ __forceinline__ static uint32_t code_nz(uint32_t v, uint32_t qbar) {
+        const uint32_t e = v / S;
+        return e == 0 ? qbar : e;
+    }
+    __device__ __forceinline__ static uint32_t to_code(uint32_t v, uint32_t qbar) { return v == kZ ? 0u : code_nz(v, qbar); }
+};
 }  // namespace zadd
 
 // ------------------------------------------------------------------------------ explicit strategies

@@ -197,38 +197,97 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
 // lookup latency of the dependent additions; they are merged by Zech additions in the thread, the
 // warp (shuffles) and the CTA, and each CTA's merged value goes to the workspace, where the last CTA
 // to arrive on the counter merges them all and encodes.  No integer sum, no remainder anywhere.
-__device__ __forceinline__ uint32_t zech_warp_merge(uint32_t v, uint32_t qbar, const uint16_t *D) {
+template <int S>
+__device__ __forceinline__ uint32_t zech_warp_merge(uint32_t v, uint32_t q, const uint16_t *D) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = zadd::add(v, __shfl_xor_sync(0xFFFFFFFFu, v, o), qbar, D);
+    for (int o = 16; o > 0; o >>= 1) v = zadd::Ops<S>::add(v, __shfl_xor_sync(0xFFFFFFFFu, v, o), q, D);
     return v;
 }
 
 // Merge over the CTA; valid in thread 0.
-__device__ __forceinline__ uint32_t zech_block_merge(uint32_t v, uint32_t *red, uint32_t qbar, const uint16_t *D) {
+template <int S>
+__device__ __forceinline__ uint32_t zech_block_merge(uint32_t v, uint32_t *red, uint32_t q, const uint16_t *D) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-    v = zech_warp_merge(v, qbar, D);
+    v = zech_warp_merge<S>(v, q, D);
     __syncthreads();
     if (lane == 0) red[warp] = v;
     __syncthreads();
-    v = zadd::kZ;
-    if (warp == 0) v = zech_warp_merge(lane < nw ? red[lane] : zadd::kZ, qbar, D);
+    v = zadd::Ops<S>::kZ;
+    if (warp == 0) v = zech_warp_merge<S>(lane < nw ? red[lane] : zadd::Ops<S>::kZ, q, D);
     return v;
 }
 
-__device__ __forceinline__ void zech_add_pair(uint32_t (&acc)[8], int j, uint32_t x, uint32_t y, uint32_t qbar,
+template <int S>
+__device__ __forceinline__ void zech_add_pair(uint32_t (&acc)[8], int j, uint32_t x, uint32_t y, uint32_t q,
                                               const uint16_t *D) {
-    acc[2 * j] = zadd::add(acc[2 * j], zadd::mul(x & 0xFFFFu, y & 0xFFFFu, qbar), qbar, D);
-    acc[2 * j + 1] = zadd::add(acc[2 * j + 1], zadd::mul(x >> 16, y >> 16, qbar), qbar, D);
+    using Z = zadd::Ops<S>;
+    acc[2 * j] = Z::add(acc[2 * j], Z::mul(x & 0xFFFFu, y & 0xFFFFu, q), q, D);
+    acc[2 * j + 1] = Z::add(acc[2 * j + 1], Z::mul(x >> 16, y >> 16, q), q, D);
 }
 
-template <int NT, int U>
+template <int S>
+__device__ __forceinline__ void zech_add_vec(uint32_t (&acc)[8], uint4 x, uint4 y, uint32_t q, const uint16_t *D) {
+    zech_add_pair<S>(acc, 0, x.x, y.x, q, D);
+    zech_add_pair<S>(acc, 1, x.y, y.y, q, D);
+    zech_add_pair<S>(acc, 2, x.z, y.z, q, D);
+    zech_add_pair<S>(acc, 3, x.w, y.w, q, D);
+}
+
+// Fast path (S = 2, odd p, 2 qbar < 2^16): the running sums never hold the zero element, so the
+// additions need no zero tests.  Each sum starts at the element 1 (v = 0) and `corr` (checked
+// arithmetic) books -1 for it.  A zero product is steered to the table's "add nothing" entry (byte
+// offset kzero, delta 0).  A sum that cancels (delta sentinel 0xFFFF) becomes odd -- every valid v is
+// even -- and is repaired once per vector: restart at 1, book -1 in corr.  The product index
+// 2 (ci + cj) - s is not folded first: the table is doubled (indices [0, 2q]) instead.
+// Per term: lane extract, one multiply-add for the index, one index fold, one select, one lookup,
+// one add and one fold for the sum.
+__device__ __forceinline__ uint32_t zech_fast_add(uint32_t s, uint32_t lane_sum, bool zero, uint32_t q,
+                                                  uint32_t kzero, uint32_t tab) {
+    uint32_t k = 2u * lane_sum - s;  // 2 (ci + cj) - s in (4 - q, 2q]
+    k = min(k, k + q);
+    k = zero ? kzero : k;
+    uint16_t d;
+    asm("ld.shared.u16 %0, [%1];" : "=h"(d) : "r"(tab + k));
+    return zadd::Ops<2>::fold(s + d, q);
+}
+
+__device__ __forceinline__ void zech_fast_pair(uint32_t (&acc)[8], int j, uint32_t x, uint32_t y, uint32_t q,
+                                               uint32_t kzero, uint32_t tab) {
+    const uint32_t P = x + y;             // codes < 2^15: both 16-bit lane sums fit, no carry between lanes
+    const uint32_t m = __vminu2(x, y);    // per lane min(ci, cj): zero iff the lane's product is zero
+    acc[2 * j] = zech_fast_add(acc[2 * j], P & 0xFFFFu, (m & 0xFFFFu) == 0, q, kzero, tab);
+    acc[2 * j + 1] = zech_fast_add(acc[2 * j + 1], P >> 16, m < 0x10000u, q, kzero, tab);
+}
+
+__device__ __forceinline__ void zech_repair(uint32_t (&acc)[8], uint32_t &corr, uint32_t q, const uint16_t *D) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if (acc[j] & 1u) {  // this sum cancelled to zero: restart it at 1 (v = 0), book -1 (v = q/2) in corr
+            acc[j] = 0u;
+            corr = zadd::Ops<2>::add(corr, q / 2u, q, D);
+        }
+    }
+}
+
+__device__ __forceinline__ void zech_fast_vec(uint32_t (&acc)[8], uint32_t &corr, uint4 x, uint4 y, uint32_t q,
+                                              uint32_t kzero, const uint16_t *D) {
+    const uint32_t tab = (uint32_t)__cvta_generic_to_shared(D);  // table base as a shared-window offset
+    zech_fast_pair(acc, 0, x.x, y.x, q, kzero, tab);
+    zech_fast_pair(acc, 1, x.y, y.y, q, kzero, tab);
+    zech_fast_pair(acc, 2, x.z, y.z, q, kzero, tab);
+    zech_fast_pair(acc, 3, x.w, y.w, q, kzero, tab);
+    if ((acc[0] | acc[1] | acc[2] | acc[3] | acc[4] | acc[5] | acc[6] | acc[7]) & 1u) zech_repair(acc, corr, q, D);
+}
+
+template <int NT, int U, int S, bool FAST>
 __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__restrict__ a,
                                                           const uint16_t *__restrict__ b, int64_t n, int64_t head,
                                                           KParams K, Workspace ws, OutSpec O) {
+    using Z = zadd::Ops<S>;
     extern __shared__ __align__(16) uint16_t s_delta[];
     __shared__ uint32_t red[32];
     __shared__ int s_last;
-    const uint32_t qbar = K.qbar;
+    const uint32_t q = (uint32_t)S * K.qbar;
     const int64_t gtid = (int64_t)blockIdx.x * NT + threadIdx.x;
     const int64_t gstride = (int64_t)gridDim.x * NT;
     const int64_t nvec = (n - head) / 8;
@@ -247,13 +306,17 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
             cb[u] = ld_stream(bv + i0 + u * NT);
         }
     }
-    stage_table(s_delta, K.zplus1, K.zplus1_entries);
+    stage_table(s_delta, FAST ? K.zplus1s : K.zplus1, FAST ? K.zplus1s_entries : K.zplus1_entries);
+    const uint32_t kzero = 2u * q + 2u;  // fast path: byte offset of the "add nothing" entry
     __syncthreads();
     const uint16_t *D = s_delta;
 
-    uint32_t acc[8];
+    uint32_t acc[8], corr = Z::kZ;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = zadd::kZ;
+    for (int j = 0; j < 8; ++j) {
+        acc[j] = FAST ? 0u : Z::kZ;  // fast path: start at the element 1 (v = 0), booked as -1 in corr
+        if (FAST) corr = Z::add(corr, q / 2u, q, D);
+    }
     while (have) {
         const int64_t nx = i0 + step;
         const bool more = nx + (U - 1) * NT < nvec;
@@ -267,10 +330,8 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            zech_add_pair(acc, 0, ca[u].x, cb[u].x, qbar, D);
-            zech_add_pair(acc, 1, ca[u].y, cb[u].y, qbar, D);
-            zech_add_pair(acc, 2, ca[u].z, cb[u].z, qbar, D);
-            zech_add_pair(acc, 3, ca[u].w, cb[u].w, qbar, D);
+            if constexpr (FAST) zech_fast_vec(acc, corr, ca[u], cb[u], q, kzero, D);
+            else zech_add_vec<S>(acc, ca[u], cb[u], q, D);
         }
         i0 = nx;
         have = more;
@@ -284,24 +345,23 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
     for (int u = 0; u < U; ++u) {
         if (i0 + u * NT < nvec) {
             const uint4 x = ld_stream(av + i0 + u * NT), y = ld_stream(bv + i0 + u * NT);
-            zech_add_pair(acc, 0, x.x, y.x, qbar, D);
-            zech_add_pair(acc, 1, x.y, y.y, qbar, D);
-            zech_add_pair(acc, 2, x.z, y.z, qbar, D);
-            zech_add_pair(acc, 3, x.w, y.w, qbar, D);
+            if constexpr (FAST) zech_fast_vec(acc, corr, x, y, q, kzero, D);
+            else zech_add_vec<S>(acc, x, y, q, D);
         }
     }
-    for (int64_t i = gtid; i < head; i += gstride) acc[0] = zadd::add(acc[0], zadd::mul(a[i], b[i], qbar), qbar, D);
+    for (int64_t i = gtid; i < head; i += gstride) acc[0] = Z::add(acc[0], Z::mul(a[i], b[i], q), q, D);
     for (int64_t i = head + nvec * 8 + gtid; i < n; i += gstride)
-        acc[1] = zadd::add(acc[1], zadd::mul(a[i], b[i], qbar), qbar, D);
+        acc[1] = Z::add(acc[1], Z::mul(a[i], b[i], q), q, D);
 
     // merge: thread (tree over its 8 accumulators) -> warp -> CTA -> workspace -> last CTA
-    acc[0] = zadd::add(acc[0], acc[1], qbar, D);
-    acc[2] = zadd::add(acc[2], acc[3], qbar, D);
-    acc[4] = zadd::add(acc[4], acc[5], qbar, D);
-    acc[6] = zadd::add(acc[6], acc[7], qbar, D);
-    acc[0] = zadd::add(acc[0], acc[2], qbar, D);
-    acc[4] = zadd::add(acc[4], acc[6], qbar, D);
-    uint32_t v = zech_block_merge(zadd::add(acc[0], acc[4], qbar, D), red, qbar, D);
+    acc[0] = Z::add(acc[0], acc[1], q, D);
+    acc[2] = Z::add(acc[2], acc[3], q, D);
+    acc[4] = Z::add(acc[4], acc[5], q, D);
+    acc[6] = Z::add(acc[6], acc[7], q, D);
+    acc[6] = Z::add(acc[6], corr, q, D);  // only nonzero on the fast path (corr starts at zero)
+    acc[0] = Z::add(acc[0], acc[2], q, D);
+    acc[4] = Z::add(acc[4], acc[6], q, D);
+    uint32_t v = zech_block_merge<S>(Z::add(acc[0], acc[4], q, D), red, q, D);
     if (threadIdx.x == 0) {
         ws.partials[1 + blockIdx.x] = v;
         unsigned int t;
@@ -310,18 +370,18 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
     }
     __syncthreads();
     if (!s_last) return;
-    v = zadd::kZ;
+    v = Z::kZ;
     for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) {
         unsigned long long w;
         asm volatile("ld.relaxed.gpu.u64 %0, [%1];" : "=l"(w) : "l"(ws.partials + 1 + i) : "memory");
-        v = zadd::add(v, (uint32_t)w, qbar, D);
+        v = Z::add(v, (uint32_t)w, q, D);
     }
-    v = zech_block_merge(v, red, qbar, D);
+    v = zech_block_merge<S>(v, red, q, D);
     if (threadIdx.x == 0) {
         if (O.mode == OUT_ENCODE) {
-            ((uint16_t *)O.out)[0] = (uint16_t)zadd::to_code(v);  // already a Zech code: no log lookup
-        } else {  // additive (classical) form for the multi-GPU sum: g^(v+1) from the antilog table
-            const uint64_t r = v == zadd::kZ ? 0 : K.antilog[v + 1];
+            ((uint16_t *)O.out)[0] = (uint16_t)Z::to_code(v, K.qbar);  // already a Zech code: no log lookup
+        } else {  // additive (classical) form for the multi-GPU sum: g^(u+1) from the antilog table
+            const uint64_t r = v == Z::kZ ? 0 : K.antilog[Z::code_nz(v, K.qbar)];  // g^code, both layouts
             if (O.mode == OUT_PARTIAL) ((uint64_t *)O.out)[0] = r;
             else ((uint64_t *)O.out)[0] += r;
         }
@@ -559,7 +619,7 @@ static int occupancy(F kernel, int block, size_t smem) {
 #ifndef GFP_DOT_PIPE
 #define GFP_DOT_PIPE 0
 #endif
-constexpr int kDotNT = 256, kDotU = 4, kFpU = 2, kZechNT = 1024, kZechU = 2, kZaddNT = 512, kZaddU = 2;
+constexpr int kDotNT = 256, kDotU = 4, kFpU = 2, kZechNT = 1024, kZechU = 2, kZaddNT = 1024, kZaddU = 2;
 constexpr bool kPipe = GFP_DOT_PIPE != 0;
 
 template <class R, int NT, int U, bool PIPE>
@@ -577,6 +637,8 @@ static int dot_occupancy(size_t smem) {
     return occupancy(dot_kernel<R, NT, U, PIPE>, NT, smem);
 }
 
+// pure-Zech fast path: small fields (2 qbar < 2^16, byte-offset table) of odd characteristic
+static bool zech_add_fast(uint64_t p) { return zech_small_layout(p) && p > 2; }
 static bool is_zech(int pol) { return pol >= P_ZS_ALL && pol <= P_ZL_THREAD; }
 static int policy_block(int pol) { return pol == P_ZECH_ADD ? kZaddNT : (is_zech(pol) ? kZechNT : kDotNT); }
 static int policy_unroll(int pol) {
@@ -631,7 +693,7 @@ static int policy_occupancy(int pol, size_t smem) {
     case pol: return dot_occupancy<__VA_ARGS__, kDotNT, kDotU, false>(smem);
         GFP_CS_CASES(GFP_OCC)
 #undef GFP_OCC
-    case P_ZECH_ADD: return occupancy(zech_add_dot_kernel<kZaddNT, kZaddU>, kZaddNT, smem);
+    case P_ZECH_ADD: return occupancy(zech_add_dot_kernel<kZaddNT, kZaddU, 2, true>, kZaddNT, smem);
     }
     return 1;
 }
@@ -661,7 +723,9 @@ cudaError_t launch_dot(const DotPlan &P, const KParams &K0, const void *a, const
         GFP_CS_CASES(GFP_LAUNCH)
 #undef GFP_LAUNCH
     case P_ZECH_ADD: {
-        auto kern = zech_add_dot_kernel<kZaddNT, kZaddU>;
+        // fast path for small odd-characteristic fields (p = 2 has qbar = 1: the checked kernel)
+        auto kern = zech_add_fast(K.p) ? zech_add_dot_kernel<kZaddNT, kZaddU, 2, true>
+                                                        : zech_add_dot_kernel<kZaddNT, kZaddU, 1, false>;
         occupancy(kern, kZaddNT, P.smem);
         kern<<<P.grid, kZaddNT, P.smem, s>>>((const uint16_t *)a, (const uint16_t *)b, n, P.head, K, ws, O);
         count_launch();
@@ -783,7 +847,7 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
     gfp_status st = resolve_strategy(I, n, opt, &xpol, &kblk, &acc_bits);
     if (st != GFP_OK) return st;
     if (xpol >= 0) pol = xpol;
-    if (pol == P_ZECH_ADD) smem = (size_t)K.zplus1_entries * 2;
+    if (pol == P_ZECH_ADD) smem = (size_t)(zech_add_fast(I.p) ? K.zplus1s_entries : K.zplus1_entries) * 2;
     const int NT = policy_block(pol), U = policy_unroll(pol), W = policy_width(pol);
     const uintptr_t pa = (uintptr_t)a, pb = (uintptr_t)b;
     int64_t head = n;

@@ -184,7 +184,7 @@ void zech_tables(uint64_t p, uint64_t g, std::vector<uint16_t> &log_table, std::
 
 void zech_plus1_delta(uint64_t p, const std::vector<uint16_t> &log_table, std::vector<uint16_t> &delta) {
     const uint64_t qbar = p - 1;
-    delta.assign(qbar + 1, 0);
+    delta.assign(qbar + 2, 0);
     std::vector<uint64_t> pw(qbar + 1);  // exponent -> element g^k, inverted from the log table
     for (uint64_t x = 1; x < p; ++x) pw[log_table[x] % qbar] = x;
     for (uint64_t k = 0; k < qbar; ++k) {
@@ -192,6 +192,7 @@ void zech_plus1_delta(uint64_t p, const std::vector<uint16_t> &log_table, std::v
         delta[k] = one_plus == 0 ? kZechDeltaZero : (uint16_t)(log_table[one_plus] % qbar);
     }
     delta[qbar] = delta[0];  // index qbar aliases 0 (g^qbar = g^0)
+    delta[qbar + 1] = 0;     // "add nothing": the index a zero product is steered to (s + 0 = s)
 }
 
 gfp_status describe(uint64_t p, gfp_rep rep, gfp_dtype dt, gfp_info *info) {

@@ -45,7 +45,8 @@ void zech_tables(uint64_t p, uint64_t g, std::vector<uint16_t> &log_table,
 
 // Pure-Zech addition table (sec. 2.4, the t_plus1 table in exponent form):
 // delta[k] = the exponent d in [0, qbar) with g^d = 1 + g^k, for k in [0, qbar]; kZechDeltaZero when
-// 1 + g^k = 0 (k = qbar/2).  delta[qbar] = delta[0].  Built from log_table (zech_tables).
+// 1 + g^k = 0 (k = qbar/2).  delta[qbar] = delta[0]; delta[qbar + 1] = 0 (the entry a zero product is
+// steered to: adding delta 0 leaves the sum unchanged).  Built from log_table (zech_tables).
 constexpr uint16_t kZechDeltaZero = 0xFFFF;
 void zech_plus1_delta(uint64_t p, const std::vector<uint16_t> &log_table, std::vector<uint16_t> &delta);
 
