@@ -210,6 +210,58 @@ gfp_status gfp_plan(uint64_t p, gfp_rep rep, gfp_dtype dt, int64_t n, const gfp_
 gfp_status gfp_dot_host(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
                         void *out, void *stream);
 
+/* ---- Install-time tuning (the paper's conclusion: an optimal dot "should
+ * switch from block methods to a floating point representation according to the vector and prime size
+ * and to the architecture ... the idea is to use an Automated Empirical Optimization of Software in
+ * order to produce a library which would determine and choose the best switching thresholds at
+ * install time").
+ *
+ * gfp_tune runs, on the current device and `stream`, every admissible accumulation of sec. 3 for each
+ * case (classical: the built-in plan and DELAYED / BLOCKED / OVERFLOW / HYBRID with m = 32 and 64;
+ * Montgomery: built-in and overflow-Montgomery; fp64: built-in, DELAYED, BLOCKED; Zech: built-in and
+ * ZECH_ADD) on synthetic canonical inputs generated on the device, checks that every candidate returns
+ * the same field element(s) (GFP_E_CUDA with a message otherwise: an exactness failure), and records
+ * the fastest in the library's tuning table (one entry per case; a re-tuned case replaces its entry).
+ * Each candidate is timed with CUDA events over about ms_per_candidate milliseconds (at least 3 calls,
+ * after 2 warm-up calls).  Device memory for the inputs is allocated and freed inside the call.
+ *
+ * GFP_STRAT_AUTO (gfp_dot, gfp_dot_batch, gfp_dot_partial, gfp_dot_ex / _batch_ex / gfp_plan with a NULL
+ * or all-zero gfp_options) then follows the table: among the entries with the call's (rep, dtype, kind)
+ * it takes the one nearest in (log2 p, log2 n) (L1 distance; first entry on ties) and uses its strategy
+ * if that strategy is admissible for the call's (p, n); otherwise -- or with an empty table -- the
+ * built-in analytic plan.  On the first AUTO call of a process the library loads a table (gfp_tune_save
+ * format) from the file the environment variable GFP_TUNE_FILE names ("" = none), or, when it is unset,
+ * from gfp_tune.txt in the directory of libgfp.so (written at install time by
+ * `python -m paper_cs_0404008_b200.autotune --out <that directory>/gfp_tune.txt`); a missing or invalid
+ * file leaves the table empty.  gfp_tune / _set / _load / _clear take precedence over that load. */
+typedef struct {
+    int32_t rep, dtype;
+    int32_t kind;  /* 0: single dot of n terms; 1: batch of rows x n (gfp_dot_batch) */
+    int32_t pad0;
+    uint64_t p;
+    int64_t n, rows;
+} gfp_tune_case;
+
+typedef struct {
+    int32_t rep, dtype, kind;
+    int32_t strategy, acc_bits; /* the winner; strategy GFP_STRAT_AUTO = the built-in plan won */
+    int32_t pad0;
+    uint64_t p;
+    int64_t n, rows;
+    double us_best, us_builtin; /* measured microseconds per call: the winner, the built-in plan */
+} gfp_tune_entry;
+
+gfp_status gfp_tune(const gfp_tune_case *cases, int32_t ncases, double ms_per_candidate, void *stream);
+/* host: copy up to cap entries of the table to out (out may be NULL with cap 0); returns the count. */
+int32_t gfp_tune_entries(gfp_tune_entry *out, int32_t cap);
+/* host: replace the table by `count` entries (validated: known rep/dtype/kind/strategy, p > 1, n >= 0). */
+gfp_status gfp_tune_set(const gfp_tune_entry *entries, int32_t count);
+/* host: text file, a "# gfp-tune v1" line then one entry per line:
+ * rep dtype kind p n rows strategy acc_bits us_best us_builtin */
+gfp_status gfp_tune_save(const char *path);
+gfp_status gfp_tune_load(const char *path);
+void gfp_tune_clear(void);
+
 /* Number of kernels the library launched on this host thread since the
  * last reset (evidence for the bench's gpu_launches claim). */
 uint64_t gfp_launch_count(int reset);

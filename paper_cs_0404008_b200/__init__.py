@@ -21,7 +21,7 @@ __all__ = [
     "CLASSICAL", "MONTGOMERY", "FP64", "ZECH", "AUTO", "DELAYED", "BLOCKED", "OVERFLOW", "HYBRID", "ZECH_ADD",
     "GfpError", "lib", "query", "plan", "dot", "dot_ex", "dot_batch", "dot_batch_ex",
     "dot_partial", "finalize", "to_rep", "from_rep", "dot_host", "launch_count", "release_caches",
-    "rep_dtype",
+    "rep_dtype", "tune", "tune_entries", "tune_set", "tune_save", "tune_load", "tune_clear",
 ]
 
 CLASSICAL, MONTGOMERY, FP64, ZECH = 0, 1, 2, 3
@@ -59,6 +59,18 @@ class GfpPlanInfo(ctypes.Structure):
                 ("kernel", ctypes.c_char * 64)]
 
 
+class GfpTuneCase(ctypes.Structure):
+    _fields_ = [("rep", ctypes.c_int32), ("dtype", ctypes.c_int32), ("kind", ctypes.c_int32),
+                ("pad0", ctypes.c_int32), ("p", ctypes.c_uint64), ("n", ctypes.c_int64), ("rows", ctypes.c_int64)]
+
+
+class GfpTuneEntry(ctypes.Structure):
+    _fields_ = [("rep", ctypes.c_int32), ("dtype", ctypes.c_int32), ("kind", ctypes.c_int32),
+                ("strategy", ctypes.c_int32), ("acc_bits", ctypes.c_int32), ("pad0", ctypes.c_int32),
+                ("p", ctypes.c_uint64), ("n", ctypes.c_int64), ("rows", ctypes.c_int64),
+                ("us_best", ctypes.c_double), ("us_builtin", ctypes.c_double)]
+
+
 lib = ctypes.CDLL(_LIB_PATH)
 _u64, _i64, _int, _vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
 _SIGS = {
@@ -73,10 +85,17 @@ _SIGS = {
     "gfp_dot_ex": [_u64, _int, _int, _vp, _vp, _i64, ctypes.POINTER(GfpOptions), _vp, _vp],
     "gfp_dot_batch_ex": [_u64, _int, _int, _vp, _i64, _vp, _i64, _i64, ctypes.POINTER(GfpOptions), _vp, _vp],
     "gfp_plan": [_u64, _int, _int, _i64, ctypes.POINTER(GfpOptions), ctypes.POINTER(GfpPlanInfo)],
+    "gfp_tune": [ctypes.POINTER(GfpTuneCase), ctypes.c_int32, ctypes.c_double, _vp],
+    "gfp_tune_entries": [ctypes.POINTER(GfpTuneEntry), ctypes.c_int32],
+    "gfp_tune_set": [ctypes.POINTER(GfpTuneEntry), ctypes.c_int32],
+    "gfp_tune_save": [ctypes.c_char_p],
+    "gfp_tune_load": [ctypes.c_char_p],
 }
 for _name, _args in _SIGS.items():
     getattr(lib, _name).argtypes = _args
     getattr(lib, _name).restype = _int
+lib.gfp_tune_clear.argtypes = []
+lib.gfp_tune_clear.restype = None
 lib.gfp_launch_count.argtypes = [_int]
 lib.gfp_launch_count.restype = _u64
 lib.gfp_status_str.argtypes = [_int]
@@ -311,3 +330,56 @@ def release_caches() -> None:
 
 def version() -> str:
     return lib.gfp_version().decode()
+
+
+# ------------------------------------------------------------------------------ install-time tuning (F4)
+_ENTRY_FIELDS = ("rep", "dtype", "kind", "strategy", "acc_bits", "p", "n", "rows", "us_best", "us_builtin")
+
+
+def _entry_dict(e) -> dict:
+    d = {f: getattr(e, f) for f in _ENTRY_FIELDS}
+    d["strategy_name"] = _STRAT_NAMES.get(d["strategy"], "?")
+    return d
+
+
+def tune(cases, ms_per_candidate: float = 20.0, device=None, stream=None) -> list:
+    """Time every admissible strategy for each case on the device and keep the fastest (gfp_tune).
+    cases: iterable of dicts {rep, p, n, dtype (torch dtype, default the rep's), kind ("dot"/"batch"),
+    rows}.  Returns the whole tuning table (list of dicts)."""
+    cs = []
+    for c in cases:
+        rep = c["rep"]
+        dt = _TORCH_DT[c.get("dtype") or rep_dtype(rep, c["p"])]
+        kind = 1 if c.get("kind", "dot") in ("batch", 1) else 0
+        cs.append(GfpTuneCase(rep, dt, kind, 0, c["p"], c["n"], c.get("rows", 0) if kind else 0))
+    arr = (GfpTuneCase * max(len(cs), 1))(*cs)
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    with torch.cuda.device(dev):
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        _check(lib.gfp_tune(arr, len(cs), ms_per_candidate, s.cuda_stream))
+    return tune_entries()
+
+
+def tune_entries() -> list:
+    n = lib.gfp_tune_entries(None, 0)
+    arr = (GfpTuneEntry * max(n, 1))()
+    n = lib.gfp_tune_entries(arr, n)
+    return [_entry_dict(arr[i]) for i in range(n)]
+
+
+def tune_set(entries) -> None:
+    es = [GfpTuneEntry(*(e.get(f, 0) if f != "pad0" else 0 for f, _ in GfpTuneEntry._fields_)) for e in entries]
+    arr = (GfpTuneEntry * max(len(es), 1))(*es)
+    _check(lib.gfp_tune_set(arr, len(es)))
+
+
+def tune_save(path: str) -> None:
+    _check(lib.gfp_tune_save(os.fsencode(path)))
+
+
+def tune_load(path: str) -> None:
+    _check(lib.gfp_tune_load(os.fsencode(path)))
+
+
+def tune_clear() -> None:
+    lib.gfp_tune_clear()

@@ -204,6 +204,10 @@ gfp_status dot_common(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, cons
 
 }  // namespace
 
+namespace gfp {
+void set_last_error(const char *msg) { t_err = msg; }
+}  // namespace gfp
+
 extern "C" {
 
 gfp_status gfp_query(uint64_t p, gfp_rep rep, gfp_dtype dt, gfp_info *info) {

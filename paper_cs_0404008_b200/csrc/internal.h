@@ -53,6 +53,15 @@ gfp_status launch_convert(const gfp_info &info, const dev::KParams &K, int dir, 
                           gfp_dtype out_dt, void *out, int64_t n, cudaStream_t s, cudaError_t *err);
 
 int num_sms(int device);
+// Set the thread-local text returned by gfp_last_error (api.cpp).
+void set_last_error(const char *msg);
+
+// Synthetic canonical elements on the device (tuner inputs): floor(hash(seed, i) p / 2^64).
+cudaError_t launch_fill(void *out, int dtype, uint64_t p, uint64_t seed, int64_t n, cudaStream_t s);
+
+// Install-time tuning table (tune.cpp): the tuned explicit options for an AUTO call of `kind` (0 dot,
+// 1 batch) with n terms (per row), or false (empty table, the built-in plan won, or tuning bypassed).
+bool tuned_options(const gfp_info &info, int kind, int64_t n, gfp_options *out);
 void count_launch();
 
 }  // namespace gfp

@@ -595,18 +595,49 @@ __global__ void __launch_bounds__(NT) convert_kernel(const TI *in, TO *out, int6
     for (int64_t i = done + gtid; i < n; i += gstride) out[i] = conv1<OP, TI, TO>(in[i], K, tab);
 }
 
+// ------------------------------------------------------------------------------ synthetic inputs (tuning)
+// Canonical elements for the install-time tuner (tune.cpp): residues floor(h p / 2^64) of a SplitMix64
+// hash of (seed, i) -- classical residues, Montgomery forms (every residue is one), exact binary64
+// integers, or Zech codes in [0, qbar] (code 0, the zero element, with probability 1/p).
+__global__ void fill_kernel(void *out, int dtype, uint64_t p, uint64_t seed, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t z = seed + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const uint64_t v = __umul64hi(z, p);
+        if (dtype == GFP_U16) ((uint16_t *)out)[i] = (uint16_t)v;
+        else if (dtype == GFP_U32) ((uint32_t *)out)[i] = (uint32_t)v;
+        else ((double *)out)[i] = (double)v;
+    }
+}
+
+cudaError_t launch_fill(void *out, int dtype, uint64_t p, uint64_t seed, int64_t n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms(dev) * 8);
+    fill_kernel<<<(int)grid, 256, 0, s>>>(out, dtype, p, seed, n);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------ launch helpers
 template <typename F>
 static int occupancy(F kernel, int block, size_t smem) {
     static std::mutex mu;
-    static std::unordered_map<std::string, int> cache;  // per (kernel, dynamic smem)
+    static std::unordered_map<std::string, int> cache;     // per (kernel, dynamic smem)
+    static std::unordered_map<uintptr_t, size_t> allowed;  // per kernel: the dynamic smem opt-in so far
     std::lock_guard<std::mutex> g(mu);
-    const std::string key = std::to_string((uintptr_t)reinterpret_cast<const void *>(kernel)) + ":" +
-                            std::to_string(smem);
+    const uintptr_t kp = (uintptr_t)reinterpret_cast<const void *>(kernel);
+    // the opt-in is a per-function attribute: only ever raise it (a kernel launched with several table
+    // sizes, e.g. Zech at several primes, must keep the largest one it has been allowed)
+    if (smem > 48 * 1024 && smem > allowed[kp]) {
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        allowed[kp] = smem;
+    }
+    const std::string key = std::to_string(kp) + ":" + std::to_string(smem);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int bps = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, block, smem) != cudaSuccess || bps < 1) bps = 1;
     cache[key] = bps;
@@ -828,6 +859,10 @@ static const char *policy_name(int pol) {
 
 gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const void *b, int64_t n,
                     const gfp_options *opt, DotPlan *P) {
+    gfp_options tuned;  // AUTO follows the install-time table when it has an admissible entry (F4)
+    if ((opt == nullptr || (opt->strategy == GFP_STRAT_AUTO && opt->acc_bits == 0)) &&
+        tuned_options(I, 0, n, &tuned) && plan_dot(I, K, a, b, n, &tuned, P) == GFP_OK)
+        return GFP_OK;
     const size_t es = elem_size(I.dtype);
     const uint64_t pm1 = I.p - 1;
     const u128 q2 = (u128)pm1 * pm1;
@@ -984,6 +1019,14 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
     int dev = 0;
     cudaGetDevice(&dev);
     *err = cudaSuccess;
+    gfp_options tuned;  // AUTO follows the install-time table when it has an admissible entry (F4)
+    if ((opt == nullptr || (opt->strategy == GFP_STRAT_AUTO && opt->acc_bits == 0)) &&
+        tuned_options(I, 1, n, &tuned)) {
+        int xpol = -1, acc_bits = 0;
+        uint64_t kblk = 0;
+        if (resolve_strategy(I, n, &tuned, &xpol, &kblk, &acc_bits) == GFP_OK && xpol >= 0 && xpol != P_ZECH_ADD)
+            opt = &tuned;
+    }
     {  // explicit strategy (gfp_dot_batch_ex): the generic warp-per-row kernel with that policy
         int xpol = -1, acc_bits = 0;
         uint64_t kblk = 0;

@@ -1,0 +1,324 @@
+// tune.cpp -- install-time empirical tuning of the accumulation strategy.
+//
+// The paper's conclusion: "an optimal version should switch from block methods to a floating
+// point representation according to the vector and prime size and to the architecture ... use an
+// Automated Empirical Optimization of Software in order to produce a library which would determine and
+// choose the best switching thresholds at install time".  gfp_tune measures every admissible strategy
+// of sec. 3 for the requested (rep, dtype, p, n) cases through the library's own C ABI, cross-checks
+// that they agree (they are all exact), and keeps the fastest; GFP_STRAT_AUTO then follows the nearest
+// tuned case.  A representation is the caller's storage choice (switching it costs a conversion pass,
+// more than the dot itself on an HBM-bound device), so the table switches strategies within one.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gfp.h"
+#include "internal.h"
+
+namespace gfp {
+namespace {
+
+std::mutex g_mu;
+std::vector<gfp_tune_entry> g_table;
+bool g_env_checked = false;
+thread_local bool t_bypass = false;  // set while timing the built-in plan
+
+bool valid_entry(const gfp_tune_entry &e) {
+    if (e.rep < GFP_REP_CLASSICAL || e.rep > GFP_REP_ZECH || e.dtype < GFP_U16 || e.dtype > GFP_F64) return false;
+    if (e.kind != 0 && e.kind != 1) return false;
+    if (e.strategy < GFP_STRAT_AUTO || e.strategy > GFP_STRAT_ZECH_ADD) return false;
+    if (e.kind == 1 && e.strategy == GFP_STRAT_ZECH_ADD) return false;  // no batch form
+    return e.p > 1 && e.n >= 0 && e.rows >= 0;
+}
+
+bool same_case(const gfp_tune_entry &e, const gfp_tune_case &c) {
+    return e.rep == c.rep && e.dtype == c.dtype && e.kind == c.kind && e.p == c.p && e.n == c.n &&
+           e.rows == (c.kind == 1 ? c.rows : 0);
+}
+
+gfp_status err(gfp_status st, const std::string &msg) {
+    set_last_error(msg.c_str());
+    return st;
+}
+
+gfp_status load_file(const char *path, std::vector<gfp_tune_entry> &out, std::string &why) {
+    FILE *f = fopen(path, "r");
+    if (!f) {
+        why = std::string("cannot open ") + path;
+        return GFP_E_INVAL;
+    }
+    char line[512];
+    int lineno = 0;
+    bool header = false;
+    while (fgets(line, sizeof line, f)) {
+        ++lineno;
+        if (lineno == 1) {
+            header = strncmp(line, "# gfp-tune v1", 13) == 0;
+            if (!header) break;
+            continue;
+        }
+        if (line[0] == '#' || line[0] == '\n') continue;
+        gfp_tune_entry e;
+        memset(&e, 0, sizeof e);
+        unsigned long long p;
+        long long n, rows;
+        if (sscanf(line, "%d %d %d %llu %lld %lld %d %d %lf %lf", &e.rep, &e.dtype, &e.kind, &p, &n, &rows,
+                   &e.strategy, &e.acc_bits, &e.us_best, &e.us_builtin) != 10) {
+            fclose(f);
+            why = std::string(path) + ":" + std::to_string(lineno) + ": malformed entry";
+            return GFP_E_INVAL;
+        }
+        e.p = p;
+        e.n = n;
+        e.rows = rows;
+        if (!valid_entry(e)) {
+            fclose(f);
+            why = std::string(path) + ":" + std::to_string(lineno) + ": invalid entry";
+            return GFP_E_INVAL;
+        }
+        out.push_back(e);
+    }
+    fclose(f);
+    if (!header) {
+        why = std::string(path) + ": missing '# gfp-tune v1' header";
+        return GFP_E_INVAL;
+    }
+    return GFP_OK;
+}
+
+struct DevBuf {
+    void *p = nullptr;
+    ~DevBuf() { cudaFree(p); }
+};
+
+size_t esize(int dt) { return dt == GFP_U16 ? 2 : (dt == GFP_U32 ? 4 : 8); }
+
+}  // namespace
+
+namespace {
+// First use in the process: load the install-time table (caller holds g_mu).
+void ensure_loaded() {
+    if (!g_env_checked) {
+        // GFP_TUNE_FILE names the table ("" disables); unset: gfp_tune.txt next to libgfp.so, the file
+        // `python -m paper_cs_0404008_b200.autotune --out <package>/gfp_tune.txt` writes at install time
+        g_env_checked = true;
+        const char *env = getenv("GFP_TUNE_FILE");
+        std::string path;
+        if (env) {
+            path = env;
+        } else {
+            Dl_info info;
+            if (dladdr(reinterpret_cast<const void *>(&gfp_tune_clear), &info) && info.dli_fname) {
+                path = info.dli_fname;
+                const size_t slash = path.rfind('/');
+                path = (slash == std::string::npos ? std::string(".") : path.substr(0, slash)) + "/gfp_tune.txt";
+            }
+        }
+        std::vector<gfp_tune_entry> v;
+        std::string why;
+        if (!path.empty() && load_file(path.c_str(), v, why) == GFP_OK) g_table = v;
+    }
+}
+}  // namespace
+
+bool tuned_options(const gfp_info &I, int kind, int64_t n, gfp_options *out) {
+    if (t_bypass) return false;
+    std::lock_guard<std::mutex> g(g_mu);
+    ensure_loaded();
+    const gfp_tune_entry *best = nullptr;
+    double bd = 0;
+    const double lp = std::log2((double)I.p), ln = std::log2((double)std::max<int64_t>(n, 1));
+    for (const auto &e : g_table) {
+        if (e.rep != I.rep || e.dtype != I.dtype || e.kind != kind) continue;
+        const double d = std::fabs(std::log2((double)e.p) - lp) + std::fabs(std::log2((double)std::max<int64_t>(e.n, 1)) - ln);
+        if (!best || d < bd) {
+            best = &e;
+            bd = d;
+        }
+    }
+    if (!best || best->strategy == GFP_STRAT_AUTO) return false;
+    out->strategy = best->strategy;
+    out->acc_bits = best->acc_bits;
+    return true;
+}
+
+}  // namespace gfp
+
+using namespace gfp;
+
+extern "C" {
+
+gfp_status gfp_tune(const gfp_tune_case *cases, int32_t ncases, double ms_per_candidate, void *stream) {
+    if ((cases == nullptr && ncases > 0) || ncases < 0 || !(ms_per_candidate > 0))
+        return err(GFP_E_INVAL, "gfp_tune: need cases (ncases >= 0) and ms_per_candidate > 0");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
+        return err(GFP_E_CUDA, "gfp_tune: cudaEventCreate failed");
+    struct EvGuard {
+        cudaEvent_t a, b;
+        ~EvGuard() {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
+    } evg{e0, e1};
+    for (int32_t ci = 0; ci < ncases; ++ci) {
+        const gfp_tune_case &c = cases[ci];
+        gfp_info I;
+        gfp_status st = gfp_query(c.p, (gfp_rep)c.rep, (gfp_dtype)c.dtype, &I);
+        if (st != GFP_OK) return st;
+        if ((c.kind != 0 && c.kind != 1) || c.n < 1 || (c.kind == 1 && c.rows < 1))
+            return err(GFP_E_INVAL, "gfp_tune: case " + std::to_string(ci) + ": kind 0/1, n >= 1, rows >= 1 (batch)");
+        const size_t es = esize(c.dtype);
+        const int64_t na = c.kind == 0 ? c.n : c.rows * c.n, nout = c.kind == 0 ? 1 : c.rows;
+        DevBuf A, B, O;
+        if (cudaMalloc(&A.p, na * es) != cudaSuccess || cudaMalloc(&B.p, c.n * es) != cudaSuccess ||
+            cudaMalloc(&O.p, nout * es + 16) != cudaSuccess)
+            return err(GFP_E_NOMEM, "gfp_tune: input allocation");
+        // residues in [0, p) (classical, Montgomery forms, fp64 integers) or Zech codes in [0, qbar]
+        if (launch_fill(A.p, c.dtype, c.p, 0x0404008ull + 2 * ci, na, s) != cudaSuccess ||
+            launch_fill(B.p, c.dtype, c.p, 0x0404009ull + 2 * ci, c.n, s) != cudaSuccess)
+            return err(GFP_E_CUDA, "gfp_tune: fill launch");
+
+        // candidates: the built-in plan first, then every explicit strategy the representation offers
+        std::vector<gfp_options> cand = {{GFP_STRAT_AUTO, 0}};
+        switch (c.rep) {
+        case GFP_REP_CLASSICAL:
+            for (int m : {32, 64})
+                for (int st2 : {GFP_STRAT_DELAYED, GFP_STRAT_BLOCKED, GFP_STRAT_OVERFLOW, GFP_STRAT_HYBRID})
+                    cand.push_back({st2, m});
+            break;
+        case GFP_REP_MONTGOMERY: cand.push_back({GFP_STRAT_OVERFLOW, 0}); break;
+        case GFP_REP_FP64:
+            cand.push_back({GFP_STRAT_DELAYED, 0});
+            cand.push_back({GFP_STRAT_BLOCKED, 0});
+            break;
+        case GFP_REP_ZECH:
+            if (c.kind == 0) cand.push_back({GFP_STRAT_ZECH_ADD, 0});
+            break;
+        }
+        auto call = [&](const gfp_options &o) -> gfp_status {
+            const bool builtin = o.strategy == GFP_STRAT_AUTO;
+            t_bypass = builtin;
+            gfp_status r = c.kind == 0
+                               ? gfp_dot_ex(c.p, (gfp_rep)c.rep, (gfp_dtype)c.dtype, A.p, B.p, c.n, builtin ? nullptr : &o,
+                                            O.p, s)
+                               : gfp_dot_batch_ex(c.p, (gfp_rep)c.rep, (gfp_dtype)c.dtype, A.p, c.n, B.p, c.rows, c.n,
+                                                  builtin ? nullptr : &o, O.p, s);
+            t_bypass = false;
+            return r;
+        };
+        std::vector<unsigned char> ref, got(nout * es);
+        double best_us = 0, builtin_us = 0;
+        gfp_options best = cand[0];
+        for (size_t k = 0; k < cand.size(); ++k) {
+            st = call(cand[k]);
+            if (st == GFP_E_BOUND || st == GFP_E_UNSUPPORTED) continue;  // not admissible for this (p, n)
+            if (st != GFP_OK) return st;
+            if (cudaMemcpyAsync(got.data(), O.p, got.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                cudaStreamSynchronize(s) != cudaSuccess)
+                return err(GFP_E_CUDA, "gfp_tune: result copy");
+            if (ref.empty()) ref = got;
+            else if (memcmp(ref.data(), got.data(), got.size()) != 0)  // every strategy is exact
+                return err(GFP_E_CUDA, "gfp_tune: case " + std::to_string(ci) + ": strategy " +
+                                           std::to_string(cand[k].strategy) + "/" + std::to_string(cand[k].acc_bits) +
+                                           " disagrees with the built-in plan");
+            for (int w = 0; w < 2; ++w) call(cand[k]);
+            cudaEventRecord(e0, s);
+            call(cand[k]);
+            cudaEventRecord(e1, s);
+            if (cudaEventSynchronize(e1) != cudaSuccess) return err(GFP_E_CUDA, "gfp_tune: timing");
+            float ms1 = 0;
+            cudaEventElapsedTime(&ms1, e0, e1);
+            const int reps = (int)std::min(2000.0, std::max(3.0, ms_per_candidate / std::max(ms1, 1e-4f)));
+            cudaEventRecord(e0, s);
+            for (int r = 0; r < reps; ++r) call(cand[k]);
+            cudaEventRecord(e1, s);
+            if (cudaEventSynchronize(e1) != cudaSuccess) return err(GFP_E_CUDA, "gfp_tune: timing");
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            const double us = 1e3 * ms / reps;
+            if (k == 0) builtin_us = us;
+            if (k == 0 || us < best_us) {
+                best_us = us;
+                best = cand[k];
+            }
+        }
+        gfp_tune_entry e;
+        memset(&e, 0, sizeof e);
+        e.rep = c.rep;
+        e.dtype = c.dtype;
+        e.kind = c.kind;
+        e.p = c.p;
+        e.n = c.n;
+        e.rows = c.kind == 1 ? c.rows : 0;
+        e.strategy = best.strategy;
+        e.acc_bits = best.acc_bits;
+        e.us_best = best_us;
+        e.us_builtin = builtin_us;
+        std::lock_guard<std::mutex> g(g_mu);
+        g_env_checked = true;  // an explicit tuning run takes precedence over GFP_TUNE_FILE
+        auto it = std::find_if(g_table.begin(), g_table.end(), [&](const gfp_tune_entry &x) { return same_case(x, c); });
+        if (it != g_table.end()) *it = e;
+        else g_table.push_back(e);
+    }
+    return GFP_OK;
+}
+
+int32_t gfp_tune_entries(gfp_tune_entry *out, int32_t cap) {
+    std::lock_guard<std::mutex> g(g_mu);
+    ensure_loaded();
+    const int32_t n = (int32_t)g_table.size();
+    for (int32_t i = 0; out && i < std::min(n, cap); ++i) out[i] = g_table[i];
+    return n;
+}
+
+gfp_status gfp_tune_set(const gfp_tune_entry *entries, int32_t count) {
+    if (count < 0 || (count > 0 && entries == nullptr)) return err(GFP_E_INVAL, "gfp_tune_set: bad arguments");
+    for (int32_t i = 0; i < count; ++i)
+        if (!valid_entry(entries[i])) return err(GFP_E_INVAL, "gfp_tune_set: entry " + std::to_string(i) + " is invalid");
+    std::lock_guard<std::mutex> g(g_mu);
+    g_env_checked = true;
+    g_table.assign(entries, entries + count);
+    return GFP_OK;
+}
+
+gfp_status gfp_tune_save(const char *path) {
+    if (path == nullptr) return err(GFP_E_INVAL, "gfp_tune_save: path is NULL");
+    std::lock_guard<std::mutex> g(g_mu);
+    FILE *f = fopen(path, "w");
+    if (!f) return err(GFP_E_INVAL, std::string("gfp_tune_save: cannot open ") + path);
+    fprintf(f, "# gfp-tune v1: rep dtype kind p n rows strategy acc_bits us_best us_builtin\n");
+    for (const auto &e : g_table)
+        fprintf(f, "%d %d %d %llu %lld %lld %d %d %.4f %.4f\n", e.rep, e.dtype, e.kind, (unsigned long long)e.p,
+                (long long)e.n, (long long)e.rows, e.strategy, e.acc_bits, e.us_best, e.us_builtin);
+    return fclose(f) == 0 ? GFP_OK : GFP_E_INVAL;
+}
+
+gfp_status gfp_tune_load(const char *path) {
+    if (path == nullptr) return err(GFP_E_INVAL, "gfp_tune_load: path is NULL");
+    std::vector<gfp_tune_entry> v;
+    std::string why;
+    gfp_status st = load_file(path, v, why);
+    if (st != GFP_OK) return err(st, "gfp_tune_load: " + why);
+    std::lock_guard<std::mutex> g(g_mu);
+    g_env_checked = true;
+    g_table = v;
+    return GFP_OK;
+}
+
+void gfp_tune_clear(void) {
+    std::lock_guard<std::mutex> g(g_mu);
+    g_env_checked = true;
+    g_table.clear();
+}
+
+}  // extern "C"

@@ -216,3 +216,109 @@ def test_plan_zech_add():
     with pytest.raises(gfp.GfpError) as e:
         P(32749, ZE, 10, strategy=gfp.ZECH_ADD, acc_bits=32)
     assert e.value.status == E_UNSUPPORTED
+
+
+# ------------------------------------------------------------------------------ install-time tuning (F4)
+def _entry(rep, dt, kind, p, n, strategy, acc_bits=0, rows=0):
+    return dict(rep=rep, dtype=dt, kind=kind, p=p, n=n, rows=rows, strategy=strategy, acc_bits=acc_bits,
+                us_best=1.0, us_builtin=2.0)
+
+
+@pytest.fixture
+def clean_table():
+    gfp.tune_clear()
+    yield
+    gfp.tune_clear()
+
+
+def test_tuned_auto_follows_nearest_case(clean_table):
+    """AUTO takes the strategy of the tuned case nearest in (log2 p, log2 n) for the same rep/dtype/kind
+    ("switching thresholds"), only when admissible; otherwise the built-in plan."""
+    P = gfp.plan
+    builtin = P(2 ** 31 - 1, CL, 10 ** 6)["kernel"]
+    assert builtin == "dot_kernel<ClassicalU32<OVERFLOW>>"
+    gfp.tune_set([_entry(CL, U32, 0, 2 ** 31 - 1, 1 << 20, gfp.HYBRID, 64),
+                  _entry(CL, U32, 0, 65537, 1 << 20, gfp.BLOCKED, 64),
+                  _entry(CL, U16, 0, 2897, 1 << 12, gfp.DELAYED, 32)])
+    assert P(2 ** 31 - 1, CL, 10 ** 6)["kernel"] == "ClassicalS<u64acc,u32,HYBRID>"
+    assert P(4294967291, CL, 10 ** 6)["kernel"] == "ClassicalS<u64acc,u32,HYBRID>"  # nearest: 2^31-1
+    assert P(1048573, CL, 10 ** 6)["kernel"] == "ClassicalS<u64acc,u32,BLOCKED>"      # nearest: 65537
+    # DELAYED at m = 32 is admissible only while n (p-1)^2 < 2^32: n = 2 is, n = 10^6 falls back
+    assert P(2897, CL, 2)["kernel"] == "ClassicalS<u32acc,u16,DELAYED>"
+    assert P(2897, CL, 10 ** 6)["kernel"] == "dot_kernel<ClassicalU16<ALL>>"  # the built-in plan
+    # explicit options are never overridden; other reps/kinds are untouched
+    assert P(2 ** 31 - 1, CL, 10 ** 6, strategy=gfp.OVERFLOW, acc_bits=64)["kernel"] == "ClassicalS<u64acc,u32,OVERFLOW>"
+    assert P(2 ** 31 - 1, MO, 10 ** 6)["kernel"] == "dot_kernel<Montgomery<2>>"
+    gfp.tune_clear()
+    assert P(2 ** 31 - 1, CL, 10 ** 6)["kernel"] == builtin
+
+
+def test_tuned_builtin_winner_keeps_builtin(clean_table):
+    gfp.tune_set([_entry(FP, F64, 0, 67108859, 10 ** 7, gfp.AUTO)])
+    assert gfp.plan(67108859, FP, 10 ** 7)["kernel"] == "dot_kernel<Fp64<2>>"
+    gfp.tune_set([_entry(FP, F64, 0, 67108859, 10 ** 7, gfp.DELAYED)])  # inadmissible at n = 10^7
+    assert gfp.plan(67108859, FP, 10 ** 7)["kernel"] == "dot_kernel<Fp64<2>>"
+    gfp.tune_set([_entry(ZE, U16, 0, 32749, 1 << 26, gfp.ZECH_ADD)])
+    assert gfp.plan(32749, ZE, 1 << 26)["kernel"] == "zech_add_dot_kernel"
+
+
+def test_tune_save_load_roundtrip(tmp_path, clean_table):
+    es = [_entry(CL, U32, 1, 2 ** 31 - 1, 512, gfp.HYBRID, 64, rows=1 << 15),
+          _entry(MO, U32, 0, 2 ** 31 - 1, 1 << 24, gfp.OVERFLOW)]
+    gfp.tune_set(es)
+    path = str(tmp_path / "t.txt")
+    gfp.tune_save(path)
+    assert open(path).readline().startswith("# gfp-tune v1")
+    gfp.tune_clear()
+    assert gfp.tune_entries() == []
+    gfp.tune_load(path)
+    got = gfp.tune_entries()
+    assert [(e["rep"], e["kind"], e["p"], e["n"], e["rows"], e["strategy"], e["acc_bits"]) for e in got] == \
+        [(e["rep"], e["kind"], e["p"], e["n"], e["rows"], e["strategy"], e["acc_bits"]) for e in es]
+    bad = tmp_path / "bad.txt"
+    bad.write_text("not a table\n")
+    with pytest.raises(gfp.GfpError) as e:
+        gfp.tune_load(str(bad))
+    assert e.value.status == E_INVAL and "header" in str(e.value)
+    bad.write_text("# gfp-tune v1\n0 1 0 7 5\n")
+    with pytest.raises(gfp.GfpError):
+        gfp.tune_load(str(bad))
+    assert len(gfp.tune_entries()) == 2  # a failed load leaves the table as it was
+
+
+def test_tune_set_rejects_invalid(clean_table):
+    for e in [_entry(9, U32, 0, 7, 5, 0), _entry(CL, U32, 2, 7, 5, 0), _entry(CL, U32, 0, 7, 5, 9),
+              _entry(ZE, U16, 1, 32749, 512, gfp.ZECH_ADD), _entry(CL, U32, 0, 1, 5, 0)]:
+        with pytest.raises(gfp.GfpError) as err:
+            gfp.tune_set([e])
+        assert err.value.status == E_INVAL
+    assert gfp.tune_entries() == []
+
+
+def test_tune_file_from_environment(tmp_path):
+    """GFP_TUNE_FILE is loaded on the first AUTO call of a process."""
+    import subprocess
+    import sys
+    path = tmp_path / "env.txt"
+    path.write_text("# gfp-tune v1\n0 1 0 2147483647 1048576 0 4 64 1.0 2.0\n")
+    code = ("import paper_cs_0404008_b200 as g; "
+            "print(g.plan(2147483647, 0, 10**6)['kernel']); print(len(g.tune_entries()))")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True,
+                         env=dict(os.environ, GFP_TUNE_FILE=str(path)), check=True).stdout.split()
+    assert out == ["ClassicalS<u64acc,u32,HYBRID>", "1"]
+
+
+def test_shipped_install_time_table_loads_by_default():
+    """Without GFP_TUNE_FILE the library loads gfp_tune.txt next to libgfp.so (the table measured on a
+    B200 by `python -m paper_cs_0404008_b200.autotune`); AUTO then follows it."""
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k != "GFP_TUNE_FILE"}
+    code = ("import paper_cs_0404008_b200 as g; es = g.tune_entries(); "
+            "print(len(es), all(e['us_best'] <= e['us_builtin'] for e in es)); "
+            "print(g.plan(2147483647, 0, 65536, dtype=__import__('torch').uint32)['kernel'])")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, env=env,
+                         check=True).stdout.split("\n")
+    n, ok = out[0].split()
+    assert int(n) >= 100 and ok == "True"
+    assert out[1] == "ClassicalS<u64acc,u32,HYBRID>"

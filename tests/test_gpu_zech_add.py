@@ -115,3 +115,16 @@ def test_zech_add_graph_capture_and_repeat():
         g.replay()
         torch.cuda.synchronize()
         assert int(out.cpu().to(torch.int64)[0]) == want
+
+
+def test_table_sizes_in_any_order():
+    """Shared-memory opt-in regression: the same kernel launched with a large table, then smaller ones,
+    then the large one again (Zech at several primes, both accumulations) must keep launching."""
+    n = 100_003
+    for p in [65521, 32771, 40009, 65521, 32749, 65521]:
+        g = oracle.primitive_root(p)
+        a = synth.zech_codes(SEED, 0, 0, n, p - 1)
+        b = synth.zech_codes(SEED, 1, 0, n, p - 1)
+        want = oracle.dot_zech(p, g, a, b)
+        assert zadd(cu(a), cu(b), p) == want, p
+        assert int(gfp.dot(cu(a), cu(b), p, ZE).cpu().to(torch.int64)[0]) == want, p
