@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
-CLASSICAL, MONTGOMERY, FP64, ZECH = 0, 1, 2, 3
+CLASSICAL, MONTGOMERY, FP64, ZECH, CENTERED = 0, 1, 2, 3, 4
 _DT = {np.dtype(np.uint16): 0, np.dtype(np.uint32): 1, np.dtype(np.uint64): 2}
 
 
@@ -50,6 +50,10 @@ def _load():
             "oracle_zech_encode_one": (u64, [u64, u64, u64]),
             "oracle_dot_zech": (u64, [u64, u64, vp, vp, i64, vp, ctypes.POINTER(i64)]),
             "oracle_zech_tplus1": (None, [u64, u64, vp, vp]),
+            "oracle_from_centered": (u64, [u64, i64]),
+            "oracle_to_centered": (i64, [u64, u64]),
+            "oracle_dot_centered": (i64, [u64, vp, vp, ci, i64, ctypes.POINTER(i64)]),
+            "oracle_dot_centered_f64": (ctypes.c_double, [u64, vp, vp, i64, ctypes.POINTER(i64)]),
             "oracle_zech_mul": (u64, [u64, u64, u64]),
             "oracle_zech_add": (u64, [u64, vp, u64, u64]),
             "oracle_dot_zech_tplus1": (u64, [u64, u64, vp, vp, i64, vp, vp, ctypes.POINTER(i64)]),
@@ -186,6 +190,35 @@ def dot_zech_tplus1(p: int, g: int, a: np.ndarray, b: np.ndarray) -> int:
     return r
 
 
+def to_centered(p: int, r: int) -> int:
+    """residue in [0, p) -> centered value in [-(p-1)/2, (p-1)/2] (sec. 3.2.2)."""
+    return int(_load().oracle_to_centered(p, r))
+
+
+def from_centered(p: int, c: int) -> int:
+    return int(_load().oracle_from_centered(p, c))
+
+
+_SDT = {np.dtype(np.int16): 0, np.dtype(np.int32): 1, np.dtype(np.int64): 2}
+
+
+def dot_centered(p: int, a: np.ndarray, b: np.ndarray):
+    """Dot of centered vectors (int16 / int32 / int64 / float64 storage); the result is centered, of
+    the same kind (an int, or a float for binary64 storage)."""
+    a, b = _c(a), _c(b)
+    if a.shape != b.shape or a.dtype != b.dtype:
+        raise ValueError("length or dtype mismatch")
+    bad = ctypes.c_int64(-1)
+    if a.dtype == np.float64:
+        r = float(_load().oracle_dot_centered_f64(p, a.ctypes.data, b.ctypes.data, a.size, ctypes.byref(bad)))
+    else:
+        r = int(_load().oracle_dot_centered(p, a.ctypes.data, b.ctypes.data, _SDT[a.dtype], a.size,
+                                            ctypes.byref(bad)))
+    if bad.value >= 0:
+        raise ValueError(f"element {bad.value} is not a centered element for p={p}")
+    return r
+
+
 def dot(p: int, rep: int, a: np.ndarray, b: np.ndarray, g: int | None = None):
     """Dot product in representation `rep`; the result stays in that representation (reading G10)."""
     if rep == CLASSICAL:
@@ -196,6 +229,8 @@ def dot(p: int, rep: int, a: np.ndarray, b: np.ndarray, g: int | None = None):
         return dot_fp64(p, a, b)
     if rep == ZECH:
         return dot_zech(p, primitive_root(p) if g is None else g, a, b)
+    if rep == CENTERED:
+        return dot_centered(p, a, b)
     raise ValueError(f"unknown representation {rep}")
 
 

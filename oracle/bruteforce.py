@@ -57,3 +57,13 @@ def to_mont(p, a):
 
 def from_mont(p, x):
     return x * pow(MONT_B, -1, p) % p
+
+
+def to_centered(p, r):
+    """sec. 3.2.2: residues above (p-1)/2 are stored as r - p."""
+    r %= p
+    return r - p if r > (p - 1) // 2 else r
+
+
+def from_centered(p, c):
+    return c % p

@@ -319,3 +319,67 @@ uint64_t oracle_dot_zech_tplus1(uint64_t p, uint64_t g, const uint16_t *a, const
     }
     return acc;
 }
+
+/* ------------------------------------- centered representation (sec 3.2.2) */
+/* Elements stored between -(p-1)/2 and (p-1)/2, p odd; storage
+ * int16, int32 (two's complement) or binary64 holding the integer.  The dot is
+ * the same field element; the result is returned centered (reading G10). */
+
+static int64_t load_signed(const void *v, int dt, int64_t i)
+{
+    switch (dt) {
+    case O_U16: return ((const int16_t *)v)[i];
+    case O_U32: return ((const int32_t *)v)[i];
+    default:    return ((const int64_t *)v)[i];
+    }
+}
+
+/* centered value c -> residue in [0, p) */
+uint64_t oracle_from_centered(uint64_t p, int64_t c)
+{
+    int64_t r = c % (int64_t)p; /* C99: sign of the dividend */
+    return (uint64_t)(r < 0 ? r + (int64_t)p : r);
+}
+
+/* residue r in [0, p) -> centered value in [-(p-1)/2, (p-1)/2] */
+int64_t oracle_to_centered(uint64_t p, uint64_t r)
+{
+    r %= p;
+    return r > (p - 1) / 2 ? (int64_t)r - (int64_t)p : (int64_t)r;
+}
+
+/* Dot of centered vectors; dt: 0 = int16, 1 = int32, 2 = int64.  *bad = first
+ * element outside [-(p-1)/2, (p-1)/2], or -1.  One 128-bit remainder per term. */
+int64_t oracle_dot_centered(uint64_t p, const void *a, const void *b, int dt, int64_t n, int64_t *bad)
+{
+    const int64_t h = (int64_t)((p - 1) / 2);
+    uint64_t acc = 0;
+    *bad = -1;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t x = load_signed(a, dt, i), y = load_signed(b, dt, i);
+        if (x < -h || x > h || y < -h || y > h) {
+            *bad = i;
+            return 0;
+        }
+        acc = (uint64_t)(((u128)acc + (u128)oracle_from_centered(p, x) * oracle_from_centered(p, y)) % p);
+    }
+    return oracle_to_centered(p, acc);
+}
+
+/* binary64 storage: check each value is an integer in the centered range, then as above. */
+double oracle_dot_centered_f64(uint64_t p, const double *a, const double *b, int64_t n, int64_t *bad)
+{
+    const double h = (double)((p - 1) / 2);
+    uint64_t acc = 0;
+    *bad = -1;
+    for (int64_t i = 0; i < n; ++i) {
+        double x = a[i], y = b[i];
+        if (!(x >= -h && x <= h && y >= -h && y <= h) || x != (double)(int64_t)x || y != (double)(int64_t)y) {
+            *bad = i;
+            return 0.0;
+        }
+        acc = (uint64_t)(((u128)acc + (u128)oracle_from_centered(p, (int64_t)x) *
+                                          oracle_from_centered(p, (int64_t)y)) % p);
+    }
+    return (double)oracle_to_centered(p, acc) + 0.0; /* + 0.0: never -0.0 */
+}

@@ -385,3 +385,60 @@ def test_dot_zech_tplus1_unique_result(p):
     assert oracle.dot_zech_tplus1(p, g, ones, ones) == 0
     with pytest.raises(ValueError):
         oracle.dot_zech_tplus1(p, g, np.array([p], np.uint32), np.array([1], np.uint32))
+
+
+# ------------------------------------------------------------------ centered representation (F2)
+@pytest.mark.parametrize("p", [3, 5, 7, 11, 101, 1009])
+def test_centered_encoding_exhaustive(p):
+    """sec. 3.2.2: the encoding is a bijection between [0, p) and [-(p-1)/2, (p-1)/2] that
+    commutes with reduction mod p; the SPEC examples 0 -> 0, p-1 -> -1, (p-1)/2 fixed."""
+    h = (p - 1) // 2
+    seen = set()
+    for r in range(p):
+        c = oracle.to_centered(p, r)
+        assert -h <= c <= h and c % p == r and c == bf.to_centered(p, r)
+        assert oracle.from_centered(p, c) == r
+        seen.add(c)
+    assert seen == set(range(-h, h + 1))
+    assert oracle.to_centered(p, 0) == 0 and oracle.to_centered(p, p - 1) == -1 and oracle.to_centered(p, h) == h
+
+
+@pytest.mark.parametrize("p", [3, 7, 101, 32749, 46337, 65521, 2 ** 31 - 1, 4294967291])
+def test_dot_centered_bruteforce(p):
+    rng = random.Random(p + 11)
+    h = (p - 1) // 2
+    dts = ([np.int16] if p <= 65535 else []) + ([np.int32] if p <= 2 ** 32 else []) + [np.int64]
+    for dt in dts:
+        for n in [0, 1, 2, 3, 64, 513]:
+            a = [rng.randint(-h, h) for _ in range(n)]
+            b = [rng.randint(-h, h) for _ in range(n)]
+            r = oracle.dot_centered(p, np.array(a, dt), np.array(b, dt))
+            assert r == bf.to_centered(p, bf.dot(p, a, b)) and -h <= r <= h
+            # the same field element as the classical dot of the decoded residues
+            ra = np.array([x % p for x in a], np.uint64)
+            rb = np.array([x % p for x in b], np.uint64)
+            assert r % p == oracle.dot_classical(p, ra, rb)
+    if p < 2 ** 53:
+        a = [float(rng.randint(-h, h)) for _ in range(300)]
+        b = [float(rng.randint(-h, h)) for _ in range(300)]
+        r = oracle.dot_centered(p, np.array(a), np.array(b))
+        assert r == float(bf.to_centered(p, bf.dot(p, [int(x) for x in a], [int(x) for x in b])))
+        assert math.copysign(1.0, oracle.dot_centered(p, np.array([0.0]), np.array([-1.0]))) == 1.0
+
+
+@pytest.mark.parametrize("p", [101, 65521, 67108859])
+def test_dot_centered_invariants(p):
+    """negation symmetry dot(-a, b) = -dot(a, b) (the centered range is symmetric), all -1 of length n
+    gives n mod p centered, and out-of-range entries are rejected."""
+    rng = random.Random(p)
+    h = (p - 1) // 2
+    a = np.array([rng.randint(-h, h) for _ in range(1000)], np.int64)
+    b = np.array([rng.randint(-h, h) for _ in range(1000)], np.int64)
+    r = oracle.dot_centered(p, a, b)
+    assert oracle.dot_centered(p, -a, b) == (-r if abs(r) != 0 else 0)
+    m = np.full(5000, -1, np.int64)
+    assert oracle.dot_centered(p, m, m) == bf.to_centered(p, 5000)
+    with pytest.raises(ValueError):
+        oracle.dot_centered(p, np.array([h + 1], np.int64), np.array([1], np.int64))
+    with pytest.raises(ValueError):
+        oracle.dot_centered(p, np.array([0.5]), np.array([1.0]))
