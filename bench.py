@@ -51,8 +51,12 @@ CONFIGS = {
     # integer accumulator (gfp_dot_ex, GFP_STRAT_ZECH_ADD = 5)
     5: dict(name="C4-zech_add", workload="configs[3] with pure-Zech t_plus1 accumulation (sec. 2.4 Table 1)",
             p=32749, rep=3, dtype=np.uint16, n=1 << 26, bpt=4, kind="dot", strategy=5, inputs_of=3),
+    # configs[1] in the centered representation (sec. 3.2.2): binary64 in [-(p-1)/2, (p-1)/2],
+    # blocks of k = 8 instead of 2; converted on device from the same residues (conversion timed apart)
+    6: dict(name="C2-centered", workload="configs[1] in the centered representation (sec. 3.2.2), binary64, k=8",
+            p=67108859, rep=4, dtype=np.float64, n=10 ** 7, bpt=16, kind="dot", inputs_of=1, host_dtype=np.uint32),
 }
-REP_NAMES = {0: "classical", 1: "montgomery", 2: "fp64", 3: "zech"}
+REP_NAMES = {0: "classical", 1: "montgomery", 2: "fp64", 3: "zech", 4: "centered"}
 DTYPE_NAMES = {np.dtype(np.uint16): "u16", np.dtype(np.uint32): "u32", np.dtype(np.float64): "f64"}
 L2_BYTES = 126 * 10 ** 6
 
@@ -159,8 +163,9 @@ def host_inputs(cfg, rank, world, limit=None):
         a = synth.zech_codes(seed, synth.STREAM_A, s0, s1 - s0, p - 1)
         b = synth.zech_codes(seed, synth.STREAM_B, s0, s1 - s0, p - 1)
     else:
-        a = synth.uniform(seed, synth.STREAM_A, s0, s1 - s0, p, cfg["dtype"])
-        b = synth.uniform(seed, synth.STREAM_B, s0, s1 - s0, p, cfg["dtype"])
+        hdt = cfg.get("host_dtype", cfg["dtype"])  # residues; converted on device when they differ
+        a = synth.uniform(seed, synth.STREAM_A, s0, s1 - s0, p, hdt)
+        b = synth.uniform(seed, synth.STREAM_B, s0, s1 - s0, p, hdt)
     return {"a": a, "b": b}
 
 
@@ -175,8 +180,11 @@ def to_device(gfp, cfg, h, dev, stream):
     a = torch.from_numpy(h["a"]).to(dev)
     b = torch.from_numpy(h["b"]).to(dev)
     torch.cuda.synchronize()  # copies ran on the default stream; the kernels run on `stream`
-    if rep == 1:
-        am, bm = torch.empty_like(a), torch.empty_like(b)
+    if rep in (1, 4):  # Montgomery a -> aB mod p / centered r -> r or r - p, on device
+        tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.uint32): torch.uint32,
+               np.dtype(np.uint16): torch.uint16}[np.dtype(cfg["dtype"])] if rep == 1 else torch.float64
+        am = torch.empty(a.numel(), dtype=tdt, device=a.device)
+        bm = torch.empty(b.numel(), dtype=tdt, device=b.device)
         with torch.cuda.stream(stream):
             for _ in range(2):  # warm
                 gfp.to_rep(a, p, rep, out=am, stream=stream)
@@ -189,10 +197,15 @@ def to_device(gfp, cfg, h, dev, stream):
             e1.record(stream)
         stream.synchronize()
         ms = e0.elapsed_time(e1) / iters
-        nbytes = 2 * a.numel() * 4 * 2  # read 4 + write 4 bytes per element per operand
-        phases["to_montgomery"] = {"ms_per_pair": ms, "GB/s": nbytes / ms / 1e6,
-                                   "note": "a -> aB mod p for both operands (P:83-84); excluded from the dot "
-                                           "timing as in the paper (P:313-320)"}
+        nbytes = 2 * a.numel() * (a.element_size() + am.element_size())  # read + write per element per operand
+        if rep == 1:
+            phases["to_montgomery"] = {"ms_per_pair": ms, "GB/s": nbytes / ms / 1e6,
+                                       "note": "a -> aB mod p for both operands (P:83-84); excluded from the dot "
+                                               "timing as in the paper (P:313-320)"}
+        else:
+            phases["to_centered"] = {"ms_per_pair": ms, "GB/s": nbytes / ms / 1e6,
+                                     "note": "u32 residues -> centered binary64 for both operands (P:394-398); "
+                                             "excluded from the dot timing (P:313-320)"}
         del a, b
         return {"a": am, "b": bm}, phases
     return {"a": a, "b": b}, phases
@@ -320,6 +333,8 @@ def oracle_time(cfg, h, budget_s=10.0, full_ok=True):
             return oracle.dot_montgomery(p, a[:m], b[:m])
         if rep == 2:
             return oracle.dot_fp64(p, a[:m], b[:m])
+        if rep == 4:
+            return oracle.dot_centered(p, a[:m], b[:m])
         return oracle.dot_zech(p, 2, a[:m], b[:m])
     m0 = min(len(a), 1 << 18)
     t0 = time.perf_counter()
@@ -407,7 +422,7 @@ def main():
     cpu = None
     if rank == 0 and not args.no_cpu:
         hh = dict(h)
-        if cfg["rep"] == 1:  # the oracle reads the Montgomery-form vectors the GPU dotted
+        if cfg["rep"] in (1, 4):  # the oracle reads the converted vectors the GPU dotted
             hh = {"a": d["a"].cpu().numpy(), "b": d["b"].cpu().numpy()}
         tps, sample, ores, m = oracle_time(cfg, hh, args.oracle_budget)
         cpu = {"value": tps, "unit": "terms/s", "cores": 1, "kind": "oracle", "sample": sample,
@@ -421,7 +436,7 @@ def main():
                 r = gfp.dot_ex(d["a"][:m], d["b"][:m], cfg["p"], cfg["rep"], strategy=cfg["strategy"])
             else:
                 r = gfp.dot(d["a"][:m], d["b"][:m], cfg["p"], cfg["rep"])
-            got = r.cpu()[0].item() if cfg["rep"] == 2 else int(r.cpu().to(torch.int64)[0])
+            got = r.cpu()[0].item() if r.dtype == torch.float64 else int(r.cpu().to(torch.int64)[0])
             parity = got == ores
         cpu["parity_checked_terms"] = int(m) if cfg["kind"] == "dot" else int(m) * cfg["n"]
 

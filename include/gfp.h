@@ -31,6 +31,11 @@
  *                      (sec. 2.4), g = smallest primitive root
  *       GFP_U16: p <= 65521 (the antilog table must fit shared memory; the
  *                paper's index bound 1073741789, is looser)
+ *   GFP_REP_CENTERED   residues stored between -(p-1)/2 and (p-1)/2, signed (sec. 3.2.2);
+ *                      blocks of lambda_c products with lambda_c ((p-1)/2)^2 + (p-1)/2 < 2^(m-1)
+ *                      (int64 accumulators) or < 2^53 (binary64)
+ *       GFP_U16 storage holds int16: odd p <= 65521     GFP_U32 storage holds int32: odd p <= 4294967291
+ *       GFP_F64: exact integers, odd p <= 189812507 (largest prime with h(h+1) < 2^53, h = (p-1)/2)
  *   p must be prime (GFP_E_NOT_PRIME) and within the bound (GFP_E_BOUND);
  *   any other (rep, dtype) pair is GFP_E_UNSUPPORTED.
  *
@@ -79,7 +84,8 @@ typedef enum {
     GFP_REP_CLASSICAL = 0,
     GFP_REP_MONTGOMERY = 1,
     GFP_REP_FP64 = 2,
-    GFP_REP_ZECH = 3
+    GFP_REP_ZECH = 3,
+    GFP_REP_CENTERED = 4
 } gfp_rep;
 
 typedef enum { GFP_U16 = 0, GFP_U32 = 1, GFP_F64 = 2 } gfp_dtype;
@@ -109,7 +115,9 @@ typedef enum {
  * 32 or 64 for classical storage (m = 32 needs p(p-1) < 2^32, i.e. p <= 65521).  Admissible
  * combinations: classical x {AUTO..HYBRID} x {32, 64}; Montgomery x {AUTO, BLOCKED (REDC every
  * k_R products, sec. 3.2.1), OVERFLOW (overflow-Montgomery, sec. 3.3)}; fp64 x {AUTO,
- * DELAYED, BLOCKED}; Zech x {AUTO, ZECH_ADD}.  Anything else: GFP_E_UNSUPPORTED; a strategy whose bound the
+ * DELAYED, BLOCKED}; Zech x {AUTO, ZECH_ADD}; centered x {AUTO, DELAYED, BLOCKED} (the signed overflow trick,
+ * P:441-457, and hybrid centered, are not offered: the paper finds the first too costly and
+ * shows the second cannot work).  Anything else: GFP_E_UNSUPPORTED; a strategy whose bound the
  * (p, n) pair violates: GFP_E_BOUND. */
 typedef struct {
     int32_t strategy;  /* gfp_strategy */
@@ -135,7 +143,9 @@ typedef struct {
     int32_t acc_bits;      /* m of Eq. (1): 64 (integer accumulators) or 53 (binary64) */
     int32_t mont_kr;       /* Montgomery: products per REDC allowed by the two G6 bounds, capped at 10^6; else 0 */
     uint64_t k;            /* Eq. (1) with a carried residue (reading G7):
-                              largest k with k(p-1)^2 + (p-1) <= 2^m - 1 (binary64: < 2^53) */
+                              largest k with k(p-1)^2 + (p-1) <= 2^m - 1 (binary64: < 2^53);
+                              centered: largest k with k h^2 + h <= 2^63 - 1 (binary64: < 2^53),
+                              h = (p-1)/2 */
     uint64_t corr;         /* CORR = 2^64 mod p (sec. 3.3) */
     uint32_t n_im;         /* Montgomery: -p^{-1} mod 2^32; else 0 */
     uint32_t pad0;

@@ -18,19 +18,19 @@ import os
 import torch
 
 __all__ = [
-    "CLASSICAL", "MONTGOMERY", "FP64", "ZECH", "AUTO", "DELAYED", "BLOCKED", "OVERFLOW", "HYBRID", "ZECH_ADD",
+    "CLASSICAL", "MONTGOMERY", "FP64", "ZECH", "CENTERED", "AUTO", "DELAYED", "BLOCKED", "OVERFLOW", "HYBRID", "ZECH_ADD",
     "GfpError", "lib", "query", "plan", "dot", "dot_ex", "dot_batch", "dot_batch_ex",
     "dot_partial", "finalize", "to_rep", "from_rep", "dot_host", "launch_count", "release_caches",
     "rep_dtype", "tune", "tune_entries", "tune_set", "tune_save", "tune_load", "tune_clear",
 ]
 
-CLASSICAL, MONTGOMERY, FP64, ZECH = 0, 1, 2, 3
+CLASSICAL, MONTGOMERY, FP64, ZECH, CENTERED = 0, 1, 2, 3, 4
 U16, U32, F64 = 0, 1, 2
 AUTO, DELAYED, BLOCKED, OVERFLOW, HYBRID = 0, 1, 2, 3, 4  # gfp_strategy (paper sec. 3)
 ZECH_ADD = 5  # pure discrete-log accumulation through t_plus1 (sec. 2.4 Table 1), Zech only
 _STRAT_NAMES = {AUTO: "auto", DELAYED: "delayed", BLOCKED: "blocked", OVERFLOW: "overflow", HYBRID: "hybrid",
                 ZECH_ADD: "zech_add"}
-_REP_NAMES = {CLASSICAL: "classical", MONTGOMERY: "montgomery", FP64: "fp64", ZECH: "zech"}
+_REP_NAMES = {CLASSICAL: "classical", MONTGOMERY: "montgomery", FP64: "fp64", ZECH: "zech", CENTERED: "centered"}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.environ.get("GFP_LIBRARY") or os.path.join(_HERE, "libgfp.so")  # override: A/B builds
@@ -119,7 +119,8 @@ def _check(status: int) -> None:
         raise GfpError(status)
 
 
-_TORCH_DT = {torch.uint16: U16, torch.uint32: U32, torch.float64: F64}
+# storage widths of gfp_dtype; the centered representation stores signed int16 / int32 in the same widths
+_TORCH_DT = {torch.uint16: U16, torch.uint32: U32, torch.float64: F64, torch.int16: U16, torch.int32: U32}
 _DT_TORCH = {U16: torch.uint16, U32: torch.uint32, F64: torch.float64}
 
 
@@ -131,14 +132,23 @@ def rep_dtype(rep: int, p: int) -> torch.dtype:
         return torch.uint32
     if rep == ZECH:
         return torch.uint16
+    if rep == CENTERED:
+        return torch.int16 if p <= 65521 else torch.int32
     return torch.uint16 if p <= 65521 else torch.uint32
 
 
-def _dt(t: torch.Tensor) -> int:
+def _dt(t: torch.Tensor, rep: int | None = None) -> int:
+    """gfp_dtype of a tensor; with `rep`, the signedness must match the representation (signed int16 /
+    int32 only for the centered representation, unsigned only for the others)."""
     try:
-        return _TORCH_DT[t.dtype]
+        d = _TORCH_DT[t.dtype]
     except KeyError:
-        raise TypeError(f"unsupported dtype {t.dtype}; use uint16, uint32 or float64") from None
+        raise TypeError(f"unsupported dtype {t.dtype}; use uint16, uint32, int16, int32 or float64") from None
+    if rep is not None and t.dtype in (torch.int16, torch.int32, torch.uint16, torch.uint32):
+        signed = t.dtype in (torch.int16, torch.int32)
+        if signed != (rep == CENTERED):
+            raise TypeError(f"{t.dtype} storage does not match representation {_REP_NAMES.get(rep, rep)}")
+    return d
 
 
 def _stream(t: torch.Tensor | None, stream) -> int:
@@ -174,7 +184,7 @@ def dot(a: torch.Tensor, b: torch.Tensor, p: int, rep: int = CLASSICAL, out: tor
     if out is None:
         out = torch.empty(1, dtype=a.dtype, device=a.device)
     with torch.cuda.device(a.device):
-        _check(lib.gfp_dot(p, rep, _dt(a), a.data_ptr(), b.data_ptr(), a.numel(), out.data_ptr(), _stream(a, stream)))
+        _check(lib.gfp_dot(p, rep, _dt(a, rep), a.data_ptr(), b.data_ptr(), a.numel(), out.data_ptr(), _stream(a, stream)))
     return out
 
 
@@ -203,7 +213,7 @@ def dot_ex(a: torch.Tensor, b: torch.Tensor, p: int, rep: int = CLASSICAL, strat
     if out is None:
         out = torch.empty(1, dtype=a.dtype, device=a.device)
     with torch.cuda.device(a.device):
-        _check(lib.gfp_dot_ex(p, rep, _dt(a), a.data_ptr(), b.data_ptr(), a.numel(), _opts(strategy, acc_bits),
+        _check(lib.gfp_dot_ex(p, rep, _dt(a, rep), a.data_ptr(), b.data_ptr(), a.numel(), _opts(strategy, acc_bits),
                               out.data_ptr(), _stream(a, stream)))
     return out
 
@@ -217,7 +227,7 @@ def dot_partial(a: torch.Tensor, b: torch.Tensor, p: int, rep: int = CLASSICAL, 
     if out is None:
         out = torch.empty(1, dtype=torch.int64, device=a.device)
     with torch.cuda.device(a.device):
-        _check(lib.gfp_dot_partial(p, rep, _dt(a), a.data_ptr(), b.data_ptr(), a.numel(), out.data_ptr(),
+        _check(lib.gfp_dot_partial(p, rep, _dt(a, rep), a.data_ptr(), b.data_ptr(), a.numel(), out.data_ptr(),
                                    _stream(a, stream)))
     return out
 
@@ -256,7 +266,7 @@ def dot_batch(A: torch.Tensor, x: torch.Tensor, p: int, rep: int = CLASSICAL, ou
     if out is None:
         out = torch.empty(rows, dtype=A.dtype, device=A.device)
     with torch.cuda.device(A.device):
-        _check(lib.gfp_dot_batch(p, rep, _dt(A), A.data_ptr(), lda, x.data_ptr(), rows, n, out.data_ptr(),
+        _check(lib.gfp_dot_batch(p, rep, _dt(A, rep), A.data_ptr(), lda, x.data_ptr(), rows, n, out.data_ptr(),
                                  _stream(A, stream)))
     return out
 
@@ -277,7 +287,7 @@ def dot_batch_ex(A: torch.Tensor, x: torch.Tensor, p: int, rep: int = CLASSICAL,
     if out is None:
         out = torch.empty(rows, dtype=A.dtype, device=A.device)
     with torch.cuda.device(A.device):
-        _check(lib.gfp_dot_batch_ex(p, rep, _dt(A), A.data_ptr(), lda, x.data_ptr(), rows, n,
+        _check(lib.gfp_dot_batch_ex(p, rep, _dt(A, rep), A.data_ptr(), lda, x.data_ptr(), rows, n,
                                     _opts(strategy, acc_bits), out.data_ptr(), _stream(A, stream)))
     return out
 
@@ -288,7 +298,8 @@ def to_rep(x: torch.Tensor, p: int, rep: int, out: torch.Tensor | None = None, s
     if out is None:
         out = torch.empty(x.numel(), dtype=rep_dtype(rep, p), device=x.device)
     with torch.cuda.device(x.device):
-        _check(lib.gfp_to_rep(p, rep, _dt(x), x.data_ptr(), _dt(out), out.data_ptr(), x.numel(), _stream(x, stream)))
+        _check(lib.gfp_to_rep(p, rep, _dt(x, CLASSICAL), x.data_ptr(), _dt(out, rep), out.data_ptr(), x.numel(),
+                              _stream(x, stream)))
     return out
 
 
@@ -299,7 +310,7 @@ def from_rep(x: torch.Tensor, p: int, rep: int, out: torch.Tensor | None = None,
     if out is None:
         out = torch.empty(x.numel(), dtype=dtype or torch.uint32, device=x.device)
     with torch.cuda.device(x.device):
-        _check(lib.gfp_from_rep(p, rep, _dt(x), x.data_ptr(), _dt(out), out.data_ptr(), x.numel(),
+        _check(lib.gfp_from_rep(p, rep, _dt(x, rep), x.data_ptr(), _dt(out, CLASSICAL), out.data_ptr(), x.numel(),
                                 _stream(x, stream)))
     return out
 
@@ -315,7 +326,7 @@ def dot_host(a: torch.Tensor, b: torch.Tensor, p: int, rep: int = CLASSICAL, str
         raise ValueError("a and b must have the same length and dtype")
     res = torch.empty(1, dtype=a.dtype)
     s = _stream(None, stream) if stream is not None else torch.cuda.current_stream().cuda_stream
-    _check(lib.gfp_dot_host(p, rep, _dt(a), a.data_ptr(), b.data_ptr(), a.numel(), res.data_ptr(), s))
+    _check(lib.gfp_dot_host(p, rep, _dt(a, rep), a.data_ptr(), b.data_ptr(), a.numel(), res.data_ptr(), s))
     return res.item() if a.dtype == torch.float64 else int(res.to(torch.int64).item())
 
 

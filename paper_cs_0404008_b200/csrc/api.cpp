@@ -97,6 +97,9 @@ gfp_status get_ctx(uint64_t p, gfp_rep rep, gfp_dtype dt, Ctx **out) {
     K.qbar = (uint32_t)c->info.qbar;
     K.corr32 = (uint32_t)((((u128)1) << 32) % p);
     K.mu32 = (uint32_t)(0xFFFFFFFFull / p);
+    K.half = (int64_t)((p - 1) / 2);
+    K.hd = (double)K.half;
+    K.c63 = (uint64_t)((((u128)1) << 63) % p);
     if (rep == GFP_REP_ZECH) {
         std::vector<uint16_t> logt, anti, delta;
         zech_tables(p, c->info.g, logt, anti);
@@ -170,7 +173,7 @@ bool aligned(const void *p, size_t a) { return ((uintptr_t)p % a) == 0; }
 
 gfp_status check_dot_args(gfp_dtype dt, const void *a, const void *b, int64_t n, const void *out, size_t out_align) {
     if ((int)dt < 0 || (int)dt > 2) return fail(GFP_E_INVAL, "unknown dtype");
-    if (n < 0) return fail(GFP_E_INVAL, "n < 0");
+    if (n < 0) return fail(GFP_E_INVAL, "n < 0");  // (centered storage reuses the widths: int16 / int32 / f64)
     if (out == nullptr) return fail(GFP_E_INVAL, "out is NULL");
     if (n > 0 && (a == nullptr || b == nullptr)) return fail(GFP_E_INVAL, "NULL operand with n > 0");
     const size_t es = dtype_size(dt);

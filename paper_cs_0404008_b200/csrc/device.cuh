@@ -263,6 +263,147 @@ struct Zech {
 };
 
 
+// Centered representation (sec. 3.2.2): residues stored between -h and h, h = (p-1)/2, as
+// int16 / int32 / binary64; products |ab| <= h^2 summed in a signed accumulator, blocks of lambda_c
+// products with lambda_c h^2 + h < 2^(m-1) (the doubled block of P:396-398).
+// signed 64-bit T -> residue in [0, p): T + 2^63 is a nonnegative u64, from which 2^63 mod p is removed
+__device__ __forceinline__ uint64_t smod_p(int64_t T, const KParams &K) {
+    const uint64_t r = mod_p((uint64_t)T ^ 0x8000000000000000ull, K.p, K.mu);
+    return r >= K.c63 ? r - K.c63 : r + K.p - K.c63;
+}
+__device__ __forceinline__ int64_t centered_of(int64_t T, const KParams &K) {
+    const uint64_t r = smod_p(T, K);
+    return r > (uint64_t)K.half ? (int64_t)r - (int64_t)K.p : (int64_t)r;
+}
+
+enum CenteredMode { CE_ALL = 0, CE_THREAD = 1, CE_BLOCKED = 2 };
+
+// int16 / int32 storage, int64 accumulator.  CE_ALL: the host proved n h^2 < 2^63, the raw signed sum is
+// returned (two's-complement sums across threads are exact); CE_THREAD: each thread reduces once at the
+// end; CE_BLOCKED: reduce to the centered residue every K.kblk = lambda_c products.
+template <typename E, int MODE>
+struct CenteredI {
+    using elem = E;
+    static constexpr int W = 16 / sizeof(E);
+    static constexpr bool kTable = false;
+    struct Acc {
+        int64_t s;
+        uint32_t cnt;
+    };
+    __device__ __forceinline__ static void init(Acc &A) {
+        A.s = 0;
+        A.cnt = 0;
+    }
+    __device__ __forceinline__ static void term(Acc &A, int32_t x, int32_t y, const KParams &K,
+                                                const uint16_t * = nullptr) {
+        if (MODE == CE_BLOCKED) {
+            if (A.cnt >= K.kblk) {
+                A.s = centered_of(A.s, K);
+                A.cnt = 0;
+            }
+            ++A.cnt;
+        }
+        A.s += (int64_t)x * y;
+    }
+    __device__ __forceinline__ static void raw(Acc &A, uint4 x, uint4 y) {
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if constexpr (sizeof(E) == 2) {  // two int16 lanes: |lo lo' + hi hi'| <= 2 h^2 < 2^31
+                const int32_t xl = (int32_t)(xs[i] << 16) >> 16, xh = (int32_t)xs[i] >> 16;
+                const int32_t yl = (int32_t)(ys[i] << 16) >> 16, yh = (int32_t)ys[i] >> 16;
+                A.s += (int64_t)(xl * yl + xh * yh);
+            } else {
+                A.s += (int64_t)(int32_t)xs[i] * (int32_t)ys[i];
+            }
+        }
+    }
+    __device__ __forceinline__ static void vec(Acc &A, uint4 x, uint4 y, const KParams &K, const uint16_t *) {
+        if (MODE == CE_BLOCKED) {
+            if (K.kblk >= (uint64_t)W) {  // bookkeeping once per vector: close the block before it overflows
+                if (A.cnt + W > K.kblk) {
+                    A.s = centered_of(A.s, K);
+                    A.cnt = 0;
+                }
+                raw(A, x, y);
+                A.cnt += W;
+            } else {
+                const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if constexpr (sizeof(E) == 2) {
+                        term(A, (int32_t)(xs[i] << 16) >> 16, (int32_t)(ys[i] << 16) >> 16, K);
+                        term(A, (int32_t)xs[i] >> 16, (int32_t)ys[i] >> 16, K);
+                    } else {
+                        term(A, (int32_t)xs[i], (int32_t)ys[i], K);
+                    }
+                }
+            }
+            return;
+        }
+        raw(A, x, y);
+    }
+    __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
+        return MODE == CE_ALL ? (uint64_t)A.s : smod_p(A.s, K);
+    }
+};
+
+// binary64 storage: T = fma(x, y, T) is exact while |T| < 2^53; every KF products the centered
+// reduction T -= rint(T invP) P (exact by FMA; the quotient is within 1 of round(T/p)) and one +-P
+// fix-up bring T back to [-h, h].  KF = 0: no reduction before the end of the thread.
+__device__ __forceinline__ double centered_reduce(double T, const KParams &K) {
+    const double q = rint(__dmul_rn(T, K.inv_p));
+    T = __fma_rn(-q, K.pd, T);
+    if (T > K.hd)
+        T -= K.pd;
+    else if (T < -K.hd)
+        T += K.pd;
+    return T;
+}
+
+template <int KF>
+struct Fp64C {
+    using elem = double;
+    static constexpr int W = 2;
+    static constexpr bool kTable = false;
+    struct Acc {
+        double T;
+        int c;
+    };
+    __device__ __forceinline__ static void init(Acc &A) {
+        A.T = 0.0;
+        A.c = 0;
+    }
+    __device__ __forceinline__ static void term(Acc &A, double x, double y, const KParams &K,
+                                                const uint16_t * = nullptr) {
+        if (KF != 0 && A.c >= KF) {
+            A.T = centered_reduce(A.T, K);
+            A.c = 0;
+        }
+        A.T = __fma_rn(x, y, A.T);
+        ++A.c;
+    }
+    __device__ __forceinline__ static void vec(Acc &A, uint4 xv, uint4 yv, const KParams &K, const uint16_t *) {
+        const double x0 = __hiloint2double(xv.y, xv.x), x1 = __hiloint2double(xv.w, xv.z);
+        const double y0 = __hiloint2double(yv.y, yv.x), y1 = __hiloint2double(yv.w, yv.z);
+        if (KF == 1) {
+            term(A, x0, y0, K);
+            term(A, x1, y1, K);
+            return;
+        }
+        if (KF != 0 && A.c + 2 > KF) {  // close the block before it would exceed KF products
+            A.T = centered_reduce(A.T, K);
+            A.c = 0;
+        }
+        A.T = __fma_rn(x0, y0, A.T);
+        A.T = __fma_rn(x1, y1, A.T);
+        A.c += 2;
+    }
+    __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
+        return smod_p((int64_t)A.T, K);  // |T| < 2^53: an exact integer
+    }
+};
+
 // Pure-Zech arithmetic (sec. 2.4, Table 1).  A nonzero element
 // g^e is held as v = S e with e in [0, qbar] (e = qbar is g^0 again: the code qbar of P:126-131), the
 // zero element as kZ.  S = 2 makes v a byte offset into the u16 table (one register + the table base

@@ -32,6 +32,9 @@ enum Policy {
     P_CS = 32, P_CS_END = P_CS + 16,
     P_MONT_OVF = 64,
     P_ZECH_ADD = 65,  // pure-Zech accumulation (F3)
+    // centered representation (sec. 3.2.2): int16 / int32 storage x {ALL, THREAD, BLOCKED}, binary64 x KF
+    P_CE16_ALL = 66, P_CE16_THREAD, P_CE16_BLK, P_CE32_ALL, P_CE32_THREAD, P_CE32_BLK,
+    P_FC0, P_FC1, P_FC2, P_FC4, P_FC8,
     P_COUNT
 };
 constexpr int cs_policy(bool acc64, bool e32, int strat) { return P_CS + 8 * acc64 + 4 * e32 + (strat - 1); }
@@ -73,6 +76,13 @@ __device__ __forceinline__ void write_result(uint64_t r, const OutSpec &O, const
     case GFP_REP_ZECH:
         ((uint16_t *)O.out)[idx] = r == 0 ? (uint16_t)0 : K.logt[r];
         break;
+    case GFP_REP_CENTERED: {  // sec. 3.2.2: residues above h are stored as r - p
+        const int64_t c = r > (uint64_t)K.half ? (int64_t)r - (int64_t)K.p : (int64_t)r;
+        if (O.dtype == GFP_U16) ((int16_t *)O.out)[idx] = (int16_t)c;
+        else if (O.dtype == GFP_U32) ((int32_t *)O.out)[idx] = (int32_t)c;
+        else ((double *)O.out)[idx] = (double)c;  // exact, +0.0 for 0
+        break;
+    }
     default:  // classical residue, or Montgomery form (the sum of aB-forms is the aB-form)
         if (O.dtype == GFP_U16)
             ((uint16_t *)O.out)[idx] = (uint16_t)r;
@@ -183,7 +193,8 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
         if (t == gridDim.x - 1) {
             unsigned long long s;
             asm volatile("ld.relaxed.gpu.u64 %0, [%1];" : "=l"(s) : "l"(sum) : "memory");
-            write_result(mod_p(s, K.p, K.mu), O, K, 0);
+            // centered sums are signed (two's complement, |total| < 2^63 by the host's bound)
+            write_result(O.rep == GFP_REP_CENTERED ? smod_p((int64_t)s, K) : mod_p(s, K.p, K.mu), O, K, 0);
             *sum = 0;  // self-reset for the next launch on this stream
             *ws.counter = 0;
         }
@@ -521,12 +532,14 @@ __global__ void __launch_bounds__(NT) batch_kernel(const typename R::elem *__res
             for (int64_t j = done + g; j < n; j += LPR) R::term(acc, Ar[j], x[j], K, tab);
         }
         uint64_t v = group_sum<LPR>(valid ? R::finish(acc, K) : 0);
-        if (valid && g == 0) write_result(mod_p(v, K.p, K.mu), O, K, row);
+        if (valid && g == 0)
+            write_result(O.rep == GFP_REP_CENTERED ? smod_p((int64_t)v, K) : mod_p(v, K.p, K.mu), O, K, row);
     }
 }
 
 // ------------------------------------------------------------------------------ conversions
-enum ConvOp { C_TO_MONT, C_FROM_MONT, C_TO_ZECH, C_FROM_ZECH_SMALL, C_FROM_ZECH_LARGE, C_CAST };
+enum ConvOp { C_TO_MONT, C_FROM_MONT, C_TO_ZECH, C_FROM_ZECH_SMALL, C_FROM_ZECH_LARGE, C_CAST, C_TO_CENTERED,
+              C_FROM_CENTERED };
 
 template <int OP, typename TI, typename TO>
 __device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab) {
@@ -546,6 +559,12 @@ __device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab)
     } else if constexpr (OP == C_FROM_ZECH_LARGE) {
         uint32_t c = (uint32_t)v;
         return (TO)tab[c <= K.qbar ? c : K.qbar];  // antilog[0] = 0 sentinel
+    } else if constexpr (OP == C_TO_CENTERED) {  // residue r -> r or r - p (sec. 3.2.2)
+        const int64_t r = (int64_t)v;
+        return (TO)(r > K.half ? r - (int64_t)K.p : r);
+    } else if constexpr (OP == C_FROM_CENTERED) {  // c -> c or c + p
+        const int64_t c = (int64_t)v;
+        return (TO)(c < 0 ? c + (int64_t)K.p : c);
     } else {
         return (TO)v;
     }
@@ -671,13 +690,18 @@ static int dot_occupancy(size_t smem) {
 // pure-Zech fast path: small fields (2 qbar < 2^16, byte-offset table) of odd characteristic
 static bool zech_add_fast(uint64_t p) { return zech_small_layout(p) && p > 2; }
 static bool is_zech(int pol) { return pol >= P_ZS_ALL && pol <= P_ZL_THREAD; }
+static bool is_fc(int pol) { return pol >= P_FC0 && pol <= P_FC8; }
 static int policy_block(int pol) { return pol == P_ZECH_ADD ? kZaddNT : (is_zech(pol) ? kZechNT : kDotNT); }
 static int policy_unroll(int pol) {
     if (pol == P_ZECH_ADD) return kZaddU;
+    if (is_fc(pol)) return kFpU;
     return is_zech(pol) ? kZechU : ((pol >= P_FP_THREAD && pol <= P_FP_K2) ? kFpU : kDotU);
 }
 static int policy_width(int pol) {
     if (pol >= P_CS && pol < P_CS_END) return ((pol - P_CS) & 4) ? 4 : 8;
+    if (pol >= P_CE16_ALL && pol <= P_CE16_BLK) return 8;
+    if (pol >= P_CE32_ALL && pol <= P_CE32_BLK) return 4;
+    if (is_fc(pol)) return 2;
     if (pol <= P_CL32_OVF || (pol >= P_MONT1 && pol <= P_MONT4) || pol == P_MONT_OVF) return 4;
     if (pol >= P_FP_THREAD && pol <= P_FP_K2) return 2;
     return 8;
@@ -701,7 +725,21 @@ static int policy_width(int pol) {
     M(cs_policy(1, 1, 2), ClassicalS<uint64_t, uint32_t, S_BLOCKED>)                        \
     M(cs_policy(1, 1, 3), ClassicalS<uint64_t, uint32_t, S_OVERFLOW>)                       \
     M(cs_policy(1, 1, 4), ClassicalS<uint64_t, uint32_t, S_HYBRID>)                         \
-    M(P_MONT_OVF, MontgomeryOverflow)
+    M(P_MONT_OVF, MontgomeryOverflow)                                                         \
+    M(P_CE16_ALL, CenteredI<int16_t, CE_ALL>)                                                 \
+    M(P_CE16_THREAD, CenteredI<int16_t, CE_THREAD>)                                           \
+    M(P_CE16_BLK, CenteredI<int16_t, CE_BLOCKED>)                                             \
+    M(P_CE32_ALL, CenteredI<int32_t, CE_ALL>)                                                 \
+    M(P_CE32_THREAD, CenteredI<int32_t, CE_THREAD>)                                           \
+    M(P_CE32_BLK, CenteredI<int32_t, CE_BLOCKED>)
+
+// binary64 centered policies (unroll kFpU like Fp64)
+#define GFP_FC_CASES(M)      \
+    M(P_FC0, Fp64C<0>)       \
+    M(P_FC1, Fp64C<1>)       \
+    M(P_FC2, Fp64C<2>)       \
+    M(P_FC4, Fp64C<4>)       \
+    M(P_FC8, Fp64C<8>)
 
 static int policy_occupancy(int pol, size_t smem) {
     switch (pol) {
@@ -724,6 +762,10 @@ static int policy_occupancy(int pol, size_t smem) {
     case pol: return dot_occupancy<__VA_ARGS__, kDotNT, kDotU, false>(smem);
         GFP_CS_CASES(GFP_OCC)
 #undef GFP_OCC
+#define GFP_OCC_FC(pol, ...) \
+    case pol: return dot_occupancy<__VA_ARGS__, kDotNT, kFpU, false>(smem);
+        GFP_FC_CASES(GFP_OCC_FC)
+#undef GFP_OCC_FC
     case P_ZECH_ADD: return occupancy(zech_add_dot_kernel<kZaddNT, kZaddU, 2, true>, kZaddNT, smem);
     }
     return 1;
@@ -753,6 +795,10 @@ cudaError_t launch_dot(const DotPlan &P, const KParams &K0, const void *a, const
     case pol: return launch_dot_t<__VA_ARGS__, kDotNT, kDotU, false>(P, K, a, b, n, ws, O, s);
         GFP_CS_CASES(GFP_LAUNCH)
 #undef GFP_LAUNCH
+#define GFP_LAUNCH_FC(pol, ...) \
+    case pol: return launch_dot_t<__VA_ARGS__, kDotNT, kFpU, false>(P, K, a, b, n, ws, O, s);
+        GFP_FC_CASES(GFP_LAUNCH_FC)
+#undef GFP_LAUNCH_FC
     case P_ZECH_ADD: {
         // fast path for small odd-characteristic fields (p = 2 has qbar = 1: the checked kernel)
         auto kern = zech_add_fast(K.p) ? zech_add_dot_kernel<kZaddNT, kZaddU, 2, true>
@@ -767,6 +813,12 @@ cudaError_t launch_dot(const DotPlan &P, const KParams &K0, const void *a, const
 }
 
 static size_t elem_size(int dt) { return dt == GFP_U16 ? 2 : (dt == GFP_U32 ? 4 : 8); }
+
+// binary64 centered: the largest compiled block KF in {8, 4, 2, 1} not above lambda_c
+static int fc_policy(uint64_t lambda_c) {
+    return lambda_c >= 8 ? P_FC8 : (lambda_c >= 4 ? P_FC4 : (lambda_c >= 2 ? P_FC2 : P_FC1));
+}
+static uint64_t fc_block(int pol) { return pol == P_FC8 ? 8 : (pol == P_FC4 ? 4 : (pol == P_FC2 ? 2 : (pol == P_FC1 ? 1 : 0))); }
 
 // Explicit strategy (gfp_options) -> policy and block length; GFP_OK or the reason it is not admissible.
 static gfp_status resolve_strategy(const gfp_info &I, int64_t n, const gfp_options *opt, int *pol, uint64_t *kblk,
@@ -820,6 +872,23 @@ static gfp_status resolve_strategy(const gfp_info &I, int64_t n, const gfp_optio
         return GFP_OK;
     case GFP_REP_ZECH:
         return (strat == GFP_STRAT_AUTO && (bits == 0 || bits == 64)) ? GFP_OK : GFP_E_UNSUPPORTED;
+    case GFP_REP_CENTERED: {  // sec. 3.2.2: DELAYED (one reduction at the end) or BLOCKED (lambda_c)
+        const bool f64 = I.dtype == GFP_F64;
+        if (bits != 0 && bits != (f64 ? 53 : 64)) return GFP_E_INVAL;
+        const u128 h = (u128)(I.p - 1) / 2, h2 = h * h;
+        if (strat == GFP_STRAT_DELAYED) {
+            if (f64 ? (u128)n * h2 + h >= ((u128)1 << 53) : (u128)n * h2 + h > (((u128)1 << 63) - 1))
+                return GFP_E_BOUND;
+            *pol = f64 ? P_FC0 : (I.dtype == GFP_U16 ? P_CE16_ALL : P_CE32_ALL);
+        } else if (strat == GFP_STRAT_BLOCKED || (strat == GFP_STRAT_AUTO && bits != 0)) {
+            *pol = f64 ? fc_policy(I.k) : (I.dtype == GFP_U16 ? P_CE16_BLK : P_CE32_BLK);
+            *kblk = f64 ? fc_block(*pol) : I.k;
+        } else if (strat != GFP_STRAT_AUTO) {
+            return GFP_E_UNSUPPORTED;  // the signed overflow trick / hybrid centered
+        }
+        *acc_bits = f64 ? 53 : 64;
+        return GFP_OK;
+    }
     }
     return GFP_E_INVAL;
 }
@@ -843,6 +912,17 @@ static const char *policy_name(int pol) {
     case P_ZL_THREAD: return "dot_kernel<Zech<LARGE,THREAD>>";
     case P_MONT_OVF: return "dot_kernel<MontgomeryOverflow>";
     case P_ZECH_ADD: return "zech_add_dot_kernel";
+    case P_CE16_ALL: return "dot_kernel<CenteredI<i16,ALL>>";
+    case P_CE16_THREAD: return "dot_kernel<CenteredI<i16,THREAD>>";
+    case P_CE16_BLK: return "dot_kernel<CenteredI<i16,BLOCKED>>";
+    case P_CE32_ALL: return "dot_kernel<CenteredI<i32,ALL>>";
+    case P_CE32_THREAD: return "dot_kernel<CenteredI<i32,THREAD>>";
+    case P_CE32_BLK: return "dot_kernel<CenteredI<i32,BLOCKED>>";
+    case P_FC0: return "dot_kernel<Fp64C<0>>";
+    case P_FC1: return "dot_kernel<Fp64C<1>>";
+    case P_FC2: return "dot_kernel<Fp64C<2>>";
+    case P_FC4: return "dot_kernel<Fp64C<4>>";
+    case P_FC8: return "dot_kernel<Fp64C<8>>";
     }
     if (pol >= P_CS && pol < P_CS_END) {
         static const char *names[16] = {
@@ -876,6 +956,9 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
     case GFP_REP_MONTGOMERY: pol = I.mont_kr >= 4 ? P_MONT4 : (I.mont_kr >= 2 ? P_MONT2 : P_MONT1); break;
     case GFP_REP_FP64: pol = I.k >= 2 ? P_FP_K2 : P_FP_K1; break;
     case GFP_REP_ZECH: pol = zech_small_layout(I.p) ? P_ZS_ALL : P_ZL_ALL; break;
+    case GFP_REP_CENTERED:
+        pol = I.dtype == GFP_F64 ? fc_policy(I.k) : (I.dtype == GFP_U16 ? P_CE16_THREAD : P_CE32_THREAD);
+        break;
     }
     int xpol = -1, acc_bits = I.acc_bits;
     uint64_t kblk = 0;
@@ -947,6 +1030,31 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
             }
             break;
         }
+        case GFP_REP_CENTERED: {  // sec. 3.2.2: the doubled block, lambda_c h^2 + h < 2^(m-1)
+            const u128 h = (u128)(I.p - 1) / 2, h2 = h * h, w63 = ((u128)1 << 63) - 1;
+            if (I.dtype == GFP_F64) {
+                if (per_thread * h2 + h < ((u128)1 << 53)) {
+                    pol = P_FC0;
+                } else {
+                    acc = GFP_ACC_BLOCKED;
+                    strat = GFP_STRAT_BLOCKED;
+                    kblk = fc_block(pol);
+                    reductions = (int64_t)(per_thread / kblk) + 1;
+                }
+            } else if ((u128)n * h2 + h <= w63) {
+                pol = I.dtype == GFP_U16 ? P_CE16_ALL : P_CE32_ALL;  // one final reduction
+                reductions = 0;
+            } else if (per_thread * h2 + h <= w63) {
+                pol = I.dtype == GFP_U16 ? P_CE16_THREAD : P_CE32_THREAD;
+            } else {
+                pol = I.dtype == GFP_U16 ? P_CE16_BLK : P_CE32_BLK;
+                acc = GFP_ACC_BLOCKED;
+                strat = GFP_STRAT_BLOCKED;
+                kblk = I.k;
+                reductions = (int64_t)(per_thread / kblk) + 1;
+            }
+            break;
+        }
         }
     } else {
         strat = (pol >= P_CS && pol < P_CS_END) ? ((pol - P_CS) & 3) + 1
@@ -957,6 +1065,7 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
         acc = strat == GFP_STRAT_OVERFLOW || strat == GFP_STRAT_HYBRID ? GFP_ACC_OVERFLOW
               : (strat == GFP_STRAT_BLOCKED ? GFP_ACC_BLOCKED : GFP_ACC_DELAYED);
         if (pol == P_FP_K2 || pol == P_FP_K1) kblk = pol == P_FP_K2 ? 2 : 1;
+        if (is_fc(pol)) kblk = fc_block(pol);
         if (strat == GFP_STRAT_OVERFLOW || strat == GFP_STRAT_ZECH_ADD) {
             reductions = (int64_t)per_thread;  // one wrap test / one Zech addition (table lookup) per term
             if (pol == P_ZECH_ADD) acc_bits = 0;
@@ -1043,6 +1152,10 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
             case P_FP_THREAD: *err = launch_batch_t<Fp64<0>, 256, 4>(K2, A, lda, x, rows, n, vec, O, s); break;
             case P_FP_K2: *err = launch_batch_t<Fp64<2>, 256, 4>(K2, A, lda, x, rows, n, vec, O, s); break;
             case P_FP_K1: *err = launch_batch_t<Fp64<1>, 256, 4>(K2, A, lda, x, rows, n, vec, O, s); break;
+#define GFP_BATCH_FC(pol, ...) \
+    case pol: *err = launch_batch_t<__VA_ARGS__, 256, 4>(K2, A, lda, x, rows, n, vec, O, s); break;
+                GFP_FC_CASES(GFP_BATCH_FC)
+#undef GFP_BATCH_FC
             default: return GFP_E_UNSUPPORTED;
             }
             return *err == cudaSuccess ? GFP_OK : GFP_E_CUDA;
@@ -1101,6 +1214,29 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
         else
             *err = launch_batch_t<Zech<false, false>, 1024, 2>(K, A, lda, x, rows, n, vec, O, s);
         break;
+    case GFP_REP_CENTERED: {  // sec. 3.2.2: per-row sums; one reduction per lane unless a row overflows
+        const u128 h = (u128)(I.p - 1) / 2, h2 = h * h, w63 = ((u128)1 << 63) - 1;
+        KParams K2 = K;
+        K2.kblk = I.k;
+        if (I.dtype == GFP_F64) {
+            if (per_lane * h2 + h < ((u128)1 << 53))
+                *err = launch_batch_t<Fp64C<0>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+            else
+                switch (fc_policy(I.k)) {
+                case P_FC8: *err = launch_batch_t<Fp64C<8>, 256, 4>(K, A, lda, x, rows, n, vec, O, s); break;
+                case P_FC4: *err = launch_batch_t<Fp64C<4>, 256, 4>(K, A, lda, x, rows, n, vec, O, s); break;
+                case P_FC2: *err = launch_batch_t<Fp64C<2>, 256, 4>(K, A, lda, x, rows, n, vec, O, s); break;
+                default: *err = launch_batch_t<Fp64C<1>, 256, 4>(K, A, lda, x, rows, n, vec, O, s); break;
+                }
+        } else if (I.dtype == GFP_U16) {
+            *err = (u128)n * h2 + h <= w63 ? launch_batch_t<CenteredI<int16_t, CE_ALL>, 256, 4>(K, A, lda, x, rows, n, vec, O, s)
+                                          : launch_batch_t<CenteredI<int16_t, CE_BLOCKED>, 256, 4>(K2, A, lda, x, rows, n, vec, O, s);
+        } else {
+            *err = (u128)n * h2 + h <= w63 ? launch_batch_t<CenteredI<int32_t, CE_ALL>, 256, 4>(K, A, lda, x, rows, n, vec, O, s)
+                                          : launch_batch_t<CenteredI<int32_t, CE_BLOCKED>, 256, 4>(K2, A, lda, x, rows, n, vec, O, s);
+        }
+        break;
+    }
     }
     return *err == cudaSuccess ? GFP_OK : GFP_E_CUDA;
 }
@@ -1150,6 +1286,29 @@ gfp_status launch_convert(const gfp_info &I, const KParams &K, int dir, gfp_dtyp
         if (in_dt != GFP_U32 || out_dt != GFP_U32) return GFP_E_UNSUPPORTED;
         *err = dir == 0 ? launch_conv_t<C_TO_MONT, uint32_t, uint32_t>(K, in, out, n, nullptr, 0, s)
                         : launch_conv_t<C_FROM_MONT, uint32_t, uint32_t>(K, in, out, n, nullptr, 0, s);
+        break;
+    case GFP_REP_CENTERED:  // sec. 3.2.2: residues <-> signed values in [-h, h] (int16 / int32 / binary64)
+        if (dir == 0) {
+            if (out_dt == GFP_F64)
+                *err = in16 ? launch_conv_t<C_TO_CENTERED, uint16_t, double>(K, in, out, n, nullptr, 0, s)
+                            : launch_conv_t<C_TO_CENTERED, uint32_t, double>(K, in, out, n, nullptr, 0, s);
+            else if (out16)
+                *err = in16 ? launch_conv_t<C_TO_CENTERED, uint16_t, int16_t>(K, in, out, n, nullptr, 0, s)
+                            : launch_conv_t<C_TO_CENTERED, uint32_t, int16_t>(K, in, out, n, nullptr, 0, s);
+            else
+                *err = in16 ? launch_conv_t<C_TO_CENTERED, uint16_t, int32_t>(K, in, out, n, nullptr, 0, s)
+                            : launch_conv_t<C_TO_CENTERED, uint32_t, int32_t>(K, in, out, n, nullptr, 0, s);
+        } else {
+            if (in_dt == GFP_F64)
+                *err = out16 ? launch_conv_t<C_FROM_CENTERED, double, uint16_t>(K, in, out, n, nullptr, 0, s)
+                             : launch_conv_t<C_FROM_CENTERED, double, uint32_t>(K, in, out, n, nullptr, 0, s);
+            else if (in16)
+                *err = out16 ? launch_conv_t<C_FROM_CENTERED, int16_t, uint16_t>(K, in, out, n, nullptr, 0, s)
+                             : launch_conv_t<C_FROM_CENTERED, int16_t, uint32_t>(K, in, out, n, nullptr, 0, s);
+            else
+                *err = out16 ? launch_conv_t<C_FROM_CENTERED, int32_t, uint16_t>(K, in, out, n, nullptr, 0, s)
+                             : launch_conv_t<C_FROM_CENTERED, int32_t, uint32_t>(K, in, out, n, nullptr, 0, s);
+        }
         break;
     case GFP_REP_ZECH: {
         const uint32_t log_entries = (uint32_t)((I.p + 7) & ~7ull);

@@ -107,6 +107,8 @@ uint64_t rep_bound(gfp_rep rep, gfp_dtype dt) {
         return dt == GFP_F64 ? 94906249ull : 0;                                // p(p-1) < 2^53
     case GFP_REP_ZECH:
         return dt == GFP_U16 ? 65521ull : 0;                                   // u16 codes
+    case GFP_REP_CENTERED:                                                     // sec. 3.2.2
+        return dt == GFP_U16 ? 65521ull : (dt == GFP_U32 ? 4294967291ull : 189812507ull);
     }
     return 0;
 }
@@ -129,8 +131,26 @@ bool rep_predicate(gfp_rep rep, gfp_dtype dt, uint64_t p) {
         return dt == GFP_F64 && P * (P - 1) < ((u128)1 << 53);
     case GFP_REP_ZECH:
         return dt == GFP_U16 && p - 1 <= 0xFFFFull;
+    case GFP_REP_CENTERED: {
+        // odd p (no symmetric range at p = 2); h = (p-1)/2 fits the signed storage; binary64:
+        // one product plus a carried residue stays exact, h^2 + h < 2^53
+        if ((p & 1) == 0) return false;
+        const u128 h = (P - 1) / 2;
+        if (dt == GFP_U16) return h <= 32767;
+        if (dt == GFP_U32) return h <= 0x7FFFFFFFull;
+        return h * h + h < ((u128)1 << 53);
+    }
     }
     return false;
+}
+
+uint64_t centered_k(uint64_t p, int m) {
+    const u128 h = (u128)(p - 1) / 2, q = h * h;
+    const u128 w = m == 53 ? ((u128)1 << 53) - 1 : ((u128)1 << 63) - 1;  // |T| <= 2^53 - 1 / 2^63 - 1
+    if (q == 0) return UINT64_MAX;
+    if (w < h) return 0;
+    u128 k = (w - h) / q;
+    return k > UINT64_MAX ? UINT64_MAX : (uint64_t)k;
 }
 
 uint64_t block_k(uint64_t p, int m) {
@@ -196,7 +216,7 @@ void zech_plus1_delta(uint64_t p, const std::vector<uint16_t> &log_table, std::v
 }
 
 gfp_status describe(uint64_t p, gfp_rep rep, gfp_dtype dt, gfp_info *info) {
-    if ((int)rep < 0 || (int)rep > 3 || (int)dt < 0 || (int)dt > 2) return GFP_E_INVAL;
+    if ((int)rep < 0 || (int)rep > 4 || (int)dt < 0 || (int)dt > 2) return GFP_E_INVAL;
     const uint64_t bound = rep_bound(rep, dt);
     if (bound == 0) return GFP_E_UNSUPPORTED;
     if (!is_prime(p)) return GFP_E_NOT_PRIME;
@@ -206,8 +226,8 @@ gfp_status describe(uint64_t p, gfp_rep rep, gfp_dtype dt, gfp_info *info) {
     I.rep = rep;
     I.dtype = dt;
     I.bound = bound;
-    I.acc_bits = rep == GFP_REP_FP64 ? 53 : 64;
-    I.k = block_k(p, I.acc_bits);
+    I.acc_bits = (rep == GFP_REP_FP64 || (rep == GFP_REP_CENTERED && dt == GFP_F64)) ? 53 : 64;
+    I.k = rep == GFP_REP_CENTERED ? centered_k(p, I.acc_bits) : block_k(p, I.acc_bits);
     I.corr = (uint64_t)((((u128)1) << 64) % p);
     I.b_mod_p = (uint64_t)((((u128)1) << 32) % p);
     I.inv_p = 1.0 / (double)p;  // IEEE round-to-nearest division (reading G8)

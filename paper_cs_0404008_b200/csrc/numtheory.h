@@ -32,6 +32,9 @@ bool rep_predicate(gfp_rep rep, gfp_dtype dt, uint64_t p);
 
 // Eq. (1) with a carried residue (reading G7): largest k with k(p-1)^2 + (p-1) <= 2^m - 1.
 uint64_t block_k(uint64_t p, int m);
+// Centered representation (sec. 3.2.2): largest k with k h^2 + h <= 2^63 - 1 (m = 64, a signed
+// 64-bit accumulator: "lambda_centered ((p-1)/2)^2 < 2^(m-1)") or < 2^53 (m = 53, binary64), h = (p-1)/2.
+uint64_t centered_k(uint64_t p, int m);
 // Montgomery products per REDC (reading G6): largest k with k(p-1)^2 <= pB (REDC precondition,
 // P:73) and k(p-1)^2 + (B-1)p <= 2^64 - 1 (T + Up fits the 64-bit word), B = 2^32.
 uint64_t mont_k(uint64_t p);

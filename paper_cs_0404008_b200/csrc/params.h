@@ -25,6 +25,10 @@ struct KParams {
     uint64_t kblk;
     uint32_t corr32;    // 2^32 mod p
     uint32_t mu32;      // floor((2^32 - 1) / p)
+    // centered representation (sec. 3.2.2)
+    int64_t half;       // h = (p - 1) / 2
+    double hd;          // h as binary64
+    uint64_t c63;       // 2^63 mod p
 };
 
 }  // namespace dev

@@ -322,3 +322,48 @@ def test_shipped_install_time_table_loads_by_default():
     n, ok = out[0].split()
     assert int(n) >= 100 and ok == "True"
     assert out[1] == "ClassicalS<u64acc,u32,HYBRID>"
+
+
+# ------------------------------------------------------------------------------ centered representation (F2)
+CE = gfp.CENTERED
+
+
+def test_centered_bounds_and_block_lengths():
+    """sec. 3.2.2: storage bounds (h = (p-1)/2 fits int16 / int32; binary64 h(h+1) < 2^53),
+    odd p only, and lambda_c: the largest k with k h^2 + h < 2^63 (int64) / 2^53 (binary64),
+    recomputed here with Python integers -- roughly twice the unsigned k at the same word."""
+    for p, dt, ok in [(65521, U16, True), (4294967291, U32, True), (189812507, F64, True),
+                      (189812533, F64, False), (2, U16, False), (65537, U16, False)]:
+        st, info = q(p, CE, dt)
+        assert (st == OK) == ok, (p, dt, st)
+        if ok:
+            h = (p - 1) // 2
+            w = 2 ** 53 if dt == F64 else 2 ** 63
+            assert info.k * h * h + h < w <= (info.k + 1) * h * h + h
+            assert info.acc_bits == (53 if dt == F64 else 64)
+    assert q(67108859, CE, F64)[1].k == 8 and q(67108859, FP, F64)[1].k == 2  # SURVEY A26: C2 k 2 -> 8
+    for p in [5, 101, 32749, 65521, 2 ** 31 - 1, 4294967291]:
+        dt = U16 if p <= 65521 else U32
+        kc, kz = q(p, CE, dt)[1].k, q(p, CL, U32)[1].k
+        assert kc >= 2 * kz - 2, p  # SPEC: K_centered >= 2 K_zpz - c (S:565)
+    for p, dt, ok in [(67108859, F64, True)]:
+        st, _ = q(p, CE, dt)
+        assert st == OK
+
+
+def test_centered_plans_and_rejections():
+    import torch
+    P = gfp.plan
+    d = P(67108859, CE, 10 ** 7, dtype=torch.float64)
+    assert d["kernel"] == "dot_kernel<Fp64C<8>>" and d["block"] == 8 and d["strategy_name"] == "blocked"
+    assert P(65521, CE, 10 ** 7, dtype=torch.int16)["kernel"] == "dot_kernel<CenteredI<i16,ALL>>"
+    assert P(4294967291, CE, 10 ** 7, dtype=torch.int32)["kernel"] == "dot_kernel<CenteredI<i32,BLOCKED>>"
+    assert P(4294967291, CE, 10 ** 7, dtype=torch.int32)["block"] == 2
+    assert P(67108859, CE, 4, dtype=torch.float64, strategy=gfp.DELAYED)["kernel"] == "dot_kernel<Fp64C<0>>"
+    for strat in (gfp.OVERFLOW, gfp.HYBRID, gfp.ZECH_ADD):  # signed overflow trick / hybrid centered: OUT
+        with pytest.raises(gfp.GfpError) as e:
+            P(32749, CE, 10, dtype=torch.int16, strategy=strat)
+        assert e.value.status == E_UNSUPPORTED
+    with pytest.raises(gfp.GfpError) as e:
+        P(67108859, CE, 10 ** 7, dtype=torch.float64, strategy=gfp.DELAYED)
+    assert e.value.status == E_BOUND
