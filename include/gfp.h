@@ -105,16 +105,20 @@ typedef enum {
     GFP_STRAT_BLOCKED = 2,  /* sec. 3.2: reduce every k = floor((2^m-1-(p-1))/(p-1)^2) products (G7) */
     GFP_STRAT_OVERFLOW = 3, /* sec. 3.3: wrap test + CORR = 2^m mod p on every product */
     GFP_STRAT_HYBRID = 4,   /* sec. 3.4 Eq. (2): one wrap test per block of lambda, lambda p(p-1) < 2^m */
-    GFP_STRAT_ZECH_ADD = 5  /* Zech only: pure discrete-log accumulation -- every product is an index
+    GFP_STRAT_ZECH_ADD = 5, /* Zech only: pure discrete-log accumulation -- every product is an index
                                addition and every sum a Zech addition through the t_plus1 table
                                (sec. 2.4, Table 1); partial sums never leave the
                                representation.  Same unique result as the default (integer) plan. */
+    GFP_STRAT_CARRY = 6     /* classical and Montgomery: the division-on-demand idea of sec. 3.3
+                               with the correction deferred -- count the wraps of the m-bit sum in a
+                               second word (carry += sum < product) and apply carry * (2^m mod p) once at
+                               the end instead of adding CORR at every wrap (SURVEY 8(f) F2 "carry-word") */
 } gfp_strategy;
 
 /* Per-call options.  acc_bits: the accumulator width m of Eq. (1): 0 = default (64; 53 for fp64),
  * 32 or 64 for classical storage (m = 32 needs p(p-1) < 2^32, i.e. p <= 65521).  Admissible
- * combinations: classical x {AUTO..HYBRID} x {32, 64}; Montgomery x {AUTO, BLOCKED (REDC every
- * k_R products, sec. 3.2.1), OVERFLOW (overflow-Montgomery, sec. 3.3)}; fp64 x {AUTO,
+ * combinations: classical x {AUTO..HYBRID, CARRY} x {32, 64}; Montgomery x {AUTO, BLOCKED (REDC every
+ * k_R products, sec. 3.2.1), OVERFLOW (overflow-Montgomery, sec. 3.3), CARRY}; fp64 x {AUTO,
  * DELAYED, BLOCKED}; Zech x {AUTO, ZECH_ADD}; centered x {AUTO, DELAYED, BLOCKED} (the signed overflow trick,
  * P:441-457, and hybrid centered, are not offered: the paper finds the first too costly and
  * shows the second cannot work).  Anything else: GFP_E_UNSUPPORTED; a strategy whose bound the

@@ -18,7 +18,7 @@ import os
 import torch
 
 __all__ = [
-    "CLASSICAL", "MONTGOMERY", "FP64", "ZECH", "CENTERED", "AUTO", "DELAYED", "BLOCKED", "OVERFLOW", "HYBRID", "ZECH_ADD",
+    "CLASSICAL", "MONTGOMERY", "FP64", "ZECH", "CENTERED", "AUTO", "DELAYED", "BLOCKED", "OVERFLOW", "HYBRID", "ZECH_ADD", "CARRY",
     "GfpError", "lib", "query", "plan", "dot", "dot_ex", "dot_batch", "dot_batch_ex",
     "dot_partial", "finalize", "to_rep", "from_rep", "dot_host", "launch_count", "release_caches",
     "rep_dtype", "tune", "tune_entries", "tune_set", "tune_save", "tune_load", "tune_clear",
@@ -28,8 +28,9 @@ CLASSICAL, MONTGOMERY, FP64, ZECH, CENTERED = 0, 1, 2, 3, 4
 U16, U32, F64 = 0, 1, 2
 AUTO, DELAYED, BLOCKED, OVERFLOW, HYBRID = 0, 1, 2, 3, 4  # gfp_strategy (paper sec. 3)
 ZECH_ADD = 5  # pure discrete-log accumulation through t_plus1 (sec. 2.4 Table 1), Zech only
+CARRY = 6  # sec. 3.3 with the wrap corrections deferred: a carry word counts wraps (classical, Montgomery)
 _STRAT_NAMES = {AUTO: "auto", DELAYED: "delayed", BLOCKED: "blocked", OVERFLOW: "overflow", HYBRID: "hybrid",
-                ZECH_ADD: "zech_add"}
+                ZECH_ADD: "zech_add", CARRY: "carry"}
 _REP_NAMES = {CLASSICAL: "classical", MONTGOMERY: "montgomery", FP64: "fp64", ZECH: "zech", CENTERED: "centered"}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))

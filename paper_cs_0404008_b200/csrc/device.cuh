@@ -461,7 +461,9 @@ struct Ops {
 //   S_OVERFLOW sec. 3.3 listing P:414-422: sum += product; if (sum < product) sum += CORR
 //   S_HYBRID   sec. 3.4, Eq. (2): one wrap test per block of K.kblk = lambda products,
 //              lambda p (p-1) < 2^m; the block sum cannot wrap twice nor re-wrap after CORR
-enum Strategy { S_DELAYED = 1, S_BLOCKED = 2, S_OVERFLOW = 3, S_HYBRID = 4 };
+//   S_CARRY    sec. 3.3 with the correction deferred: carry += (sum < product) counts the wraps;
+//              the thread's value is carry 2^m + sum = carry (2^m mod p) + sum (mod p)
+enum Strategy { S_DELAYED = 1, S_BLOCKED = 2, S_OVERFLOW = 3, S_HYBRID = 4, S_CARRY = 6 };
 
 template <typename ACC, typename E, int STRAT>
 struct ClassicalS {
@@ -501,6 +503,9 @@ struct ClassicalS {
         } else if (STRAT == S_OVERFLOW) {
             A.s += prod;
             if (A.s < prod) A.s += corr(K);
+        } else if (STRAT == S_CARRY) {
+            A.s += prod;
+            A.base += A.s < prod;  // `base` holds the wrap count (carry word)
         } else {  // S_HYBRID: close the block (its one wrap test) before it would exceed lambda products
             if (A.cnt >= K.kblk) {
                 if (A.s < A.base) A.s += corr(K);
@@ -562,6 +567,10 @@ struct ClassicalS {
         }
     }
     __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
+        if (STRAT == S_CARRY) {  // carry 2^m + s: carry < 2^32 terms per thread, (2^m mod p) < p < 2^32
+            const uint64_t c = mod_p((uint64_t)A.base, K.p, K.mu) * (sizeof(ACC) == 4 ? (uint64_t)K.corr32 : K.corr);
+            return mod_p(mod_p(c, K.p, K.mu) + (uint64_t)reduce(A.s, K), K.p, K.mu);
+        }
         if (STRAT == S_HYBRID && A.s < A.base) A.s += corr(K);  // the last, partial block
         return (uint64_t)reduce(A.s, K);
     }
@@ -592,6 +601,35 @@ struct MontgomeryOverflow {
     __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
         const uint32_t p = (uint32_t)K.p;
         const uint32_t r = redc(mod_p(A.S, K.p, K.mu), p, K.n_im);  // T < p <= pB: r <= p
+        return r >= p ? r - p : r;
+    }
+};
+
+// Montgomery with the carry word: products x~ y~ = ab B^2 summed in a u64 with the wraps counted in a
+// second word; the thread's value carry 2^64 + S reduces to (carry CORR + S) mod p, then ONE REDC returns
+// to B^1 scale (as overflow-Montgomery, with the corrections deferred to the end).
+struct MontgomeryCarry {
+    using elem = uint32_t;
+    static constexpr int W = 4;
+    static constexpr bool kTable = false;
+    struct Acc { uint64_t S, carry; };
+    __device__ __forceinline__ static void init(Acc &A) { A.S = 0; A.carry = 0; }
+    __device__ __forceinline__ static void term(Acc &A, uint32_t x, uint32_t y, const KParams &,
+                                                const uint16_t * = nullptr) {
+        const uint64_t prod = (uint64_t)x * y;
+        A.S += prod;
+        A.carry += A.S < prod;
+    }
+    __device__ __forceinline__ static void vec(Acc &A, uint4 x, uint4 y, const KParams &K, const uint16_t *) {
+        term(A, x.x, y.x, K);
+        term(A, x.y, y.y, K);
+        term(A, x.z, y.z, K);
+        term(A, x.w, y.w, K);
+    }
+    __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
+        const uint32_t p = (uint32_t)K.p;
+        const uint64_t T = mod_p(mod_p(A.carry, K.p, K.mu) * K.corr + mod_p(A.S, K.p, K.mu), K.p, K.mu);
+        const uint32_t r = redc(T, p, K.n_im);  // T < p <= pB: r <= p
         return r >= p ? r - p : r;
     }
 };

@@ -28,8 +28,10 @@ enum Policy {
     P_MONT1, P_MONT2, P_MONT4,
     P_FP_THREAD, P_FP_K1, P_FP_K2,
     P_ZS_ALL, P_ZS_THREAD, P_ZL_ALL, P_ZL_THREAD,
-    // explicit strategies (gfp_dot_ex): P_CS + 8*acc64 + 4*elem32 + (strategy - 1)
-    P_CS = 32, P_CS_END = P_CS + 16,
+    // explicit strategies (gfp_dot_ex): P_CS + 10*acc64 + 5*elem32 + (strategy - 1), strategies 1..4 and
+    // the carry word (slot 4)
+    P_CS = 32, P_CS_END = P_CS + 20,
+    P_MONT_CARRY = 63,  // Montgomery with the carry word
     P_MONT_OVF = 64,
     P_ZECH_ADD = 65,  // pure-Zech accumulation (F3)
     // centered representation (sec. 3.2.2): int16 / int32 storage x {ALL, THREAD, BLOCKED}, binary64 x KF
@@ -37,7 +39,9 @@ enum Policy {
     P_FC0, P_FC1, P_FC2, P_FC4, P_FC8,
     P_COUNT
 };
-constexpr int cs_policy(bool acc64, bool e32, int strat) { return P_CS + 8 * acc64 + 4 * e32 + (strat - 1); }
+constexpr int cs_slot(int strat) { return strat == GFP_STRAT_CARRY ? 4 : strat - 1; }
+constexpr int cs_policy(bool acc64, bool e32, int strat) { return P_CS + 10 * acc64 + 5 * e32 + cs_slot(strat); }
+constexpr int cs_strategy(int pol) { return (pol - P_CS) % 5 == 4 ? GFP_STRAT_CARRY : (pol - P_CS) % 5 + 1; }
 
 static thread_local uint64_t t_launches = 0;
 void count_launch() { ++t_launches; }
@@ -698,7 +702,7 @@ static int policy_unroll(int pol) {
     return is_zech(pol) ? kZechU : ((pol >= P_FP_THREAD && pol <= P_FP_K2) ? kFpU : kDotU);
 }
 static int policy_width(int pol) {
-    if (pol >= P_CS && pol < P_CS_END) return ((pol - P_CS) & 4) ? 4 : 8;
+    if (pol >= P_CS && pol < P_CS_END) return ((pol - P_CS) % 10 >= 5) ? 4 : 8;
     if (pol >= P_CE16_ALL && pol <= P_CE16_BLK) return 8;
     if (pol >= P_CE32_ALL && pol <= P_CE32_BLK) return 4;
     if (is_fc(pol)) return 2;
@@ -713,19 +717,24 @@ static int policy_width(int pol) {
     M(cs_policy(0, 0, 2), ClassicalS<uint32_t, uint16_t, S_BLOCKED>)                        \
     M(cs_policy(0, 0, 3), ClassicalS<uint32_t, uint16_t, S_OVERFLOW>)                       \
     M(cs_policy(0, 0, 4), ClassicalS<uint32_t, uint16_t, S_HYBRID>)                         \
+    M(cs_policy(0, 0, GFP_STRAT_CARRY), ClassicalS<uint32_t, uint16_t, S_CARRY>)            \
     M(cs_policy(0, 1, 1), ClassicalS<uint32_t, uint32_t, S_DELAYED>)                        \
     M(cs_policy(0, 1, 2), ClassicalS<uint32_t, uint32_t, S_BLOCKED>)                        \
     M(cs_policy(0, 1, 3), ClassicalS<uint32_t, uint32_t, S_OVERFLOW>)                       \
     M(cs_policy(0, 1, 4), ClassicalS<uint32_t, uint32_t, S_HYBRID>)                         \
+    M(cs_policy(0, 1, GFP_STRAT_CARRY), ClassicalS<uint32_t, uint32_t, S_CARRY>)            \
     M(cs_policy(1, 0, 1), ClassicalS<uint64_t, uint16_t, S_DELAYED>)                        \
     M(cs_policy(1, 0, 2), ClassicalS<uint64_t, uint16_t, S_BLOCKED>)                        \
     M(cs_policy(1, 0, 3), ClassicalS<uint64_t, uint16_t, S_OVERFLOW>)                       \
     M(cs_policy(1, 0, 4), ClassicalS<uint64_t, uint16_t, S_HYBRID>)                         \
+    M(cs_policy(1, 0, GFP_STRAT_CARRY), ClassicalS<uint64_t, uint16_t, S_CARRY>)            \
     M(cs_policy(1, 1, 1), ClassicalS<uint64_t, uint32_t, S_DELAYED>)                        \
     M(cs_policy(1, 1, 2), ClassicalS<uint64_t, uint32_t, S_BLOCKED>)                        \
     M(cs_policy(1, 1, 3), ClassicalS<uint64_t, uint32_t, S_OVERFLOW>)                       \
     M(cs_policy(1, 1, 4), ClassicalS<uint64_t, uint32_t, S_HYBRID>)                         \
+    M(cs_policy(1, 1, GFP_STRAT_CARRY), ClassicalS<uint64_t, uint32_t, S_CARRY>)            \
     M(P_MONT_OVF, MontgomeryOverflow)                                                         \
+    M(P_MONT_CARRY, MontgomeryCarry)                                                          \
     M(P_CE16_ALL, CenteredI<int16_t, CE_ALL>)                                                 \
     M(P_CE16_THREAD, CenteredI<int16_t, CE_THREAD>)                                           \
     M(P_CE16_BLK, CenteredI<int16_t, CE_BLOCKED>)                                             \
@@ -827,7 +836,7 @@ static gfp_status resolve_strategy(const gfp_info &I, int64_t n, const gfp_optio
     const int bits = opt ? opt->acc_bits : 0;
     *kblk = 0;
     *acc_bits = I.acc_bits;
-    if (strat < GFP_STRAT_AUTO || strat > GFP_STRAT_ZECH_ADD) return GFP_E_INVAL;
+    if (strat < GFP_STRAT_AUTO || strat > GFP_STRAT_CARRY) return GFP_E_INVAL;
     if (strat == GFP_STRAT_ZECH_ADD) {
         if (I.rep != GFP_REP_ZECH || (bits != 0 && bits != 64)) return GFP_E_UNSUPPORTED;
         *pol = P_ZECH_ADD;
@@ -857,6 +866,7 @@ static gfp_status resolve_strategy(const gfp_info &I, int64_t n, const gfp_optio
     case GFP_REP_MONTGOMERY:
         if (bits != 0 && bits != 64) return GFP_E_INVAL;
         if (strat == GFP_STRAT_OVERFLOW) *pol = P_MONT_OVF;
+        else if (strat == GFP_STRAT_CARRY) *pol = P_MONT_CARRY;
         else if (strat != GFP_STRAT_AUTO && strat != GFP_STRAT_BLOCKED) return GFP_E_UNSUPPORTED;
         return GFP_OK;
     case GFP_REP_FP64:
@@ -911,6 +921,7 @@ static const char *policy_name(int pol) {
     case P_ZL_ALL: return "dot_kernel<Zech<LARGE,ALL>>";
     case P_ZL_THREAD: return "dot_kernel<Zech<LARGE,THREAD>>";
     case P_MONT_OVF: return "dot_kernel<MontgomeryOverflow>";
+    case P_MONT_CARRY: return "dot_kernel<MontgomeryCarry>";
     case P_ZECH_ADD: return "zech_add_dot_kernel";
     case P_CE16_ALL: return "dot_kernel<CenteredI<i16,ALL>>";
     case P_CE16_THREAD: return "dot_kernel<CenteredI<i16,THREAD>>";
@@ -925,14 +936,15 @@ static const char *policy_name(int pol) {
     case P_FC8: return "dot_kernel<Fp64C<8>>";
     }
     if (pol >= P_CS && pol < P_CS_END) {
-        static const char *names[16] = {
-            "ClassicalS<u32acc,u16,DELAYED>", "ClassicalS<u32acc,u16,BLOCKED>", "ClassicalS<u32acc,u16,OVERFLOW>",
-            "ClassicalS<u32acc,u16,HYBRID>", "ClassicalS<u32acc,u32,DELAYED>", "ClassicalS<u32acc,u32,BLOCKED>",
-            "ClassicalS<u32acc,u32,OVERFLOW>", "ClassicalS<u32acc,u32,HYBRID>", "ClassicalS<u64acc,u16,DELAYED>",
-            "ClassicalS<u64acc,u16,BLOCKED>", "ClassicalS<u64acc,u16,OVERFLOW>", "ClassicalS<u64acc,u16,HYBRID>",
-            "ClassicalS<u64acc,u32,DELAYED>", "ClassicalS<u64acc,u32,BLOCKED>", "ClassicalS<u64acc,u32,OVERFLOW>",
-            "ClassicalS<u64acc,u32,HYBRID>"};
-        return names[pol - P_CS];
+        static const char *slot[5] = {"DELAYED", "BLOCKED", "OVERFLOW", "HYBRID", "CARRY"};
+        static std::string names[20];
+        static std::once_flag once;
+        std::call_once(once, [] {
+            for (int i = 0; i < 20; ++i)
+                names[i] = std::string("ClassicalS<") + (i >= 10 ? "u64acc," : "u32acc,") + (i % 10 >= 5 ? "u32," : "u16,") +
+                           slot[i % 5] + ">";
+        });
+        return names[pol - P_CS].c_str();
     }
     return "?";
 }
@@ -1057,16 +1069,17 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
         }
         }
     } else {
-        strat = (pol >= P_CS && pol < P_CS_END) ? ((pol - P_CS) & 3) + 1
-                : (pol == P_MONT_OVF ? GFP_STRAT_OVERFLOW : (opt ? opt->strategy : GFP_STRAT_AUTO));
+        strat = (pol >= P_CS && pol < P_CS_END) ? cs_strategy(pol)
+                : (pol == P_MONT_OVF ? GFP_STRAT_OVERFLOW
+                   : (pol == P_MONT_CARRY ? GFP_STRAT_CARRY : (opt ? opt->strategy : GFP_STRAT_AUTO)));
         if (strat == GFP_STRAT_AUTO) strat = GFP_STRAT_BLOCKED;
         if (pol == P_ZECH_ADD) strat = GFP_STRAT_ZECH_ADD;  // no integer accumulator at all
 
-        acc = strat == GFP_STRAT_OVERFLOW || strat == GFP_STRAT_HYBRID ? GFP_ACC_OVERFLOW
+        acc = strat == GFP_STRAT_OVERFLOW || strat == GFP_STRAT_HYBRID || strat == GFP_STRAT_CARRY ? GFP_ACC_OVERFLOW
               : (strat == GFP_STRAT_BLOCKED ? GFP_ACC_BLOCKED : GFP_ACC_DELAYED);
         if (pol == P_FP_K2 || pol == P_FP_K1) kblk = pol == P_FP_K2 ? 2 : 1;
         if (is_fc(pol)) kblk = fc_block(pol);
-        if (strat == GFP_STRAT_OVERFLOW || strat == GFP_STRAT_ZECH_ADD) {
+        if (strat == GFP_STRAT_OVERFLOW || strat == GFP_STRAT_ZECH_ADD || strat == GFP_STRAT_CARRY) {
             reductions = (int64_t)per_thread;  // one wrap test / one Zech addition (table lookup) per term
             if (pol == P_ZECH_ADD) acc_bits = 0;
         } else if (strat == GFP_STRAT_BLOCKED || strat == GFP_STRAT_HYBRID)

@@ -34,7 +34,7 @@ thread_local bool t_bypass = false;  // set while timing the built-in plan
 bool valid_entry(const gfp_tune_entry &e) {
     if (e.rep < GFP_REP_CLASSICAL || e.rep > GFP_REP_ZECH || e.dtype < GFP_U16 || e.dtype > GFP_F64) return false;
     if (e.kind != 0 && e.kind != 1) return false;
-    if (e.strategy < GFP_STRAT_AUTO || e.strategy > GFP_STRAT_ZECH_ADD) return false;
+    if (e.strategy < GFP_STRAT_AUTO || e.strategy > GFP_STRAT_CARRY) return false;
     if (e.kind == 1 && e.strategy == GFP_STRAT_ZECH_ADD) return false;  // no batch form
     return e.p > 1 && e.n >= 0 && e.rows >= 0;
 }
@@ -193,10 +193,13 @@ gfp_status gfp_tune(const gfp_tune_case *cases, int32_t ncases, double ms_per_ca
         switch (c.rep) {
         case GFP_REP_CLASSICAL:
             for (int m : {32, 64})
-                for (int st2 : {GFP_STRAT_DELAYED, GFP_STRAT_BLOCKED, GFP_STRAT_OVERFLOW, GFP_STRAT_HYBRID})
+                for (int st2 : {GFP_STRAT_DELAYED, GFP_STRAT_BLOCKED, GFP_STRAT_OVERFLOW, GFP_STRAT_HYBRID, GFP_STRAT_CARRY})
                     cand.push_back({st2, m});
             break;
-        case GFP_REP_MONTGOMERY: cand.push_back({GFP_STRAT_OVERFLOW, 0}); break;
+        case GFP_REP_MONTGOMERY:
+            cand.push_back({GFP_STRAT_OVERFLOW, 0});
+            cand.push_back({GFP_STRAT_CARRY, 0});
+            break;
         case GFP_REP_FP64:
             cand.push_back({GFP_STRAT_DELAYED, 0});
             cand.push_back({GFP_STRAT_BLOCKED, 0});

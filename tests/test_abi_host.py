@@ -367,3 +367,23 @@ def test_centered_plans_and_rejections():
     with pytest.raises(gfp.GfpError) as e:
         P(67108859, CE, 10 ** 7, dtype=torch.float64, strategy=gfp.DELAYED)
     assert e.value.status == E_BOUND
+
+
+def test_plan_carry_word():
+    """F2 carry word: a second word counts the wraps of the m-bit sum (sec. 3.3 with the CORR deferred);
+    admissible wherever the overflow strategy is (classical m = 32 / 64, Montgomery)."""
+    import torch
+    P = gfp.plan
+    assert P(4294967291, CL, 10 ** 6, strategy=gfp.CARRY, acc_bits=64)["kernel"] == "ClassicalS<u64acc,u32,CARRY>"
+    assert P(65521, CL, 10 ** 6, strategy=gfp.CARRY, acc_bits=32)["kernel"] == "ClassicalS<u32acc,u16,CARRY>"
+    assert P(65521, CL, 10, dtype=torch.uint32, strategy=gfp.CARRY, acc_bits=32)["kernel"] == "ClassicalS<u32acc,u32,CARRY>"
+    assert P(2 ** 31 - 1, MO, 10, strategy=gfp.CARRY)["kernel"] == "dot_kernel<MontgomeryCarry>"
+    assert P(2 ** 31 - 1, MO, 10, strategy=gfp.CARRY)["strategy_name"] == "carry"
+    for rep, p in [(FP, 67108859), (ZE, 32749), (CE, 32749)]:
+        with pytest.raises(gfp.GfpError) as e:
+            P(p, rep, 10, strategy=gfp.CARRY)
+        assert e.value.status == E_UNSUPPORTED
+    # every explicit classical policy keeps its own name (the 5-slot encoding)
+    names = {P(65521, CL, 1, strategy=s, acc_bits=m)["kernel"] for s in (gfp.DELAYED, gfp.BLOCKED, gfp.OVERFLOW,
+                                                                          gfp.HYBRID, gfp.CARRY) for m in (32, 64)}
+    assert len(names) == 10

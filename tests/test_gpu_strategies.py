@@ -17,7 +17,7 @@ gfp = pytest.importorskip("paper_cs_0404008_b200")
 CL, MO, FP = gfp.CLASSICAL, gfp.MONTGOMERY, gfp.FP64
 DEV = "cuda:0"
 SEED = synth.BASE_SEED + 77
-STRATS = [gfp.DELAYED, gfp.BLOCKED, gfp.OVERFLOW, gfp.HYBRID]
+STRATS = [gfp.DELAYED, gfp.BLOCKED, gfp.OVERFLOW, gfp.HYBRID, gfp.CARRY]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -67,7 +67,7 @@ def test_classical_strategies_small_primes(p):
 
 @pytest.mark.parametrize("p", [65537, 2 ** 31 - 1, 3037000493, 4294967291])
 def test_classical_strategies_large_primes_u64(p):
-    for strat in (gfp.BLOCKED, gfp.OVERFLOW, gfp.HYBRID):
+    for strat in (gfp.BLOCKED, gfp.OVERFLOW, gfp.HYBRID, gfp.CARRY):
         for n in [1, 2, 3, 4, 5, 1000, 100_003]:
             a = synth.uniform(SEED, 0, 0, n, p, np.uint32)
             b = synth.uniform(SEED, 1, 0, n, p, np.uint32)
@@ -86,8 +86,10 @@ def test_montgomery_overflow_variant(p):
         want = oracle.to_mont(p, oracle.dot_classical(p, a, b))
         assert as_int(gfp.dot_ex(am, bm, p, MO, strategy=gfp.OVERFLOW)) == want, (p, n)
         assert as_int(gfp.dot_ex(am, bm, p, MO, strategy=gfp.BLOCKED)) == want, (p, n)
+        assert as_int(gfp.dot_ex(am, bm, p, MO, strategy=gfp.CARRY)) == want, (p, n)
     w = gfp.to_rep(cu(np.full(300_001, p - 1, np.uint32)), p, MO)
     assert as_int(gfp.dot_ex(w, w, p, MO, strategy=gfp.OVERFLOW)) == oracle.to_mont(p, 300_001 % p)
+    assert as_int(gfp.dot_ex(w, w, p, MO, strategy=gfp.CARRY)) == oracle.to_mont(p, 300_001 % p)
 
 
 @pytest.mark.parametrize("p", [3, 101, 65521, 67108859, 94906249])
