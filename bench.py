@@ -219,7 +219,10 @@ def replicas(d, nbytes):
     return [d] + [{k: v.clone() for k, v in d.items()} for _ in range(R - 1)]
 
 
-def make_step(gfp, cfg, reps, world, group, stream):
+def make_step(gfp, cfg, reps, world, group, stream, xchg=None):
+    """One step of the hot path.  N > 1 single dots: the fused combine (one kernel per rank: shard dot +
+    peer-memory exchange + finalize, `xchg` a PeerExchange) or, with xchg None, gfp_dot_partial + one NCCL
+    all_reduce of 8 bytes + gfp_finalize."""
     from paper_cs_0404008_b200 import dist as gfp_dist
     p, rep = cfg["p"], cfg["rep"]
     ev = []  # (start, end) events around the dominant kernel of each step
@@ -256,12 +259,14 @@ def make_step(gfp, cfg, reps, world, group, stream):
             gfp.dot_ex(a, b, p, rep, strategy=cfg["strategy"], out=out, stream=stream)
         elif world == 1:
             gfp.dot(a, b, p, rep, out=out, stream=stream)
+        elif xchg is not None:
+            gfp_dist.dot_fused(a, b, p, rep, xchg, out=out, stream=stream)
         else:
             gfp.dot_partial(a, b, p, rep, out=partial, stream=stream)
         if record:
             e.record(stream)
             ev.append((s, e))
-        if world > 1:
+        if world > 1 and xchg is None:
             gfp_dist.combine_partials(partial, group)  # one all_reduce(SUM) of 8 bytes over NCCL
             gfp.finalize(partial, p, rep, a.dtype, out=out, stream=stream)
     return step, ev, out
@@ -360,6 +365,8 @@ def main():
     ap.add_argument("--no-secondary", action="store_true", help="skip the per-config kernel table")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--combine", default="fused", choices=["fused", "nccl"],
+                    help="N > 1 single dots: one fused kernel per rank (peer-memory exchange) or partial + NCCL")
     ap.add_argument("--oracle-budget", type=float, default=12.0, help="seconds of oracle work per sample")
     ap.add_argument("--sweep", default=None, metavar="OUT.jsonl",
                     help="SURVEY 8(f) F1: paper-shaped prime sweep of DIM=512 batched dots per strategy, "
@@ -397,14 +404,19 @@ def main():
         local_bytes = local_terms * cfg["bpt"]
     total_terms = cfg["rows"] * cfg["n"] if cfg["kind"] == "batch" else cfg["n"]
     reps = replicas(d, local_bytes)
-    step, ev, out = make_step(gfp, cfg, reps, world, group, stream)
+    xchg = None
+    if world > 1 and cfg["kind"] == "dot" and args.combine == "fused":
+        from paper_cs_0404008_b200 import dist as gfp_dist
+        xchg = gfp_dist.PeerExchange(group)
+    step, ev, out = make_step(gfp, cfg, reps, world, group, stream, xchg)
 
     with torch.cuda.stream(stream):
         gfp.launch_count(reset=True)
         with ClockSampler(local) as clk:
             ms = time_steps(step, stream, args.steps, args.warmup, world)
         launches_total = gfp.launch_count()
-    launches_timed = launches_total - args.warmup * (1 if world == 1 or cfg["kind"] == "batch" else 2)
+    per_step = 1 if (world == 1 or cfg["kind"] == "batch" or xchg is not None) else 2
+    launches_timed = launches_total - args.warmup * per_step
     kern_ms = [s.elapsed_time(e) for s, e in ev[-args.steps:]]
     kern_avg = statistics.mean(kern_ms)
     ms_max = max_over_ranks(ms, world)
@@ -418,6 +430,15 @@ def main():
             "peak_source": peak_src, "spec_8TBps_frac": round(achieved / 8000.0, 4)}
 
     # ---------------------------------------------------------------- correctness of the timed result
+    combine_check = None
+    if world > 1 and cfg["kind"] == "dot":  # the timed combine's result vs the NCCL path, every rank
+        from paper_cs_0404008_b200 import dist as gfp_dist
+        with torch.cuda.stream(stream):
+            ref = gfp_dist.dot(reps[0]["a"], reps[0]["b"], cfg["p"], cfg["rep"], group=group, stream=stream)
+            if xchg is not None:
+                got = gfp_dist.dot_fused(reps[0]["a"], reps[0]["b"], cfg["p"], cfg["rep"], xchg, stream=stream)
+        torch.cuda.synchronize()
+        combine_check = bool(torch.equal(got.cpu(), ref.cpu())) if xchg is not None else None
     parity = None
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -456,17 +477,22 @@ def main():
             "vs_baseline": None, "dtype": DTYPE_NAMES[np.dtype(cfg["dtype"])], "data": "synthetic",
             "config": {"workload": cfg["workload"], "p": cfg["p"], "representation": REP_NAMES[cfg["rep"]],
                        "n_total": total_terms, "terms_per_rank": local_terms,
-                       "parallelism": f"shard x{world}" + (" + NCCL all_reduce(int64)" if world > 1 and
-                                                           cfg["kind"] == "dot" else ""),
+                       "parallelism": f"shard x{world}" + ((" + fused peer-memory combine (1 launch)" if xchg is not None
+                                                            else " + NCCL all_reduce(int64)")
+                                                           if world > 1 and cfg["kind"] == "dot" else ""),
                        "l2": "inputs larger than L2: %.0f MiB per rank x %d rotating copies vs 126 MB L2"
                              % (local_bytes / 2 ** 20, len(reps)),
                        "seed": synth.BASE_SEED + cfg.get("inputs_of", args.config)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_timed,
             "clocks": clk.summary(), "parity_vs_oracle": parity, "phases": phases,
+            "combine_equals_nccl_path": combine_check,
             "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
+    if xchg is not None:
+        torch.cuda.synchronize()
+        xchg.close()
     if world > 1:
         dist.destroy_process_group()
 

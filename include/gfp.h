@@ -203,6 +203,45 @@ gfp_status gfp_dot_partial(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a,
 gfp_status gfp_finalize(uint64_t p, gfp_rep rep, gfp_dtype dt, const uint64_t *summed, void *out,
                         void *stream);
 
+/* ---- Fused multi-GPU dot (SURVEY 8(e) "fused variant"): ONE kernel per rank
+ * computes the rank's shard, and its last CTA exchanges the shard's partial with every peer over peer
+ * memory (NVLink / NVSwitch stores) and finalizes -- no NCCL launch on the data path.
+ *
+ * Setup, once per process group: each rank creates an exchange buffer (gfp_xchg_create: device memory of
+ * gfp_xchg_bytes() bytes, zeroed, owned by the library, plus its 64-byte CUDA IPC handle); the caller
+ * passes the handles to every rank over any host channel (e.g. torch.distributed.all_gather_object);
+ * each rank maps its peers' buffers with gfp_xchg_open (its own buffer is used directly) and fills a
+ * gfp_xchg {rank, world, peers[r] = rank r's buffer as mapped in this process}.
+ *
+ * Protocol (all ranks call gfp_dot_allreduce in the same order -- the usual collective contract; the
+ * state lives in device memory, so calls may be captured in CUDA graphs): the calling rank's epoch e is
+ * its buffer's counter + 1; the last CTA stores its partial residue (additive form, as gfp_dot_partial)
+ * into slot [e mod 2][rank] of every peer's buffer, then publishes flag [e mod 2][rank] = e on every peer
+ * with a system-scope release; it waits (system-scope acquire) until its own flags [e mod 2][r] >= e for
+ * every r, sums the slots, reduces mod p, encodes out[0] and stores e.  Two slot sets suffice: a rank
+ * can only write epoch e + 2's slots after every rank published epoch e + 1, i.e. after every rank has
+ * read epoch e's.  A peer that never arrives makes the kernel trap after about 30 s (the error surfaces
+ * at the next synchronisation) instead of hanging.  Every rank receives the same out[0]. */
+#define GFP_XCHG_MAX_WORLD 16
+typedef struct {
+    int32_t rank, world;              /* 1 <= world <= GFP_XCHG_MAX_WORLD, 0 <= rank < world */
+    void *peers[GFP_XCHG_MAX_WORLD];  /* peers[r]: rank r's exchange buffer (device pointer valid here) */
+} gfp_xchg;
+
+uint64_t gfp_xchg_bytes(void);
+/* host: allocate + zero this rank's exchange buffer on the current device; *buf = device pointer,
+ * ipc_handle (64 bytes, caller-provided) receives its CUDA IPC handle. */
+gfp_status gfp_xchg_create(void **buf, void *ipc_handle);
+/* host: map a peer's buffer from its 64-byte handle (GFP_E_CUDA if the devices cannot peer). */
+gfp_status gfp_xchg_open(const void *ipc_handle, void **peer_buf);
+gfp_status gfp_xchg_close(void *peer_buf);  /* unmap a gfp_xchg_open mapping */
+gfp_status gfp_xchg_destroy(void *buf);     /* free a gfp_xchg_create buffer (after every peer closed it) */
+/* The whole-group dot: a, b are this rank's shards (n may differ across ranks, may be 0); out[0] (device,
+ * one element of dt) receives sum over all ranks' shards of a_i b_i in GF(p), in the representation.  One
+ * launch; the default (AUTO) accumulation plan. */
+gfp_status gfp_dot_allreduce(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
+                             const gfp_xchg *x, void *out, void *stream);
+
 /* gfp_dot / gfp_dot_batch with explicit options (NULL = defaults): the paper's strategies side by
  * side, exact in every admissible combination.  Same pointers, streams and errors as gfp_dot. */
 gfp_status gfp_dot_ex(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,

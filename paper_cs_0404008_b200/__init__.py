@@ -72,6 +72,14 @@ class GfpTuneEntry(ctypes.Structure):
                 ("us_best", ctypes.c_double), ("us_builtin", ctypes.c_double)]
 
 
+XCHG_MAX_WORLD = 16
+
+
+class GfpXchg(ctypes.Structure):
+    """gfp_xchg: this rank, the group size and every rank's exchange buffer as mapped in this process."""
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("peers", ctypes.c_void_p * XCHG_MAX_WORLD)]
+
+
 lib = ctypes.CDLL(_LIB_PATH)
 _u64, _i64, _int, _vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
 _SIGS = {
@@ -91,10 +99,17 @@ _SIGS = {
     "gfp_tune_set": [ctypes.POINTER(GfpTuneEntry), ctypes.c_int32],
     "gfp_tune_save": [ctypes.c_char_p],
     "gfp_tune_load": [ctypes.c_char_p],
+    "gfp_xchg_create": [ctypes.POINTER(_vp), _vp],
+    "gfp_xchg_open": [_vp, ctypes.POINTER(_vp)],
+    "gfp_xchg_close": [_vp],
+    "gfp_xchg_destroy": [_vp],
+    "gfp_dot_allreduce": [_u64, _int, _int, _vp, _vp, _i64, ctypes.POINTER(GfpXchg), _vp, _vp],
 }
 for _name, _args in _SIGS.items():
     getattr(lib, _name).argtypes = _args
     getattr(lib, _name).restype = _int
+lib.gfp_xchg_bytes.argtypes = []
+lib.gfp_xchg_bytes.restype = _u64
 lib.gfp_tune_clear.argtypes = []
 lib.gfp_tune_clear.restype = None
 lib.gfp_launch_count.argtypes = [_int]
@@ -395,3 +410,41 @@ def tune_load(path: str) -> None:
 
 def tune_clear() -> None:
     lib.gfp_tune_clear()
+
+
+# ------------------------------------------------------------------------------ fused multi-GPU combine
+def xchg_create() -> tuple[int, bytes]:
+    """This rank's exchange buffer on the current device: (device pointer, 64-byte CUDA IPC handle)."""
+    buf = ctypes.c_void_p()
+    handle = ctypes.create_string_buffer(64)
+    _check(lib.gfp_xchg_create(ctypes.byref(buf), handle))
+    return int(buf.value), bytes(handle.raw)
+
+
+def xchg_open(handle: bytes) -> int:
+    ptr = ctypes.c_void_p()
+    _check(lib.gfp_xchg_open(ctypes.create_string_buffer(handle, 64), ctypes.byref(ptr)))
+    return int(ptr.value)
+
+
+def xchg_close(ptr: int) -> None:
+    _check(lib.gfp_xchg_close(ptr))
+
+
+def xchg_destroy(ptr: int) -> None:
+    _check(lib.gfp_xchg_destroy(ptr))
+
+
+def dot_allreduce(a: torch.Tensor, b: torch.Tensor, p: int, rep: int, xchg: GfpXchg,
+                  out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Whole-group dot of the sharded vectors in ONE launch per rank (gfp_dot_allreduce): the kernel's
+    last CTA exchanges the shard partial with every peer over NVLink peer memory and encodes the result."""
+    a, b = _flat_cuda(a, "a"), _flat_cuda(b, "b")
+    if a.numel() != b.numel() or a.dtype != b.dtype:
+        raise ValueError("a and b must have the same length and dtype")
+    if out is None:
+        out = torch.empty(1, dtype=a.dtype, device=a.device)
+    with torch.cuda.device(a.device):
+        _check(lib.gfp_dot_allreduce(p, rep, _dt(a, rep), a.data_ptr(), b.data_ptr(), a.numel(), ctypes.byref(xchg),
+                                     out.data_ptr(), _stream(a, stream)))
+    return out

@@ -191,8 +191,8 @@ gfp_status plan_fail(gfp_status st) {
 }
 
 gfp_status dot_common(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n, void *out,
-                      int mode, cudaStream_t s, const gfp_options *opt = nullptr) {
-    gfp_status st = check_dot_args(dt, a, b, n, out, mode == OUT_ENCODE ? dtype_size(dt) : 8);
+                      int mode, cudaStream_t s, const gfp_options *opt = nullptr, const XchgSpec *x = nullptr) {
+    gfp_status st = check_dot_args(dt, a, b, n, out, (mode == OUT_ENCODE || mode == OUT_XCHG) ? dtype_size(dt) : 8);
     if (st != GFP_OK) return st;
     Ctx *c;
     if ((st = get_ctx(p, rep, dt, &c)) != GFP_OK) return st;
@@ -201,6 +201,7 @@ gfp_status dot_common(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, cons
     DotPlan plan;
     if ((st = plan_dot(c->info, c->K, a, b, n, opt, &plan)) != GFP_OK) return plan_fail(st);
     OutSpec o{out, (int)rep, (int)dt, mode};
+    if (x != nullptr) o.x = *x;
     cudaError_t e = launch_dot(plan, c->K, a, b, n, ws, o, s);
     return e == cudaSuccess ? GFP_OK : cuda_fail(e, "dot launch");
 }
@@ -231,6 +232,67 @@ gfp_status gfp_dot(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const v
 gfp_status gfp_dot_partial(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
                            uint64_t *partial, void *stream) {
     return dot_common(p, rep, dt, a, b, n, partial, OUT_PARTIAL, (cudaStream_t)stream);
+}
+
+uint64_t gfp_xchg_bytes(void) { return (uint64_t)kXWords * sizeof(uint64_t); }
+
+gfp_status gfp_xchg_create(void **buf, void *ipc_handle) {
+    if (buf == nullptr || ipc_handle == nullptr) return fail(GFP_E_INVAL, "gfp_xchg_create: NULL argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handles are 64 bytes");
+    void *d = nullptr;
+    cudaError_t e = cudaMalloc(&d, gfp_xchg_bytes());
+    if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? fail(GFP_E_NOMEM, "exchange buffer") : cuda_fail(e, "exchange buffer");
+    cudaIpcMemHandle_t h;
+    if ((e = cudaMemset(d, 0, gfp_xchg_bytes())) != cudaSuccess || (e = cudaIpcGetMemHandle(&h, d)) != cudaSuccess) {
+        cudaFree(d);
+        return cuda_fail(e, "gfp_xchg_create");
+    }
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) {
+        cudaFree(d);
+        return cuda_fail(e, "gfp_xchg_create");
+    }
+    memcpy(ipc_handle, &h, sizeof h);
+    *buf = d;
+    return GFP_OK;
+}
+
+gfp_status gfp_xchg_open(const void *ipc_handle, void **peer_buf) {
+    if (ipc_handle == nullptr || peer_buf == nullptr) return fail(GFP_E_INVAL, "gfp_xchg_open: NULL argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handle, sizeof h);
+    void *d = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&d, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "gfp_xchg_open (peer access over NVLink / PCIe required)");
+    *peer_buf = d;
+    return GFP_OK;
+}
+
+gfp_status gfp_xchg_close(void *peer_buf) {
+    if (peer_buf == nullptr) return fail(GFP_E_INVAL, "gfp_xchg_close: NULL");
+    cudaError_t e = cudaIpcCloseMemHandle(peer_buf);
+    return e == cudaSuccess ? GFP_OK : cuda_fail(e, "gfp_xchg_close");
+}
+
+gfp_status gfp_xchg_destroy(void *buf) {
+    if (buf == nullptr) return fail(GFP_E_INVAL, "gfp_xchg_destroy: NULL");
+    cudaError_t e = cudaFree(buf);
+    return e == cudaSuccess ? GFP_OK : cuda_fail(e, "gfp_xchg_destroy");
+}
+
+gfp_status gfp_dot_allreduce(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
+                             const gfp_xchg *x, void *out, void *stream) {
+    if (x == nullptr) return fail(GFP_E_INVAL, "gfp_dot_allreduce: x is NULL");
+    if (x->world < 1 || x->world > GFP_XCHG_MAX_WORLD || x->rank < 0 || x->rank >= x->world)
+        return fail(GFP_E_INVAL, "gfp_dot_allreduce: need 1 <= world <= 16 and 0 <= rank < world");
+    XchgSpec xs;
+    xs.rank = x->rank;
+    xs.world = x->world;
+    for (int r = 0; r < GFP_XCHG_MAX_WORLD; ++r) {
+        xs.peers[r] = r < x->world ? (uint64_t *)x->peers[r] : nullptr;
+        if (r < x->world && (x->peers[r] == nullptr || !aligned(x->peers[r], 8)))
+            return fail(GFP_E_INVAL, "gfp_dot_allreduce: peers[r] must be an 8-byte aligned exchange buffer");
+    }
+    return dot_common(p, rep, dt, a, b, n, out, OUT_XCHG, (cudaStream_t)stream, nullptr, &xs);
 }
 
 gfp_status gfp_finalize(uint64_t p, gfp_rep rep, gfp_dtype dt, const uint64_t *summed, void *out, void *stream) {

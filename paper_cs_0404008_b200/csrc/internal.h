@@ -15,12 +15,21 @@ struct Workspace {
     unsigned int *counter;
 };
 
-// Where the final residue goes.
-enum OutMode { OUT_ENCODE = 0, OUT_PARTIAL = 1, OUT_ACCUMULATE = 2 };
-struct OutSpec {
-    void *out;          // OUT_ENCODE: element of (rep, dtype); else uint64_t*
-    int rep, dtype, mode;
+// Where the final residue goes.  OUT_XCHG: exchange with the peers of `x` first (fused multi-GPU
+// combine, gfp_dot_allreduce), then encode like OUT_ENCODE.
+enum OutMode { OUT_ENCODE = 0, OUT_PARTIAL = 1, OUT_ACCUMULATE = 2, OUT_XCHG = 3 };
+struct XchgSpec {
+    int rank, world;
+    uint64_t *peers[GFP_XCHG_MAX_WORLD];
 };
+struct OutSpec {
+    void *out;          // OUT_ENCODE / OUT_XCHG: element of (rep, dtype); else uint64_t*
+    int rep, dtype, mode;
+    XchgSpec x;         // OUT_XCHG only
+};
+// Exchange-buffer layout (u64 words): [0] this rank's epoch; flags at kXFlags + parity * MAXW + r;
+// partial slots at kXSlots + parity * MAXW + r.
+constexpr int kXFlags = 8, kXSlots = 8 + 2 * GFP_XCHG_MAX_WORLD, kXWords = 8 + 4 * GFP_XCHG_MAX_WORLD;
 
 constexpr int kMaxGrid = 4096;
 

@@ -95,6 +95,46 @@ __device__ __forceinline__ void write_result(uint64_t r, const OutSpec &O, const
     }
 }
 
+// ------------------------------------------------------------------------------ fused multi-GPU combine
+// gfp_dot_allreduce (gfp.h protocol): called by ONE thread of the last CTA with this rank's partial residue
+// r (additive form, < p); returns the residue of the sum over all ranks.  Peer buffers are other GPUs'
+// memory mapped over NVLink (CUDA IPC): system-scope release/acquire orders the slot stores before the
+// flag that publishes them.
+__device__ __forceinline__ uint64_t xchg_allreduce(uint64_t r, const XchgSpec *X, uint64_t p, uint64_t mu) {
+    uint64_t *own = X->peers[X->rank];
+    const uint64_t e = own[0] + 1;  // this rank's epoch: only this rank's kernels touch word 0, in stream order
+    const int par = (int)(e & 1);
+    for (int q = 0; q < X->world; ++q) {
+        uint64_t *slot = X->peers[q] + kXSlots + par * GFP_XCHG_MAX_WORLD + X->rank;
+        asm volatile("st.relaxed.sys.u64 [%0], %1;" ::"l"(slot), "l"(r) : "memory");
+    }
+    for (int q = 0; q < X->world; ++q) {
+        uint64_t *flag = X->peers[q] + kXFlags + par * GFP_XCHG_MAX_WORLD + X->rank;
+        asm volatile("st.release.sys.u64 [%0], %1;" ::"l"(flag), "l"(e) : "memory");
+    }
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    uint64_t sum = 0;
+    for (int q = 0; q < X->world; ++q) {
+        const uint64_t *flag = own + kXFlags + par * GFP_XCHG_MAX_WORLD + q;
+        for (;;) {
+            uint64_t f;
+            asm volatile("ld.acquire.sys.u64 %0, [%1];" : "=l"(f) : "l"(flag) : "memory");
+            if (f >= e) break;
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 30000000000ull) __trap();  // a peer never arrived: fail loudly, do not hang
+            __nanosleep(64);
+        }
+        uint64_t v;
+        asm volatile("ld.relaxed.sys.u64 %0, [%1];" : "=l"(v) : "l"(own + kXSlots + par * GFP_XCHG_MAX_WORLD + q)
+                     : "memory");
+        sum += v;  // world <= 16 residues < 2^32: no wrap
+    }
+    own[0] = e;
+    return mod_p(sum, p, mu);
+}
+
 // Stage a u16 table (entries padded to a multiple of 8) from global into shared memory.
 __device__ __forceinline__ void stage_table(uint16_t *dst, const uint16_t *src, uint32_t entries) {
     const uint4 *s = reinterpret_cast<const uint4 *>(src);
@@ -198,7 +238,9 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
             unsigned long long s;
             asm volatile("ld.relaxed.gpu.u64 %0, [%1];" : "=l"(s) : "l"(sum) : "memory");
             // centered sums are signed (two's complement, |total| < 2^63 by the host's bound)
-            write_result(O.rep == GFP_REP_CENTERED ? smod_p((int64_t)s, K) : mod_p(s, K.p, K.mu), O, K, 0);
+            uint64_t r = O.rep == GFP_REP_CENTERED ? smod_p((int64_t)s, K) : mod_p(s, K.p, K.mu);
+            if (O.mode == OUT_XCHG) r = xchg_allreduce(r, &O.x, K.p, K.mu);  // fused multi-GPU combine
+            write_result(r, O, K, 0);
             *sum = 0;  // self-reset for the next launch on this stream
             *ws.counter = 0;
         }

@@ -7,6 +7,11 @@ encodes (one tiny kernel).  Partials are residues < p < 2^32 in the representati
 (classical value, Montgomery form -- the representation is linear --, fp64 integer, Zech classical value),
 so the int64 sum of up to 2^31 ranks cannot overflow.
 
+Fused variant: `PeerExchange` maps every rank's small exchange buffer into every process
+(CUDA IPC over NVLink; handles exchanged once with all_gather_object), and `dot_fused` runs ONE kernel per
+rank whose last CTA stores the shard partial into every peer's buffer, waits for all peers' partials and
+finalizes (gfp_dot_allreduce) -- no NCCL launch, no separate finalize.
+
 Batch (matrix-vector): rows are independent, so rank g owns a contiguous row block and there is no
 collective on the data path ("weak" in the sense of no exchange); the output stays sharded unless
 gather=True asks for an all_gather.
@@ -16,6 +21,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
+from . import dot_allreduce as _dot_allreduce
 from . import dot_batch as _dot_batch
 from . import dot_partial as _dot_partial
 from . import finalize as _finalize
@@ -35,6 +41,86 @@ def combine_partials(partial: torch.Tensor, group=None) -> torch.Tensor:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
     return partial
+
+
+class _LibXchg:
+    """The library's exchange-buffer calls (the default backend of PeerExchange)."""
+
+    @staticmethod
+    def create():
+        from . import xchg_create
+        return xchg_create()
+
+    @staticmethod
+    def open(handle):
+        from . import xchg_open
+        return xchg_open(handle)
+
+    @staticmethod
+    def close(ptr):
+        from . import xchg_close
+        xchg_close(ptr)
+
+    @staticmethod
+    def destroy(ptr):
+        from . import xchg_destroy
+        xchg_destroy(ptr)
+
+
+class PeerExchange:
+    """Exchange buffers of a process group for the fused combine: this rank creates one, the IPC handles
+    are all-gathered (host objects), every peer's buffer is mapped here, and `spec` is the gfp_xchg the
+    kernel needs (peers in rank order, this rank's own pointer at its own index).  `backend` provides
+    create() -> (ptr, handle), open(handle) -> ptr, close(ptr), destroy(ptr) (injectable for tests)."""
+
+    def __init__(self, group=None, backend=None):
+        from . import XCHG_MAX_WORLD, GfpXchg
+        self.backend = backend or _LibXchg
+        init = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if init else 1
+        self.rank = dist.get_rank(group) if init else 0
+        if self.world > XCHG_MAX_WORLD:
+            raise ValueError(f"the fused combine supports up to {XCHG_MAX_WORLD} ranks")
+        self.own, handle = self.backend.create()
+        handles = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(handles, (self.rank, handle), group=group)
+        else:
+            handles = [(0, handle)]
+        if [r for r, _ in handles] != list(range(self.world)):
+            raise RuntimeError("exchange handles arrived out of rank order")
+        self.ptrs = []
+        self.opened = []
+        for r, h in handles:
+            if r == self.rank:
+                self.ptrs.append(self.own)
+            else:
+                ptr = self.backend.open(h)
+                self.ptrs.append(ptr)
+                self.opened.append(ptr)
+        self.spec = GfpXchg()
+        self.spec.rank, self.spec.world = self.rank, self.world
+        for r, ptr in enumerate(self.ptrs):
+            self.spec.peers[r] = ptr
+        self.group = group
+
+    def close(self):
+        """Unmap the peers' buffers, wait for every rank to have done the same, free this rank's buffer."""
+        for ptr in self.opened:
+            self.backend.close(ptr)
+        self.opened = []
+        if self.world > 1:
+            dist.barrier(group=self.group)
+        if self.own is not None:
+            self.backend.destroy(self.own)
+            self.own = None
+
+
+def dot_fused(a_shard: torch.Tensor, b_shard: torch.Tensor, p: int, rep: int, xchg: PeerExchange,
+              out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Exact dot of the globally sharded vectors in ONE kernel launch per rank (compute + exchange +
+    finalize); every rank receives the result (device, 1 element)."""
+    return _dot_allreduce(a_shard, b_shard, p, rep, xchg.spec, out=out, stream=stream)
 
 
 def dot(a_shard: torch.Tensor, b_shard: torch.Tensor, p: int, rep: int, group=None,

@@ -478,3 +478,55 @@ def test_batch_many_rows_closed_form():
     x = _full(n, p - 1, torch.uint16)
     out = gfp.dot_batch(A, x, p, CL)
     assert bool((out.to(torch.int32) == n % p).all())
+
+
+# ------------------------------------------------------------------------------ fused combine (world 1)
+def test_fused_allreduce_single_rank():
+    """gfp_dot_allreduce on a one-rank group (the only group one GPU can host): the whole exchange protocol
+    runs against the rank's own buffer; repeated calls advance the epoch, CUDA-graph replays reuse the
+    device-resident state, and every representation matches the plain dot."""
+    from paper_cs_0404008_b200 import dist as gd
+    x = gd.PeerExchange()
+    try:
+        for p, rep, dt, gen in [(65521, gfp.CLASSICAL, np.uint32, "u"), (2 ** 31 - 1, gfp.MONTGOMERY, np.uint32, "u"),
+                                (67108859, gfp.FP64, np.float64, "u"), (32749, gfp.ZECH, np.uint16, "z")]:
+            for n in [0, 1, 1000, 1_000_003]:
+                if gen == "z":
+                    a, b = synth.zech_codes(SEED, 0, 0, n, p - 1), synth.zech_codes(SEED, 1, 0, n, p - 1)
+                else:
+                    a, b = synth.uniform(SEED, 0, 0, n, p, dt), synth.uniform(SEED, 1, 0, n, p, dt)
+                ga, gb = cu(a), cu(b)
+                want = gfp.dot(ga, gb, p, rep).cpu()
+                for _ in range(3):
+                    got = gd.dot_fused(ga, gb, p, rep, x).cpu()
+                    assert torch.equal(got, want), (p, rep, n)
+        p, n = 2 ** 31 - 1, 1 << 20
+        a, b = cu(synth.uniform(SEED, 0, 0, n, p, np.uint32)), cu(synth.uniform(SEED, 1, 0, n, p, np.uint32))
+        want = int(gfp.dot(a, b, p, gfp.CLASSICAL).cpu().to(torch.int64)[0])
+        out = torch.empty(1, dtype=torch.uint32, device=DEV)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            gd.dot_fused(a, b, p, gfp.CLASSICAL, x, out=out, stream=s)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                gd.dot_fused(a, b, p, gfp.CLASSICAL, x, out=out, stream=s)
+        for _ in range(10):
+            out.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert int(out.cpu().to(torch.int64)[0]) == want
+    finally:
+        torch.cuda.synchronize()
+        x.close()
+
+
+def test_fused_allreduce_rejects_bad_groups():
+    xs = gfp.GfpXchg()
+    xs.rank, xs.world = 0, 0
+    a = cu(np.ones(4, np.uint32))
+    with pytest.raises(gfp.GfpError):
+        gfp.dot_allreduce(a, a, 65521, gfp.CLASSICAL, xs)
+    xs.world, xs.rank = 2, 0
+    xs.peers[0] = 0
+    with pytest.raises(gfp.GfpError):
+        gfp.dot_allreduce(a, a, 65521, gfp.CLASSICAL, xs)
