@@ -191,7 +191,7 @@ gfp_status plan_fail(gfp_status st) {
 }
 
 gfp_status dot_common(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n, void *out,
-                      int mode, cudaStream_t s, const gfp_options *opt = nullptr, const XchgSpec *x = nullptr) {
+                      int mode, cudaStream_t s, const gfp_options *opt = nullptr, uint64_t *xchg = nullptr) {
     gfp_status st = check_dot_args(dt, a, b, n, out, (mode == OUT_ENCODE || mode == OUT_XCHG) ? dtype_size(dt) : 8);
     if (st != GFP_OK) return st;
     Ctx *c;
@@ -200,8 +200,7 @@ gfp_status dot_common(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, cons
     if ((st = get_ws(s, &ws)) != GFP_OK) return st;
     DotPlan plan;
     if ((st = plan_dot(c->info, c->K, a, b, n, opt, &plan)) != GFP_OK) return plan_fail(st);
-    OutSpec o{out, (int)rep, (int)dt, mode};
-    if (x != nullptr) o.x = *x;
+    OutSpec o{out, (int)rep, (int)dt, mode, xchg};
     cudaError_t e = launch_dot(plan, c->K, a, b, n, ws, o, s);
     return e == cudaSuccess ? GFP_OK : cuda_fail(e, "dot launch");
 }
@@ -236,6 +235,17 @@ gfp_status gfp_dot_partial(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a,
 
 uint64_t gfp_xchg_bytes(void) { return (uint64_t)kXWords * sizeof(uint64_t); }
 
+}  // extern "C"
+namespace {
+std::mutex g_xmu;
+std::map<uint64_t *, std::vector<uint64_t>> g_xdesc;  // group description last written into each own buffer
+void forget_xchg(void *buf) {
+    std::lock_guard<std::mutex> g(g_xmu);
+    g_xdesc.erase((uint64_t *)buf);
+}
+}  // namespace
+extern "C" {
+
 gfp_status gfp_xchg_create(void **buf, void *ipc_handle) {
     if (buf == nullptr || ipc_handle == nullptr) return fail(GFP_E_INVAL, "gfp_xchg_create: NULL argument");
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handles are 64 bytes");
@@ -252,6 +262,7 @@ gfp_status gfp_xchg_create(void **buf, void *ipc_handle) {
         return cuda_fail(e, "gfp_xchg_create");
     }
     memcpy(ipc_handle, &h, sizeof h);
+    forget_xchg(d);  // a recycled address carries no description
     *buf = d;
     return GFP_OK;
 }
@@ -275,6 +286,7 @@ gfp_status gfp_xchg_close(void *peer_buf) {
 
 gfp_status gfp_xchg_destroy(void *buf) {
     if (buf == nullptr) return fail(GFP_E_INVAL, "gfp_xchg_destroy: NULL");
+    forget_xchg(buf);
     cudaError_t e = cudaFree(buf);
     return e == cudaSuccess ? GFP_OK : cuda_fail(e, "gfp_xchg_destroy");
 }
@@ -284,15 +296,26 @@ gfp_status gfp_dot_allreduce(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *
     if (x == nullptr) return fail(GFP_E_INVAL, "gfp_dot_allreduce: x is NULL");
     if (x->world < 1 || x->world > GFP_XCHG_MAX_WORLD || x->rank < 0 || x->rank >= x->world)
         return fail(GFP_E_INVAL, "gfp_dot_allreduce: need 1 <= world <= 16 and 0 <= rank < world");
-    XchgSpec xs;
-    xs.rank = x->rank;
-    xs.world = x->world;
-    for (int r = 0; r < GFP_XCHG_MAX_WORLD; ++r) {
-        xs.peers[r] = r < x->world ? (uint64_t *)x->peers[r] : nullptr;
-        if (r < x->world && (x->peers[r] == nullptr || !aligned(x->peers[r], 8)))
+    for (int r = 0; r < x->world; ++r)
+        if (x->peers[r] == nullptr || !aligned(x->peers[r], 8))
             return fail(GFP_E_INVAL, "gfp_dot_allreduce: peers[r] must be an 8-byte aligned exchange buffer");
+    // rank, world and the peer table live in this rank's own buffer (one kernel pointer parameter); a tiny
+    // kernel writes them, stream-ordered before the dot, whenever this buffer's group description changes
+    uint64_t *own = (uint64_t *)x->peers[x->rank];
+    std::vector<uint64_t> desc(2 + GFP_XCHG_MAX_WORLD, 0);
+    desc[0] = (uint64_t)x->rank;
+    desc[1] = (uint64_t)x->world;
+    for (int r = 0; r < x->world; ++r) desc[2 + r] = (uint64_t)(uintptr_t)x->peers[r];
+    {
+        std::lock_guard<std::mutex> g(g_xmu);
+        auto it = g_xdesc.find(own);
+        if (it == g_xdesc.end() || it->second != desc) {
+            cudaError_t e = launch_xchg_setup(own, x->rank, x->world, (uint64_t *const *)x->peers, (cudaStream_t)stream);
+            if (e != cudaSuccess) return cuda_fail(e, "gfp_dot_allreduce: group description");
+            g_xdesc[own] = desc;
+        }
     }
-    return dot_common(p, rep, dt, a, b, n, out, OUT_XCHG, (cudaStream_t)stream, nullptr, &xs);
+    return dot_common(p, rep, dt, a, b, n, out, OUT_XCHG, (cudaStream_t)stream, nullptr, own);
 }
 
 gfp_status gfp_finalize(uint64_t p, gfp_rep rep, gfp_dtype dt, const uint64_t *summed, void *out, void *stream) {

@@ -15,21 +15,19 @@ struct Workspace {
     unsigned int *counter;
 };
 
-// Where the final residue goes.  OUT_XCHG: exchange with the peers of `x` first (fused multi-GPU
+// Where the final residue goes.  OUT_XCHG: exchange with the group's peers first (fused multi-GPU
 // combine, gfp_dot_allreduce), then encode like OUT_ENCODE.
 enum OutMode { OUT_ENCODE = 0, OUT_PARTIAL = 1, OUT_ACCUMULATE = 2, OUT_XCHG = 3 };
-struct XchgSpec {
-    int rank, world;
-    uint64_t *peers[GFP_XCHG_MAX_WORLD];
-};
 struct OutSpec {
     void *out;          // OUT_ENCODE / OUT_XCHG: element of (rep, dtype); else uint64_t*
     int rep, dtype, mode;
-    XchgSpec x;         // OUT_XCHG only
+    uint64_t *xchg;     // OUT_XCHG: this rank's exchange buffer (it holds rank, world and the peer table)
 };
-// Exchange-buffer layout (u64 words): [0] this rank's epoch; flags at kXFlags + parity * MAXW + r;
-// partial slots at kXSlots + parity * MAXW + r.
-constexpr int kXFlags = 8, kXSlots = 8 + 2 * GFP_XCHG_MAX_WORLD, kXWords = 8 + 4 * GFP_XCHG_MAX_WORLD;
+// Exchange-buffer layout (u64 words): [0] this rank's epoch, [1] rank, [2] world; flags at
+// kXFlags + parity * MAXW + r; partial slots at kXSlots + parity * MAXW + r; the peer table (every rank's
+// buffer as mapped in this process) at kXPeers + r.  Kernel parameters stay small: one pointer.
+constexpr int kXFlags = 8, kXSlots = 8 + 2 * GFP_XCHG_MAX_WORLD, kXPeers = 8 + 4 * GFP_XCHG_MAX_WORLD,
+              kXWords = 8 + 5 * GFP_XCHG_MAX_WORLD;
 
 constexpr int kMaxGrid = 4096;
 
@@ -62,6 +60,8 @@ gfp_status launch_convert(const gfp_info &info, const dev::KParams &K, int dir, 
                           gfp_dtype out_dt, void *out, int64_t n, cudaStream_t s, cudaError_t *err);
 
 int num_sms(int device);
+// Write rank, world and the peer table into an exchange buffer (one thread, stream-ordered).
+cudaError_t launch_xchg_setup(uint64_t *own, int rank, int world, uint64_t *const *peers, cudaStream_t s);
 // Set the thread-local text returned by gfp_last_error (api.cpp).
 void set_last_error(const char *msg);
 

@@ -100,22 +100,23 @@ __device__ __forceinline__ void write_result(uint64_t r, const OutSpec &O, const
 // r (additive form, < p); returns the residue of the sum over all ranks.  Peer buffers are other GPUs'
 // memory mapped over NVLink (CUDA IPC): system-scope release/acquire orders the slot stores before the
 // flag that publishes them.
-__device__ __forceinline__ uint64_t xchg_allreduce(uint64_t r, const XchgSpec *X, uint64_t p, uint64_t mu) {
-    uint64_t *own = X->peers[X->rank];
+__device__ __forceinline__ uint64_t xchg_allreduce(uint64_t r, uint64_t *own, uint64_t p, uint64_t mu) {
     const uint64_t e = own[0] + 1;  // this rank's epoch: only this rank's kernels touch word 0, in stream order
+    const int rank = (int)own[1], world = (int)own[2];
+    uint64_t *const *peers = reinterpret_cast<uint64_t *const *>(own + kXPeers);
     const int par = (int)(e & 1);
-    for (int q = 0; q < X->world; ++q) {
-        uint64_t *slot = X->peers[q] + kXSlots + par * GFP_XCHG_MAX_WORLD + X->rank;
+    for (int q = 0; q < world; ++q) {
+        uint64_t *slot = peers[q] + kXSlots + par * GFP_XCHG_MAX_WORLD + rank;
         asm volatile("st.relaxed.sys.u64 [%0], %1;" ::"l"(slot), "l"(r) : "memory");
     }
-    for (int q = 0; q < X->world; ++q) {
-        uint64_t *flag = X->peers[q] + kXFlags + par * GFP_XCHG_MAX_WORLD + X->rank;
+    for (int q = 0; q < world; ++q) {
+        uint64_t *flag = peers[q] + kXFlags + par * GFP_XCHG_MAX_WORLD + rank;
         asm volatile("st.release.sys.u64 [%0], %1;" ::"l"(flag), "l"(e) : "memory");
     }
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     uint64_t sum = 0;
-    for (int q = 0; q < X->world; ++q) {
+    for (int q = 0; q < world; ++q) {
         const uint64_t *flag = own + kXFlags + par * GFP_XCHG_MAX_WORLD + q;
         for (;;) {
             uint64_t f;
@@ -133,6 +134,23 @@ __device__ __forceinline__ uint64_t xchg_allreduce(uint64_t r, const XchgSpec *X
     }
     own[0] = e;
     return mod_p(sum, p, mu);
+}
+
+struct XchgDesc {
+    uint64_t *peers[GFP_XCHG_MAX_WORLD];
+};
+__global__ void xchg_setup_kernel(uint64_t *own, int rank, int world, XchgDesc d) {
+    own[1] = (uint64_t)rank;
+    own[2] = (uint64_t)world;
+    for (int r = 0; r < GFP_XCHG_MAX_WORLD; ++r) own[kXPeers + r] = r < world ? (uint64_t)(uintptr_t)d.peers[r] : 0;
+}
+
+cudaError_t launch_xchg_setup(uint64_t *own, int rank, int world, uint64_t *const *peers, cudaStream_t s) {
+    XchgDesc d;
+    for (int r = 0; r < GFP_XCHG_MAX_WORLD; ++r) d.peers[r] = r < world ? peers[r] : nullptr;
+    xchg_setup_kernel<<<1, 1, 0, s>>>(own, rank, world, d);
+    count_launch();
+    return cudaGetLastError();
 }
 
 // Stage a u16 table (entries padded to a multiple of 8) from global into shared memory.
@@ -239,7 +257,7 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
             asm volatile("ld.relaxed.gpu.u64 %0, [%1];" : "=l"(s) : "l"(sum) : "memory");
             // centered sums are signed (two's complement, |total| < 2^63 by the host's bound)
             uint64_t r = O.rep == GFP_REP_CENTERED ? smod_p((int64_t)s, K) : mod_p(s, K.p, K.mu);
-            if (O.mode == OUT_XCHG) r = xchg_allreduce(r, &O.x, K.p, K.mu);  // fused multi-GPU combine
+            if (O.mode == OUT_XCHG) r = xchg_allreduce(r, O.xchg, K.p, K.mu);  // fused multi-GPU combine
             write_result(r, O, K, 0);
             *sum = 0;  // self-reset for the next launch on this stream
             *ws.counter = 0;

@@ -59,7 +59,8 @@ def main():
     with open(out, "w") as f:
         f.write("\n".join(lines) + "\n")
     if traffic_key and traffic:
-        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "traffic.json")
+        path = os.environ.get("TRAFFIC_JSON") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "..",
+                                                              "profiles", "traffic.json")
         t = json.load(open(path)) if os.path.exists(path) else {}
         t[traffic_key] = int(sum(traffic) / len(traffic))
         json.dump(t, open(path, "w"), indent=1, sort_keys=True)

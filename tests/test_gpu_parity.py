@@ -530,3 +530,19 @@ def test_fused_allreduce_rejects_bad_groups():
     xs.peers[0] = 0
     with pytest.raises(gfp.GfpError):
         gfp.dot_allreduce(a, a, 65521, gfp.CLASSICAL, xs)
+
+
+def test_fused_allreduce_buffer_reuse():
+    """Exchange buffers created and destroyed repeatedly (recycled addresses) keep a correct group
+    description: each new group writes its own rank / world / peer table before its first dot."""
+    from paper_cs_0404008_b200 import dist as gd
+    p, n = 65521, 100_003
+    a, b = synth.uniform(SEED, 0, 0, n, p, np.uint32), synth.uniform(SEED, 1, 0, n, p, np.uint32)
+    want = oracle.dot_classical(p, a, b)
+    ga, gb = cu(a), cu(b)
+    for _ in range(4):
+        x = gd.PeerExchange()
+        for _ in range(3):
+            assert int(gd.dot_fused(ga, gb, p, gfp.CLASSICAL, x).cpu().to(torch.int64)[0]) == want
+        torch.cuda.synchronize()
+        x.close()
