@@ -276,7 +276,8 @@ gfp_status gfp_dot_host(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, co
  * the same field element(s) (GFP_E_CUDA with a message otherwise: an exactness failure), and records
  * the fastest in the library's tuning table (one entry per case; a re-tuned case replaces its entry).
  * Each candidate is timed with CUDA events over about ms_per_candidate milliseconds (at least 3 calls,
- * after 2 warm-up calls).  Device memory for the inputs is allocated and freed inside the call.
+ * after 2 warm-up calls), rotating through enough input sets that >= 3x the L2 is streamed between two
+ * uses of a set (at most 64 sets / 1 GiB).  Device memory is allocated and freed inside the call.
  *
  * GFP_STRAT_AUTO (gfp_dot, gfp_dot_batch, gfp_dot_partial, gfp_dot_ex / _batch_ex / gfp_plan with a NULL
  * or all-zero gfp_options) then follows the table: among the entries with the call's (rep, dtype, kind)

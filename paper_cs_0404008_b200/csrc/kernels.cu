@@ -555,17 +555,26 @@ __global__ void __launch_bounds__(NT) batch_cl16_kernel(const uint16_t *__restri
 // ------------------------------------------------------------------------------ batch: generic
 // Warp per row with policy R.  x read through the read-only path (L1-resident, reused by every
 // row).  VEC: rows and x are 16-byte aligned (A, lda*sizeof, x) -> 16-byte loads.
-template <class R, int NT, int U, bool VEC, int LPR>
+template <class R, int NT, int U, bool VEC, int LPR, bool XS>
 __global__ void __launch_bounds__(NT) batch_kernel(const typename R::elem *__restrict__ A, int64_t lda,
                                                    const typename R::elem *__restrict__ x, int64_t rows,
                                                    int64_t n, KParams K, OutSpec O) {
     extern __shared__ __align__(16) uint16_t s_tab[];
     const uint16_t *tab = nullptr;
+    const uint32_t tab_bytes = R::kTable ? ((K.antilog_entries * 2 + 15) & ~15u) : 0;
     if constexpr (R::kTable) {
         stage_table(s_tab, K.antilog, K.antilog_entries);
-        __syncthreads();
         tab = s_tab;
     }
+    // XS: x staged once per CTA in shared memory (16-byte vectors; every row reuses it)
+    const uint4 *xs = reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(s_tab) + tab_bytes);
+    if constexpr (XS) {
+        const int64_t nxv = n / R::W;
+        uint4 *d = reinterpret_cast<uint4 *>(reinterpret_cast<char *>(s_tab) + tab_bytes);
+        const uint4 *src = reinterpret_cast<const uint4 *>(x);
+        for (int64_t i = threadIdx.x; i < nxv; i += NT) d[i] = __ldg(src + i);
+    }
+    if constexpr (R::kTable || XS) __syncthreads();
     constexpr int RPW = 32 / LPR;
     const int lane = threadIdx.x & 31, g = lane % LPR;
     const int64_t warp0 = (int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
@@ -579,18 +588,29 @@ __global__ void __launch_bounds__(NT) batch_kernel(const typename R::elem *__res
         if (valid) {
             int64_t done = 0;
             if (VEC) {
+                // U 16-byte loads per lane in flight per chunk; the launcher sizes U so that a short row
+                // is one chunk (its epilogue then costs one round trip per row, not per chunk)
                 const int64_t nvec = n / R::W;
                 const uint4 *av = reinterpret_cast<const uint4 *>(Ar);
-                const uint4 *xv = reinterpret_cast<const uint4 *>(x);
+                const uint4 *xv = XS ? xs : reinterpret_cast<const uint4 *>(x);
                 int64_t v0 = g;
                 for (; v0 + LPR * (U - 1) < nvec; v0 += LPR * U) {
                     uint4 ra[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u) ra[u] = ld_stream(av + v0 + u * LPR);
 #pragma unroll
-                    for (int u = 0; u < U; ++u) R::vec(acc, ra[u], __ldg(xv + v0 + u * LPR), K, tab);
+                    for (int u = 0; u < U; ++u) R::vec(acc, ra[u], XS ? xv[v0 + u * LPR] : __ldg(xv + v0 + u * LPR), K, tab);
                 }
-                for (; v0 < nvec; v0 += LPR) R::vec(acc, ld_stream(av + v0), __ldg(xv + v0), K, tab);
+                if (v0 < nvec) {  // a partial chunk: predicated loads, all still in flight together
+                    uint4 ra[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (v0 + u * LPR < nvec) ra[u] = ld_stream(av + v0 + u * LPR);
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (v0 + u * LPR < nvec)
+                            R::vec(acc, ra[u], XS ? xv[v0 + u * LPR] : __ldg(xv + v0 + u * LPR), K, tab);
+                }
                 done = nvec * R::W;
             }
             for (int64_t j = done + g; j < n; j += LPR) R::term(acc, Ar[j], x[j], K, tab);
@@ -1167,28 +1187,61 @@ cudaError_t launch_finalize(const KParams &K, const uint64_t *summed, int count,
 }
 
 // ------------------------------------------------------------------------------ batch launch
+constexpr size_t kBatchSmemX = 200 * 1024;  // table + staged x, per CTA
+#ifndef GFP_BATCH_U
+#define GFP_BATCH_U 4
+#endif
+constexpr int kBatchU = GFP_BATCH_U;  // 16-byte A vectors in flight per lane (generic batch kernel)
+
 template <class R, int NT, int U, int LPR>
 static cudaError_t launch_batch_lpr(const KParams &K, const void *A, int64_t lda, const void *x, int64_t rows,
-                                   int64_t n, bool vec, OutSpec O, cudaStream_t s) {
+                                   int64_t n, bool vec, int64_t grid, OutSpec O, cudaStream_t s) {
     using E = typename R::elem;
-    const size_t smem = R::kTable ? (size_t)K.antilog_entries * 2 : 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const int64_t rpb = (NT / 32) * (32 / LPR);  // rows per CTA per sweep
-    auto kern = vec ? batch_kernel<R, NT, U, true, LPR> : batch_kernel<R, NT, U, false, LPR>;
-    int bps = occupancy(kern, NT, smem);
-    int64_t grid = std::min<int64_t>((rows + rpb - 1) / rpb, (int64_t)num_sms(dev) * bps);
+    const size_t tab = R::kTable ? (((size_t)K.antilog_entries * 2 + 15) & ~size_t(15)) : 0;
+    const size_t xbytes = (size_t)(n / R::W) * 16;
+    // x in shared memory when it fits beside the table (every row reuses it; L1 is not needed for it)
+    const bool xs = vec && (R::kTable ? tab + xbytes <= kBatchSmemX : xbytes <= 32 * 1024);
+    const size_t smem = tab + (xs ? xbytes : 0);
+    auto kern = vec ? (xs ? batch_kernel<R, NT, U, true, LPR, true> : batch_kernel<R, NT, U, true, LPR, false>)
+                    : batch_kernel<R, NT, U, false, LPR, false>;
+    occupancy(kern, NT, smem);  // sets the shared-memory opt-in
     kern<<<(int)std::max<int64_t>(grid, 1), NT, smem, s>>>((const E *)A, lda, (const E *)x, rows, n, K, O);
     count_launch();
     return cudaGetLastError();
 }
 
-// Lanes per row: a full warp for long rows, 8 lanes (4 rows per warp) when a row has < 256 vectors.
+template <class R, int NT, int U, int LPR>
+static int batch_occupancy(const KParams &K, int64_t n, bool vec) {
+    const size_t tab = R::kTable ? (((size_t)K.antilog_entries * 2 + 15) & ~size_t(15)) : 0;
+    const size_t xbytes = (size_t)(n / R::W) * 16;
+    const bool xs = vec && (R::kTable ? tab + xbytes <= kBatchSmemX : xbytes <= 32 * 1024);
+    const size_t smem = tab + (xs ? xbytes : 0);
+    auto kern = vec ? (xs ? batch_kernel<R, NT, U, true, LPR, true> : batch_kernel<R, NT, U, true, LPR, false>)
+                    : batch_kernel<R, NT, U, false, LPR, false>;
+    return occupancy(kern, NT, smem);
+}
+
+// Lanes per row and grid.  A row is summed by LPR lanes (RPW = 32 / LPR rows per warp) with U 16-byte loads per
+// lane in flight per chunk (U = 4: larger U makes the heavier policies spill into fewer resident warps).  The
+// grid spreads the rows over as few CTAs as the resident sweeps need (no partially filled last sweep).
+template <class R, int NT, int U, int LPR>
+static cudaError_t launch_batch_shape(const KParams &K, const void *A, int64_t lda, const void *x, int64_t rows,
+                                      int64_t n, bool vec, OutSpec O, cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int bps = batch_occupancy<R, NT, U, LPR>(K, n, vec);
+    const int64_t rpb = (NT / 32) * (32 / LPR), gmax = (int64_t)num_sms(dev) * bps;
+    const int64_t sweeps = std::max<int64_t>((rows + gmax * rpb - 1) / (gmax * rpb), 1);
+    const int64_t grid = (rows + sweeps * rpb - 1) / (sweeps * rpb);
+    return launch_batch_lpr<R, NT, U, LPR>(K, A, lda, x, rows, n, vec, grid, O, s);
+}
+
 template <class R, int NT, int U>
 static cudaError_t launch_batch_t(const KParams &K, const void *A, int64_t lda, const void *x, int64_t rows,
                                   int64_t n, bool vec, OutSpec O, cudaStream_t s) {
-    if (n / R::W >= 256 || R::kTable) return launch_batch_lpr<R, NT, U, 32>(K, A, lda, x, rows, n, vec, O, s);
-    return launch_batch_lpr<R, NT, U, 8>(K, A, lda, x, rows, n, vec, O, s);
+    // a full warp per long row (>= 256 vectors) or per table kernel row, else 8 lanes (4 rows per warp)
+    if (n / R::W >= 256 || R::kTable) return launch_batch_shape<R, NT, U, 32>(K, A, lda, x, rows, n, vec, O, s);
+    return launch_batch_shape<R, NT, U, 8>(K, A, lda, x, rows, n, vec, O, s);
 }
 
 gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int64_t lda, const void *x, int64_t rows,
@@ -1219,14 +1272,14 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
             K2.kblk = kblk;
             switch (xpol) {
 #define GFP_BATCH(pol, ...) \
-    case pol: *err = launch_batch_t<__VA_ARGS__, 256, 4>(K2, A, lda, x, rows, n, vec, O, s); break;
+    case pol: *err = launch_batch_t<__VA_ARGS__, 256, kBatchU>(K2, A, lda, x, rows, n, vec, O, s); break;
                 GFP_CS_CASES(GFP_BATCH)
 #undef GFP_BATCH
-            case P_FP_THREAD: *err = launch_batch_t<Fp64<0>, 256, 4>(K2, A, lda, x, rows, n, vec, O, s); break;
-            case P_FP_K2: *err = launch_batch_t<Fp64<2>, 256, 4>(K2, A, lda, x, rows, n, vec, O, s); break;
-            case P_FP_K1: *err = launch_batch_t<Fp64<1>, 256, 4>(K2, A, lda, x, rows, n, vec, O, s); break;
+            case P_FP_THREAD: *err = launch_batch_t<Fp64<0>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, O, s); break;
+            case P_FP_K2: *err = launch_batch_t<Fp64<2>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, O, s); break;
+            case P_FP_K1: *err = launch_batch_t<Fp64<1>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, O, s); break;
 #define GFP_BATCH_FC(pol, ...) \
-    case pol: *err = launch_batch_t<__VA_ARGS__, 256, 4>(K2, A, lda, x, rows, n, vec, O, s); break;
+    case pol: *err = launch_batch_t<__VA_ARGS__, 256, kBatchU>(K2, A, lda, x, rows, n, vec, O, s); break;
                 GFP_FC_CASES(GFP_BATCH_FC)
 #undef GFP_BATCH_FC
             default: return GFP_E_UNSUPPORTED;
@@ -1251,35 +1304,35 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
                 *err = cudaGetLastError();
             } else if (per_lane * q2 <= max64) {
                 *err = (u128)n * q2 <= max64
-                           ? launch_batch_t<ClassicalU16<CL_ALL>, 256, 4>(K, A, lda, x, rows, n, vec, O, s)
-                           : launch_batch_t<ClassicalU16<CL_THREAD>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+                           ? launch_batch_t<ClassicalU16<CL_ALL>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s)
+                           : launch_batch_t<ClassicalU16<CL_THREAD>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
             } else {
                 return GFP_E_UNSUPPORTED;
             }
         } else {
             if ((u128)n * q2 <= max64)
-                *err = launch_batch_t<ClassicalU32<CL_ALL>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+                *err = launch_batch_t<ClassicalU32<CL_ALL>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
             else if (per_lane * q2 <= max64)
-                *err = launch_batch_t<ClassicalU32<CL_THREAD>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+                *err = launch_batch_t<ClassicalU32<CL_THREAD>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
             else
-                *err = launch_batch_t<ClassicalU32<CL_OVERFLOW>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+                *err = launch_batch_t<ClassicalU32<CL_OVERFLOW>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
         }
         break;
     case GFP_REP_MONTGOMERY:
         if (I.mont_kr >= 4)
-            *err = launch_batch_t<Montgomery<4>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Montgomery<4>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
         else if (I.mont_kr >= 2)
-            *err = launch_batch_t<Montgomery<2>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Montgomery<2>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
         else
-            *err = launch_batch_t<Montgomery<1>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Montgomery<1>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
         break;
     case GFP_REP_FP64:
         if (per_lane * q2 < ((u128)1 << 53))
-            *err = launch_batch_t<Fp64<0>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Fp64<0>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
         else if (I.k >= 2)
-            *err = launch_batch_t<Fp64<2>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Fp64<2>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
         else
-            *err = launch_batch_t<Fp64<1>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Fp64<1>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
         break;
     case GFP_REP_ZECH:
         if (zech_small_layout(I.p))
@@ -1293,20 +1346,20 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
         K2.kblk = I.k;
         if (I.dtype == GFP_F64) {
             if (per_lane * h2 + h < ((u128)1 << 53))
-                *err = launch_batch_t<Fp64C<0>, 256, 4>(K, A, lda, x, rows, n, vec, O, s);
+                *err = launch_batch_t<Fp64C<0>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
             else
                 switch (fc_policy(I.k)) {
-                case P_FC8: *err = launch_batch_t<Fp64C<8>, 256, 4>(K, A, lda, x, rows, n, vec, O, s); break;
-                case P_FC4: *err = launch_batch_t<Fp64C<4>, 256, 4>(K, A, lda, x, rows, n, vec, O, s); break;
-                case P_FC2: *err = launch_batch_t<Fp64C<2>, 256, 4>(K, A, lda, x, rows, n, vec, O, s); break;
-                default: *err = launch_batch_t<Fp64C<1>, 256, 4>(K, A, lda, x, rows, n, vec, O, s); break;
+                case P_FC8: *err = launch_batch_t<Fp64C<8>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s); break;
+                case P_FC4: *err = launch_batch_t<Fp64C<4>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s); break;
+                case P_FC2: *err = launch_batch_t<Fp64C<2>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s); break;
+                default: *err = launch_batch_t<Fp64C<1>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s); break;
                 }
         } else if (I.dtype == GFP_U16) {
-            *err = (u128)n * h2 + h <= w63 ? launch_batch_t<CenteredI<int16_t, CE_ALL>, 256, 4>(K, A, lda, x, rows, n, vec, O, s)
-                                          : launch_batch_t<CenteredI<int16_t, CE_BLOCKED>, 256, 4>(K2, A, lda, x, rows, n, vec, O, s);
+            *err = (u128)n * h2 + h <= w63 ? launch_batch_t<CenteredI<int16_t, CE_ALL>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s)
+                                          : launch_batch_t<CenteredI<int16_t, CE_BLOCKED>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, O, s);
         } else {
-            *err = (u128)n * h2 + h <= w63 ? launch_batch_t<CenteredI<int32_t, CE_ALL>, 256, 4>(K, A, lda, x, rows, n, vec, O, s)
-                                          : launch_batch_t<CenteredI<int32_t, CE_BLOCKED>, 256, 4>(K2, A, lda, x, rows, n, vec, O, s);
+            *err = (u128)n * h2 + h <= w63 ? launch_batch_t<CenteredI<int32_t, CE_ALL>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s)
+                                          : launch_batch_t<CenteredI<int32_t, CE_BLOCKED>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, O, s);
         }
         break;
     }

@@ -179,14 +179,23 @@ gfp_status gfp_tune(const gfp_tune_case *cases, int32_t ncases, double ms_per_ca
             return err(GFP_E_INVAL, "gfp_tune: case " + std::to_string(ci) + ": kind 0/1, n >= 1, rows >= 1 (batch)");
         const size_t es = esize(c.dtype);
         const int64_t na = c.kind == 0 ? c.n : c.rows * c.n, nout = c.kind == 0 ? 1 : c.rows;
-        DevBuf A, B, O;
-        if (cudaMalloc(&A.p, na * es) != cudaSuccess || cudaMalloc(&B.p, c.n * es) != cudaSuccess ||
-            cudaMalloc(&O.p, nout * es + 16) != cudaSuccess)
-            return err(GFP_E_NOMEM, "gfp_tune: input allocation");
-        // residues in [0, p) (classical, Montgomery forms, fp64 integers) or Zech codes in [0, qbar]
-        if (launch_fill(A.p, c.dtype, c.p, 0x0404008ull + 2 * ci, na, s) != cudaSuccess ||
-            launch_fill(B.p, c.dtype, c.p, 0x0404009ull + 2 * ci, c.n, s) != cudaSuccess)
-            return err(GFP_E_CUDA, "gfp_tune: fill launch");
+        // input sets rotated through while timing, so that the timed calls stream >= 3x the L2 between two
+        // uses of the same set (inputs from HBM, as in bench.py); at most 64 sets and 1 GiB
+        const double set_bytes = (double)(na + c.n) * es;
+        int nsets = (int)std::min(64.0, std::max(1.0, std::ceil(3.0 * 126e6 / set_bytes)));
+        while (nsets > 1 && nsets * set_bytes > 1073741824.0) --nsets;
+        std::vector<DevBuf> A(nsets), B(nsets);
+        DevBuf O;
+        if (cudaMalloc(&O.p, nout * es + 16) != cudaSuccess) return err(GFP_E_NOMEM, "gfp_tune: output allocation");
+        for (int k = 0; k < nsets; ++k) {
+            if (cudaMalloc(&A[k].p, na * es) != cudaSuccess || cudaMalloc(&B[k].p, c.n * es) != cudaSuccess)
+                return err(GFP_E_NOMEM, "gfp_tune: input allocation");
+            // residues in [0, p) (classical, Montgomery forms, fp64 integers) or Zech codes in [0, qbar]
+            if (launch_fill(A[k].p, c.dtype, c.p, 0x0404008ull + 2 * ci + 1000 * k, na, s) != cudaSuccess ||
+                launch_fill(B[k].p, c.dtype, c.p, 0x0404009ull + 2 * ci + 1000 * k, c.n, s) != cudaSuccess)
+                return err(GFP_E_CUDA, "gfp_tune: fill launch");
+        }
+        int next = 0;
 
         // candidates: the built-in plan first, then every explicit strategy the representation offers
         std::vector<gfp_options> cand = {{GFP_STRAT_AUTO, 0}};
@@ -208,13 +217,14 @@ gfp_status gfp_tune(const gfp_tune_case *cases, int32_t ncases, double ms_per_ca
             if (c.kind == 0) cand.push_back({GFP_STRAT_ZECH_ADD, 0});
             break;
         }
-        auto call = [&](const gfp_options &o) -> gfp_status {
+        auto call = [&](const gfp_options &o, int set) -> gfp_status {
             const bool builtin = o.strategy == GFP_STRAT_AUTO;
             t_bypass = builtin;
+            const void *a = A[set].p, *b = B[set].p;
             gfp_status r = c.kind == 0
-                               ? gfp_dot_ex(c.p, (gfp_rep)c.rep, (gfp_dtype)c.dtype, A.p, B.p, c.n, builtin ? nullptr : &o,
+                               ? gfp_dot_ex(c.p, (gfp_rep)c.rep, (gfp_dtype)c.dtype, a, b, c.n, builtin ? nullptr : &o,
                                             O.p, s)
-                               : gfp_dot_batch_ex(c.p, (gfp_rep)c.rep, (gfp_dtype)c.dtype, A.p, c.n, B.p, c.rows, c.n,
+                               : gfp_dot_batch_ex(c.p, (gfp_rep)c.rep, (gfp_dtype)c.dtype, a, c.n, b, c.rows, c.n,
                                                   builtin ? nullptr : &o, O.p, s);
             t_bypass = false;
             return r;
@@ -223,7 +233,7 @@ gfp_status gfp_tune(const gfp_tune_case *cases, int32_t ncases, double ms_per_ca
         double best_us = 0, builtin_us = 0;
         gfp_options best = cand[0];
         for (size_t k = 0; k < cand.size(); ++k) {
-            st = call(cand[k]);
+            st = call(cand[k], 0);  // the cross-check runs on set 0 for every candidate
             if (st == GFP_E_BOUND || st == GFP_E_UNSUPPORTED) continue;  // not admissible for this (p, n)
             if (st != GFP_OK) return st;
             if (cudaMemcpyAsync(got.data(), O.p, got.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
@@ -234,16 +244,16 @@ gfp_status gfp_tune(const gfp_tune_case *cases, int32_t ncases, double ms_per_ca
                 return err(GFP_E_CUDA, "gfp_tune: case " + std::to_string(ci) + ": strategy " +
                                            std::to_string(cand[k].strategy) + "/" + std::to_string(cand[k].acc_bits) +
                                            " disagrees with the built-in plan");
-            for (int w = 0; w < 2; ++w) call(cand[k]);
+            for (int w = 0; w < 2; ++w) call(cand[k], (next++) % nsets);
             cudaEventRecord(e0, s);
-            call(cand[k]);
+            call(cand[k], (next++) % nsets);
             cudaEventRecord(e1, s);
             if (cudaEventSynchronize(e1) != cudaSuccess) return err(GFP_E_CUDA, "gfp_tune: timing");
             float ms1 = 0;
             cudaEventElapsedTime(&ms1, e0, e1);
             const int reps = (int)std::min(2000.0, std::max(3.0, ms_per_candidate / std::max(ms1, 1e-4f)));
             cudaEventRecord(e0, s);
-            for (int r = 0; r < reps; ++r) call(cand[k]);
+            for (int r = 0; r < reps; ++r) call(cand[k], (next++) % nsets);
             cudaEventRecord(e1, s);
             if (cudaEventSynchronize(e1) != cudaSuccess) return err(GFP_E_CUDA, "gfp_tune: timing");
             float ms = 0;
