@@ -636,9 +636,12 @@ def prime_sweep(args):
     small, large = sweep_primes(gfp)
     rows, n = args.sweep_rows, 512
     peak, _ = peak_hbm()
-    strategies = [("auto", gfp.AUTO, 0), ("blocked32", gfp.BLOCKED, 32), ("overflow32", gfp.OVERFLOW, 32),
-                  ("hybrid32", gfp.HYBRID, 32), ("blocked64", gfp.BLOCKED, 64), ("overflow64", gfp.OVERFLOW, 64),
-                  ("hybrid64", gfp.HYBRID, 64)]
+    # "auto": AUTO with the install-time table (F4); "builtin": AUTO with the table cleared (the analytic plan)
+    strategies = [("auto", gfp.AUTO, 0), ("builtin", gfp.AUTO, 0), ("blocked32", gfp.BLOCKED, 32),
+                  ("overflow32", gfp.OVERFLOW, 32), ("hybrid32", gfp.HYBRID, 32), ("carry32", gfp.CARRY, 32),
+                  ("blocked64", gfp.BLOCKED, 64), ("overflow64", gfp.OVERFLOW, 64), ("hybrid64", gfp.HYBRID, 64),
+                  ("carry64", gfp.CARRY, 64)]
+    table = gfp.tune_entries()
     cells = []
     out = open(args.sweep, "w")
     for p in small + large:
@@ -650,6 +653,10 @@ def prime_sweep(args):
         ref = gfp.dot_batch(A, x, p, gfp.CLASSICAL)
         nbytes = A.numel() * A.element_size() + n * A.element_size() + rows * A.element_size()
         for name, strat, m in strategies:
+            if name == "builtin":
+                gfp.tune_clear()
+            elif name == "blocked32":
+                gfp.tune_set(table)
             try:
                 pl = gfp.plan(p, gfp.CLASSICAL, n, dtype=dt_t, strategy=strat, acc_bits=m)
             except gfp.GfpError:

@@ -8,8 +8,8 @@ cells = [json.loads(line) for line in open(sys.argv[1])]
 by = collections.defaultdict(dict)
 for c in cells:
     by[c["p"]][c["strategy"]] = c
-names = ["auto", "blocked32", "overflow32", "hybrid32", "blocked64", "overflow64", "hybrid64"]
-print("# F1 prime sweep (bench.py --sweep): DIM=512 dots, 2^19 rows per cell; terms/s / 1e12 per strategy; k32 = blocked "
+names = ["auto", "builtin", "blocked32", "overflow32", "hybrid32", "carry32", "blocked64", "overflow64", "hybrid64", "carry64"]
+print("# F1 prime sweep (bench.py --sweep): DIM=512 dots, 2^19 rows per cell; terms/s / 1e12 per strategy (auto = AUTO with the shipped install-time table, builtin = AUTO without it); k32 = blocked "
       "block length at m=32; red/lane32 = reductions per lane (16 terms); all cells bit-equal to the default plan: %s"
       % all(c["equal_to_default"] for c in cells))
 print("p".rjust(11), *[n.rjust(10) for n in names], "k32".rjust(11), "red/lane32".rjust(10))
