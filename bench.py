@@ -528,8 +528,8 @@ def e2e_leg(gfp, cfg, d, world, steps, stream, dev):
 
         def one():
             r = gfp.dot_host(a, b, p, rep, stream=stream)
-            if world > 1:  # combine the per-rank results (additive in every rep but Zech)
-                part.fill_(int(r))
+            if world > 1:  # combine the per-rank results (additive in every rep but Zech; centered -> residue)
+                part.fill_(int(r) % p)
                 dist.all_reduce(part)
                 gfp.finalize(part, p, rep, a.dtype, out=fin, stream=stream)
                 fin.cpu()
@@ -544,8 +544,23 @@ def e2e_leg(gfp, cfg, d, world, steps, stream, dev):
     torch.cuda.synchronize()
     dt = max_over_ranks(time.perf_counter() - t0, world)
     total = sum_over_ranks(terms, world)
+    # the e2e roofline: this rank's host->device link, measured here with a plain pinned copy
+    probe = torch.empty(64 << 20, dtype=torch.uint8).pin_memory()
+    dprobe = torch.empty_like(probe, device=dev)
+    dprobe.copy_(probe, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(8):
+        dprobe.copy_(probe, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    link = 8 * probe.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9
+    achieved = h2d * steps / dt / 1e9
     return {"value": total * steps / dt, "unit": "terms/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "h2d_GBps": round(achieved, 2), "h2d_copy_peak_GBps": round(link, 2),
+            "link_frac": round(achieved / link, 3),
             "api": "gfp_dot_host (chunked pinned H2D overlapped with the dot kernels)"
             if cfg["kind"] == "dot" else "torch H2D + gfp_dot_batch + D2H",
             "clock": "host wall clock around synchronous calls, max over ranks"}
