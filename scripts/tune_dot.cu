@@ -72,6 +72,42 @@ __global__ void __launch_bounds__(NT) v_ldg(const uint4 *av, const uint4 *bv, in
     finish_cta(acc, K, out);
 }
 
+// 256-bit loads (LDG.E.256, sm_100): each thread streams 32 contiguous bytes per load and operand.
+__device__ __forceinline__ void ld256(const uint4 *p, uint4 &lo, uint4 &hi) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                 : "l"(p));
+}
+
+template <int NT, int U>
+__global__ void __launch_bounds__(NT) v_ldg256(const uint4 *av, const uint4 *bv, int64_t nvec, KParams K,
+                                               unsigned long long *out) {
+    R::Acc acc;
+    R::init(acc);
+    const int64_t npair = nvec / 2;  // 32-byte units
+    int64_t i0 = (int64_t)blockIdx.x * (NT * U) + threadIdx.x;
+    const int64_t step = (int64_t)gridDim.x * (NT * U);
+    for (; i0 + (U - 1) * NT < npair; i0 += step) {
+        uint4 xa[2 * U], xb[2 * U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            ld256(av + 2 * (i0 + u * NT), xa[2 * u], xa[2 * u + 1]);
+            ld256(bv + 2 * (i0 + u * NT), xb[2 * u], xb[2 * u + 1]);
+        }
+#pragma unroll
+        for (int u = 0; u < 2 * U; ++u) R::vec(acc, xa[u], xb[u], K, nullptr);
+    }
+    for (int u = 0; u < U; ++u)
+        if (i0 + u * NT < npair) {
+            uint4 a0, a1, b0, b1;
+            ld256(av + 2 * (i0 + u * NT), a0, a1);
+            ld256(bv + 2 * (i0 + u * NT), b0, b1);
+            R::vec(acc, a0, b0, K, nullptr);
+            R::vec(acc, a1, b1, K, nullptr);
+        }
+    finish_cta(acc, K, out);
+}
+
 // Contiguous per-CTA ranges instead of grid-stride (each CTA streams one long run of DRAM pages).
 template <int NT, int U>
 __global__ void __launch_bounds__(NT) v_ldg_block(const uint4 *av, const uint4 *bv, int64_t nvec, KParams K,
@@ -248,6 +284,22 @@ int main(int argc, char **argv) {
     LDG(256, 4, 0, 2)
     LDG(256, 4, 0, 8)
     LDG(256, 16, 0, 1)
+#define LDG256(NT, U)                                                                                     \
+    {                                                                                                     \
+        int bps;                                                                                          \
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, v_ldg256<NT, U>, NT, 0));                  \
+        int grid = sms * bps;                                                                             \
+        double ms = time_it([&] { v_ldg256<NT, U><<<grid, NT>>>(av, bv, nvec, K, d_out); }, 20, d_out, &res); \
+        char nm[96];                                                                                      \
+        snprintf(nm, sizeof nm, "ldg256 NT=%d U=%d grid=%d", NT, U, grid);                               \
+        report(nm, ms);                                                                                   \
+    }
+    LDG256(256, 1)
+    LDG256(256, 2)
+    LDG256(256, 4)
+    LDG256(512, 2)
+    LDG256(128, 4)
+    LDG(256, 4, 0, 1)
     {
         int bps;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, v_ldg_block<256, 4>, 256, 0));
