@@ -545,17 +545,18 @@ def e2e_leg(gfp, cfg, d, world, steps, stream, dev):
     dt = max_over_ranks(time.perf_counter() - t0, world)
     total = sum_over_ranks(terms, world)
     # the e2e roofline: this rank's host->device link, measured here with a plain pinned copy
-    probe = torch.empty(64 << 20, dtype=torch.uint8).pin_memory()
+    probe = torch.empty(512 << 20, dtype=torch.uint8).pin_memory()
     dprobe = torch.empty_like(probe, device=dev)
     dprobe.copy_(probe, non_blocking=True)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(8):
+    for _ in range(4):
         dprobe.copy_(probe, non_blocking=True)
     e1.record()
     torch.cuda.synchronize()
-    link = 8 * probe.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9
+    link = 4 * probe.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9
+    del probe, dprobe
     achieved = h2d * steps / dt / 1e9
     return {"value": total * steps / dt, "unit": "terms/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps,
