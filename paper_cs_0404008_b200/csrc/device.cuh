@@ -426,7 +426,7 @@ struct Ops {
 
     // product of two codes (each in [0, qbar]); a zero operand gives kZ.  Result in [0, q].
     __device__ __forceinline__ static uint32_t mul(uint32_t ci, uint32_t cj, uint32_t q) {
-        const uint32_t v = fold((uint32_t)S * (ci + cj), q);
+        const uint32_t v = min(fold((uint32_t)S * (ci + cj), q), q);  // clamp: non-canonical codes stay in range
         return (ci == 0 || cj == 0) ? kZ : v;
     }
 

@@ -318,8 +318,8 @@ __device__ __forceinline__ void zech_add_vec(uint32_t (&acc)[8], uint4 x, uint4 
 // one add and one fold for the sum.
 __device__ __forceinline__ uint32_t zech_fast_add(uint32_t s, uint32_t lane_sum, bool zero, uint32_t q,
                                                   uint32_t kzero, uint32_t tab) {
-    uint32_t k = 2u * lane_sum - s;  // 2 (ci + cj) - s in (4 - q, 2q]
-    k = min(k, k + q);
+    uint32_t k = 2u * lane_sum - s;  // 2 (ci + cj) - s in (4 - q, 2q] for canonical codes
+    k = min(min(k, k + q), 2u * q);   // the clamp keeps non-canonical codes inside the table (gfp.h)
     k = zero ? kzero : k;
     uint16_t d;
     asm("ld.shared.u16 %0, [%1];" : "=h"(d) : "r"(tab + k));

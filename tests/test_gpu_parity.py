@@ -546,3 +546,24 @@ def test_fused_allreduce_buffer_reuse():
             assert int(gd.dot_fused(ga, gb, p, gfp.CLASSICAL, x).cpu().to(torch.int64)[0]) == want
         torch.cuda.synchronize()
         x.close()
+
+
+def test_non_canonical_inputs_never_fault():
+    """P:49-50 preconditions are not checked on the hot path; violating them gives an unspecified value but
+    must never fault (gfp.h): random 16-bit Zech codes at large and small fields, residues >= p, and
+    a following canonical call is still exact."""
+    rng = np.random.default_rng(7)
+    n = 50_001
+    raw16 = cu(rng.integers(0, 65536, n, dtype=np.uint16))
+    raw32 = cu(rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32))
+    for p in [101, 32749, 40009, 65521]:
+        gfp.dot(raw16, raw16, p, gfp.ZECH)
+        gfp.dot_batch(raw16[: 49 * 1000].view(49, 1000), raw16[:1000], p, gfp.ZECH)
+        gfp.from_rep(raw16, p, gfp.ZECH)
+        gfp.to_rep(raw32, p, gfp.ZECH, out=torch.empty(n, dtype=torch.uint16, device=DEV))
+    gfp.dot(raw32, raw32, 65521, gfp.CLASSICAL)
+    gfp.dot(raw32, raw32, 2 ** 31 - 1, gfp.MONTGOMERY)
+    torch.cuda.synchronize()
+    p = 32749
+    a, b = synth.zech_codes(SEED, 0, 0, n, p - 1), synth.zech_codes(SEED, 1, 0, n, p - 1)
+    assert int(gfp.dot(cu(a), cu(b), p, gfp.ZECH).cpu().to(torch.int64)[0]) == oracle.dot_zech(p, 2, a, b)

@@ -128,3 +128,19 @@ def test_table_sizes_in_any_order():
         want = oracle.dot_zech(p, g, a, b)
         assert zadd(cu(a), cu(b), p) == want, p
         assert int(gfp.dot(cu(a), cu(b), p, ZE).cpu().to(torch.int64)[0]) == want, p
+
+
+@pytest.mark.parametrize("p", [3, 101, 32749, 40009, 65521])
+def test_zech_add_non_canonical_codes_stay_in_bounds(p):
+    """Preconditions are not checked on the hot path, but non-canonical codes (> q-1) must not
+    fault (gfp.h): every lookup index is clamped into the table.  The result is unspecified; the next
+    call on canonical data must still be exact (no sticky error, workspace intact)."""
+    n = 100_003
+    rng = np.random.default_rng(p)
+    a = rng.integers(0, 65536, n, dtype=np.uint16)
+    b = rng.integers(0, 65536, n, dtype=np.uint16)
+    zadd(cu(a), cu(b), p)
+    torch.cuda.synchronize()
+    ca = synth.zech_codes(SEED, 0, 0, n, p - 1)
+    cb = synth.zech_codes(SEED, 1, 0, n, p - 1)
+    assert zadd(cu(ca), cu(cb), p) == oracle.dot_zech(p, oracle.primitive_root(p), ca, cb)
