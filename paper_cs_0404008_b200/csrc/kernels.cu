@@ -4,11 +4,16 @@
 //                   16-byte loads, per-thread delayed-modulus accumulation (policy R, device.cuh),
 //                   warp-shuffle + CTA tree, per-CTA partial, last-CTA-done final reduction and
 //                   encoding -- one launch per dot.
+//                   With OUT_XCHG the last CTA also exchanges the partial with the peer GPUs over
+//                   NVLink peer memory and finalizes (gfp_dot_allreduce, a9 fused).
+//   zech_add_dot_kernel  the pure-Zech dot (F3): Table-1 products, t_plus1 additions in shared memory.
 //   batch_cl16      C5 matrix-vector over classical u16: warp per row, x byte-split in shared
 //                   memory, two DP2A per pair of terms (a8).
-//   batch_kernel    generic batch (any policy): warp per row.
+//   batch_kernel    generic batch (any policy): LPR lanes per row, x staged in shared memory.
 //   convert_kernel  representation conversions (a2).
 //   finalize_kernel sum of partial residues -> mod p -> encode (a7/a9).
+//   fill_kernel     synthetic canonical inputs for the install-time tuner (F4, tune.cpp).
+//   xchg_setup_kernel  writes a fused-combine group description into an exchange buffer.
 #include <algorithm>
 #include <mutex>
 #include <string>
@@ -753,7 +758,13 @@ static int occupancy(F kernel, int block, size_t smem) {
 #ifndef GFP_DOT_PIPE
 #define GFP_DOT_PIPE 0
 #endif
-constexpr int kDotNT = 256, kDotU = 4, kFpU = 2, kZechNT = 1024, kZechU = 2, kZaddNT = 1024, kZaddU = 2;
+#ifndef GFP_FP_U
+#define GFP_FP_U 2
+#endif
+#ifndef GFP_DOT_U
+#define GFP_DOT_U 4
+#endif
+constexpr int kDotNT = 256, kDotU = GFP_DOT_U, kFpU = GFP_FP_U, kZechNT = 1024, kZechU = 2, kZaddNT = 1024, kZaddU = 2;
 constexpr bool kPipe = GFP_DOT_PIPE != 0;
 
 template <class R, int NT, int U, bool PIPE>
