@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
                                                  int64_t head, KParams K, Workspace ws, OutSpec O) {
     extern __shared__ __align__(16) uint16_t s_tab[];
     __shared__ uint64_t red[32];
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // stream order (no-op without a programmatic launch)
     typename R::Acc acc;
     R::init(acc);
     const int64_t gtid = (int64_t)blockIdx.x * NT + threadIdx.x;
@@ -267,6 +268,7 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
             *sum = 0;  // self-reset for the next launch on this stream
             *ws.counter = 0;
         }
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after this CTA's last write
     }
 }
 
@@ -367,6 +369,7 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
     extern __shared__ __align__(16) uint16_t s_delta[];
     __shared__ uint32_t red[32];
     __shared__ int s_last;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // stream order (see launch_pdl)
     const uint32_t q = (uint32_t)S * K.qbar;
     const int64_t gtid = (int64_t)blockIdx.x * NT + threadIdx.x;
     const int64_t gstride = (int64_t)gridDim.x * NT;
@@ -447,6 +450,7 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
         unsigned int t;
         asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(ws.counter) : "memory");
         s_last = t == gridDim.x - 1;
+        if (!s_last) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after the last write
     }
     __syncthreads();
     if (!s_last) return;
@@ -466,6 +470,7 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
             else ((uint64_t *)O.out)[0] += r;
         }
         *ws.counter = 0;
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }
 }
 
@@ -730,6 +735,28 @@ cudaError_t launch_fill(void *out, int dtype, uint64_t p, uint64_t seed, int64_t
 }
 
 // ------------------------------------------------------------------------------ launch helpers
+// Programmatic dependent launch for the dot kernels: the launch of dot N+1 is staged while dot N runs.
+// The kernel waits (griddepcontrol.wait) before doing anything and each CTA signals its dependents
+// (griddepcontrol.launch_dependents) only after its last global write, so memory order is exactly the
+// stream order; what overlaps is the launch latency of the next dot.
+#ifndef GFP_PDL
+#define GFP_PDL 1
+#endif
+template <typename Kern, typename... Args>
+static cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = GFP_PDL;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <typename F>
 static int occupancy(F kernel, int block, size_t smem) {
     static std::mutex mu;
@@ -772,9 +799,10 @@ static cudaError_t launch_dot_t(const DotPlan &P, const KParams &K, const void *
                                 Workspace ws, OutSpec O, cudaStream_t s) {
     auto kern = dot_kernel<R, NT, U, PIPE>;
     occupancy(kern, NT, P.smem);  // sets the smem attribute once
-    kern<<<P.grid, NT, P.smem, s>>>((const typename R::elem *)a, (const typename R::elem *)b, n, P.head, K, ws, O);
+    cudaError_t e = launch_pdl(kern, dim3(P.grid), dim3(NT), P.smem, s, (const typename R::elem *)a,
+                               (const typename R::elem *)b, n, P.head, K, ws, O);
     count_launch();
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <class R, int NT, int U, bool PIPE>
@@ -904,7 +932,9 @@ cudaError_t launch_dot(const DotPlan &P, const KParams &K0, const void *a, const
         auto kern = zech_add_fast(K.p) ? zech_add_dot_kernel<kZaddNT, kZaddU, 2, true>
                                                         : zech_add_dot_kernel<kZaddNT, kZaddU, 1, false>;
         occupancy(kern, kZaddNT, P.smem);
-        kern<<<P.grid, kZaddNT, P.smem, s>>>((const uint16_t *)a, (const uint16_t *)b, n, P.head, K, ws, O);
+        cudaError_t e = launch_pdl(kern, dim3(P.grid), dim3(kZaddNT), P.smem, s, (const uint16_t *)a,
+                                   (const uint16_t *)b, n, P.head, K, ws, O);
+        if (e != cudaSuccess) return e;
         count_launch();
         return cudaGetLastError();
     }

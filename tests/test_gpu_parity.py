@@ -567,3 +567,38 @@ def test_non_canonical_inputs_never_fault():
     p = 32749
     a, b = synth.zech_codes(SEED, 0, 0, n, p - 1), synth.zech_codes(SEED, 1, 0, n, p - 1)
     assert int(gfp.dot(cu(a), cu(b), p, gfp.ZECH).cpu().to(torch.int64)[0]) == oracle.dot_zech(p, 2, a, b)
+
+
+def test_back_to_back_dots_keep_stream_order():
+    """Dots are launched with programmatic dependent launch (the next launch is staged while the previous
+    dot runs); memory order must stay the stream order: a dot whose output lands inside the next dot's
+    operand is seen by that dot, in plain launches and in a CUDA graph."""
+    p, n = 65521, 1 << 20
+    a1, b1 = cu(synth.uniform(SEED, 0, 0, n, p, np.uint32)), cu(synth.uniform(SEED, 1, 0, n, p, np.uint32))
+    b2 = cu(synth.uniform(SEED, 2, 0, n, p, np.uint32))
+    r1 = oracle.dot_classical(p, a1.cpu().numpy(), b1.cpu().numpy())
+    x = cu(synth.uniform(SEED, 3, 0, n, p, np.uint32))
+    xh = x.cpu().numpy().copy()
+    xh[n // 2] = r1
+    want = oracle.dot_classical(p, xh, b2.cpu().numpy())
+    s = torch.cuda.Stream()
+    out2 = torch.empty(1, dtype=torch.uint32, device=DEV)
+    with torch.cuda.stream(s):
+        for _ in range(5):
+            x[n // 2] = 0
+            gfp.dot(a1, b1, p, gfp.CLASSICAL, out=x[n // 2: n // 2 + 1], stream=s)
+            gfp.dot(x, b2, p, gfp.CLASSICAL, out=out2, stream=s)
+            s.synchronize()
+            assert int(out2.cpu().to(torch.int64)[0]) == want
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(3):
+                gfp.dot(a1, b1, p, gfp.CLASSICAL, out=x[n // 2: n // 2 + 1], stream=s)
+                gfp.dot(x, b2, p, gfp.CLASSICAL, out=out2, stream=s)
+    for _ in range(5):
+        x[n // 2] = 0
+        out2.zero_()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        assert int(out2.cpu().to(torch.int64)[0]) == want
