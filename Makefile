@@ -49,3 +49,7 @@ scripts/tune_small: scripts/tune_small.cu $(CSRC)/device.cuh $(CSRC)/params.h
 gfp-pipe: $(PKG)/libgfp_pipe.so
 $(PKG)/libgfp_pipe.so: $(GFP_SRCS) $(GFP_HDRS)
 	$(NVCC) $(NVFLAGS) -DGFP_DOT_PIPE=1 -shared -o $@ $(GFP_SRCS) -lcudart 2> /dev/null
+
+# generic A/B variant: make variant NAME=x VFLAGS="-DGFP_CONV_U=2 ..." -> $(PKG)/libgfp_x.so
+variant:
+	$(NVCC) $(NVFLAGS) $(VFLAGS) -shared -o $(PKG)/libgfp_$(NAME).so $(GFP_SRCS) -lcudart 2> /dev/null

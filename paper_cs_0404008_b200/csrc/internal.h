@@ -22,6 +22,7 @@ struct OutSpec {
     void *out;          // OUT_ENCODE / OUT_XCHG: element of (rep, dtype); else uint64_t*
     int rep, dtype, mode;
     uint64_t *xchg;     // OUT_XCHG: this rank's exchange buffer (it holds rank, world and the peer table)
+    int prefetch;       // set by the launcher: prefetch the first chunk into L2 before griddepcontrol.wait
 };
 // Exchange-buffer layout (u64 words): [0] this rank's epoch, [1] rank, [2] world; flags at
 // kXFlags + parity * MAXW + r; partial slots at kXSlots + parity * MAXW + r; the peer table (every rank's

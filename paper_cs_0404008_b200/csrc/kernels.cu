@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <unordered_map>
 
 #include "device.cuh"
@@ -165,14 +166,60 @@ __device__ __forceinline__ void stage_table(uint16_t *dst, const uint16_t *src, 
     for (uint32_t i = threadIdx.x; i < entries / 8; i += blockDim.x) d[i] = __ldg(s + i);
 }
 
+// ------------------------------------------------------------------------------ programmatic dependent launch
+// Every hot kernel is launched with programmatic stream serialization (launch_pdl): the next kernel's
+// launch is staged while this one runs.  Each kernel waits (griddepcontrol.wait: every earlier kernel in
+// the stream has completed and its writes are visible) before its first load, so memory order is the
+// stream order, and each CTA signals its dependents after its last global write.
+// Short streams (the launcher sets O.prefetch) first prefetch the thread's first chunk of both operands
+// into L2, so the DRAM round trip of the first loads overlaps the previous kernel's drain (its last CTA's
+// combine and the memory flush).  An L2 prefetch cannot observe stale data: L2 is the device's point of
+// coherence and nothing is loaded into registers or L1 before the wait.  A/B on the B200
+// (scripts/ab_secondary.sh, profiles/r01_pdl_ab.txt): prefetch -6% at C2, -1.5% at C4 / F3 / C5; for long
+// streams (C3, conversions) it costs ~1% and is off.  Signalling the dependents at CTA entry instead
+// (GFP_PDL_EARLY=1) was slower on every config.
+#ifndef GFP_PDL_EARLY
+#define GFP_PDL_EARLY 0
+#endif
+#ifndef GFP_PDL_PREFETCH
+#define GFP_PDL_PREFETCH 1
+#endif
+// prefetch when each thread streams at most this many U-chunks
+constexpr int64_t kPrefetchMaxIters = 32;
+__device__ __forceinline__ void prefetch_l2(const void *ptr) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+}
+template <int U, int NT>
+__device__ __forceinline__ void pdl_enter(const uint4 *av, const uint4 *bv, int64_t i0, int64_t nvec, bool pf) {
+    if (GFP_PDL_PREFETCH && pf) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u * NT < nvec) {
+                prefetch_l2(av + i0 + u * NT);
+                prefetch_l2(bv + i0 + u * NT);
+            }
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // stream order (no-op without a programmatic launch)
+    if (GFP_PDL_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_exit() {
+    if (!GFP_PDL_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after the last write
+}
+
 // ------------------------------------------------------------------------------ single dot
+// Policies whose dots are long streams in practice (R::kNoPrefetch, Montgomery at C3) carry no prefetch
+// code at all: the register allocation of their streaming loop stays as A/B-tuned.
+template <class R, class = void>
+struct Prefetches { static constexpr bool value = true; };
+template <class R>
+struct Prefetches<R, std::void_t<decltype(R::kNoPrefetch)>> { static constexpr bool value = !R::kNoPrefetch; };
+
 template <class R, int NT, int U, bool PIPE>
 __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restrict__ a,
                                                  const typename R::elem *__restrict__ b, int64_t n,
                                                  int64_t head, KParams K, Workspace ws, OutSpec O) {
     extern __shared__ __align__(16) uint16_t s_tab[];
     __shared__ uint64_t red[32];
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // stream order (no-op without a programmatic launch)
     typename R::Acc acc;
     R::init(acc);
     const int64_t gtid = (int64_t)blockIdx.x * NT + threadIdx.x;
@@ -181,6 +228,7 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
     const uint4 *av = reinterpret_cast<const uint4 *>(a + head);
     const uint4 *bv = reinterpret_cast<const uint4 *>(b + head);
     int64_t i0 = (int64_t)blockIdx.x * (NT * U) + threadIdx.x;
+    pdl_enter<U, NT>(av, bv, i0, nvec, Prefetches<R>::value && O.prefetch != 0);
     const int64_t step = (int64_t)gridDim.x * (NT * U);
     const uint16_t *tab = nullptr;
 
@@ -268,7 +316,7 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
             *sum = 0;  // self-reset for the next launch on this stream
             *ws.counter = 0;
         }
-        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after this CTA's last write
+        pdl_exit();
     }
 }
 
@@ -369,7 +417,6 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
     extern __shared__ __align__(16) uint16_t s_delta[];
     __shared__ uint32_t red[32];
     __shared__ int s_last;
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // stream order (see launch_pdl)
     const uint32_t q = (uint32_t)S * K.qbar;
     const int64_t gtid = (int64_t)blockIdx.x * NT + threadIdx.x;
     const int64_t gstride = (int64_t)gridDim.x * NT;
@@ -377,6 +424,7 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
     const uint4 *av = reinterpret_cast<const uint4 *>(a + head);
     const uint4 *bv = reinterpret_cast<const uint4 *>(b + head);
     int64_t i0 = (int64_t)blockIdx.x * (NT * U) + threadIdx.x;
+    pdl_enter<U, NT>(av, bv, i0, nvec, O.prefetch != 0);
     const int64_t step = (int64_t)gridDim.x * (NT * U);
 
     // first loads in flight while the table is staged from L2
@@ -450,7 +498,7 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
         unsigned int t;
         asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(ws.counter) : "memory");
         s_last = t == gridDim.x - 1;
-        if (!s_last) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after the last write
+        if (!s_last) pdl_exit();
     }
     __syncthreads();
     if (!s_last) return;
@@ -470,7 +518,7 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
             else ((uint64_t *)O.out)[0] += r;
         }
         *ws.counter = 0;
-        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        pdl_exit();
     }
 }
 
@@ -496,6 +544,25 @@ __device__ __forceinline__ uint64_t group_sum(uint64_t v) {
     return v;
 }
 
+// Batch kernels under programmatic dependent launch (see pdl_enter): when pf, prefetch into
+// L2 the first chunk of this lane's first row (U 16-byte vectors, LPR lanes per row; A16 is the row base
+// in u16 units, lda16 the row stride in u16 units), then wait for the stream's earlier kernels.
+template <int U, int LPR, int NT>
+__device__ __forceinline__ void batch_pdl_enter(const void *A, int64_t lda16, int64_t rows, int64_t nvec, bool pf) {
+    if (GFP_PDL_PREFETCH && pf) {
+        const int lane = threadIdx.x & 31;
+        const int64_t row = ((int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5)) * (32 / LPR) + lane / LPR;
+        if (row < rows) {
+            const uint4 *av = reinterpret_cast<const uint4 *>(reinterpret_cast<const uint16_t *>(A) + row * lda16);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (lane % LPR + u * LPR < nvec) prefetch_l2(av + lane % LPR + u * LPR);
+        }
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (GFP_PDL_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // LPR lanes per row (32: a warp per long row; 8: four short rows per warp, so DIM = 512 rows still
 // keep 8 vectors per lane in flight and pay a 3-step instead of a 5-step shuffle per row).
 template <int NT, int U, int LPR>
@@ -503,6 +570,7 @@ __global__ void __launch_bounds__(NT) batch_cl16_kernel(const uint16_t *__restri
                                                         const uint16_t *__restrict__ x, int64_t rows, int64_t n,
                                                         KParams K, OutSpec O) {
     extern __shared__ __align__(16) uint32_t s_xw[];
+    batch_pdl_enter<U, LPR, NT>(A, lda, rows, n / 8, O.prefetch != 0);
     const int64_t nw = (n + 1) / 2;
     const int64_t nwpad = (nw + 3) & ~int64_t(3);
     for (int64_t j = threadIdx.x; j < nwpad; j += NT) {
@@ -560,6 +628,7 @@ __global__ void __launch_bounds__(NT) batch_cl16_kernel(const uint16_t *__restri
         tot = group_sum<LPR>(tot);
         if (valid && g == 0) write_result(mod_p(tot, K.p, K.mu), O, K, row);
     }
+    pdl_exit();
 }
 
 // ------------------------------------------------------------------------------ batch: generic
@@ -570,6 +639,8 @@ __global__ void __launch_bounds__(NT) batch_kernel(const typename R::elem *__res
                                                    const typename R::elem *__restrict__ x, int64_t rows,
                                                    int64_t n, KParams K, OutSpec O) {
     extern __shared__ __align__(16) uint16_t s_tab[];
+    batch_pdl_enter<U, LPR, NT>(A, lda * (int64_t)sizeof(typename R::elem) / 2, rows, VEC ? n / R::W : 0,
+                                O.prefetch != 0);
     const uint16_t *tab = nullptr;
     const uint32_t tab_bytes = R::kTable ? ((K.antilog_entries * 2 + 15) & ~15u) : 0;
     if constexpr (R::kTable) {
@@ -629,6 +700,7 @@ __global__ void __launch_bounds__(NT) batch_kernel(const typename R::elem *__res
         if (valid && g == 0)
             write_result(O.rep == GFP_REP_CENTERED ? smod_p((int64_t)v, K) : mod_p(v, K.p, K.mu), O, K, row);
     }
+    pdl_exit();
 }
 
 // ------------------------------------------------------------------------------ conversions
@@ -681,21 +753,40 @@ __device__ __forceinline__ void store8(T *p, const T (&v)[8]) {
     for (int i = 0; i < NV; ++i) __stcs(reinterpret_cast<uint4 *>(p) + i, r[i]);
 }
 
-template <int OP, typename TI, typename TO, int NT>
+// Elementwise conversion, streaming: each thread holds U chunks of 8 elements (all loads issued before
+// any store, so in == out is safe: a chunk is read and written by one thread only), coalesced per u.
+template <int OP, typename TI, typename TO, int NT, int U>
 __global__ void __launch_bounds__(NT) convert_kernel(const TI *in, TO *out, int64_t n, bool vec_ok, KParams K,
                                                      const uint16_t *table, uint32_t table_entries) {
     extern __shared__ __align__(16) uint16_t s_tab[];
+    const int64_t gtid = (int64_t)blockIdx.x * NT + threadIdx.x, gstride = (int64_t)gridDim.x * NT;
+    const int64_t nchunk = vec_ok ? n / 8 : 0;
+    int64_t c0 = (int64_t)blockIdx.x * (NT * U) + threadIdx.x;
+    const int64_t step = (int64_t)gridDim.x * (NT * U);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // stream order (launch_pdl; no prefetch: a long stream)
+    if (GFP_PDL_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint16_t *tab = nullptr;
     if (table != nullptr) {
         stage_table(s_tab, table, table_entries);
         __syncthreads();
         tab = s_tab;
     }
-    const int64_t gtid = (int64_t)blockIdx.x * NT + threadIdx.x, gstride = (int64_t)gridDim.x * NT;
-    int64_t done = 0;
-    if (vec_ok) {
-        const int64_t nchunk = n / 8;
-        for (int64_t c = gtid; c < nchunk; c += gstride) {
+    for (; c0 + (U - 1) * NT < nchunk; c0 += step) {
+        TI v[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) load8(in + 8 * (c0 + u * NT), v[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            TO w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = conv1<OP, TI, TO>(v[u][i], K, tab);
+            store8(out + 8 * (c0 + u * NT), w);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t c = c0 + u * NT;
+        if (c < nchunk) {
             TI v[8];
             TO w[8];
             load8(in + 8 * c, v);
@@ -703,9 +794,9 @@ __global__ void __launch_bounds__(NT) convert_kernel(const TI *in, TO *out, int6
             for (int i = 0; i < 8; ++i) w[i] = conv1<OP, TI, TO>(v[i], K, tab);
             store8(out + 8 * c, w);
         }
-        done = nchunk * 8;
     }
-    for (int64_t i = done + gtid; i < n; i += gstride) out[i] = conv1<OP, TI, TO>(in[i], K, tab);
+    for (int64_t i = nchunk * 8 + gtid; i < n; i += gstride) out[i] = conv1<OP, TI, TO>(in[i], K, tab);
+    pdl_exit();
 }
 
 // ------------------------------------------------------------------------------ synthetic inputs (tuning)
@@ -790,6 +881,9 @@ static int occupancy(F kernel, int block, size_t smem) {
 #endif
 #ifndef GFP_DOT_U
 #define GFP_DOT_U 4
+#endif
+#ifndef GFP_CONV_U
+#define GFP_CONV_U 2  // B200 A/B: U = 1 / 2 / 4 -> 5.50 / 5.61 / 5.17 TB/s (to_montgomery, 4 GiB)
 #endif
 constexpr int kDotNT = 256, kDotU = GFP_DOT_U, kFpU = GFP_FP_U, kZechNT = 1024, kZechU = 2, kZaddNT = 1024, kZaddU = 2;
 constexpr bool kPipe = GFP_DOT_PIPE != 0;
@@ -903,6 +997,11 @@ cudaError_t launch_dot(const DotPlan &P, const KParams &K0, const void *a, const
                        OutSpec O, cudaStream_t s) {
     KParams K = K0;
     K.kblk = P.kblk;
+    {  // L2 prefetch of the first chunk before the PDL wait: short streams only (see pdl_enter)
+        const int64_t nvec = (n - P.head) / policy_width(P.policy);
+        const int64_t per_sweep = (int64_t)std::max(P.grid, 1) * policy_block(P.policy) * policy_unroll(P.policy);
+        O.prefetch = nvec <= kPrefetchMaxIters * per_sweep;
+    }
     switch (P.policy) {
     case P_CL32_ALL: return launch_dot_t<ClassicalU32<CL_ALL>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
     case P_CL32_THREAD: return launch_dot_t<ClassicalU32<CL_THREAD>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
@@ -1246,9 +1345,10 @@ static cudaError_t launch_batch_lpr(const KParams &K, const void *A, int64_t lda
     auto kern = vec ? (xs ? batch_kernel<R, NT, U, true, LPR, true> : batch_kernel<R, NT, U, true, LPR, false>)
                     : batch_kernel<R, NT, U, false, LPR, false>;
     occupancy(kern, NT, smem);  // sets the shared-memory opt-in
-    kern<<<(int)std::max<int64_t>(grid, 1), NT, smem, s>>>((const E *)A, lda, (const E *)x, rows, n, K, O);
+    cudaError_t e = launch_pdl(kern, dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(NT), smem, s, (const E *)A, lda,
+                               (const E *)x, rows, n, K, O);
     count_launch();
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <class R, int NT, int U, int LPR>
@@ -1287,6 +1387,7 @@ static cudaError_t launch_batch_t(const KParams &K, const void *A, int64_t lda, 
 
 gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int64_t lda, const void *x, int64_t rows,
                         int64_t n, const gfp_options *opt, OutSpec O, cudaStream_t s, cudaError_t *err) {
+    O.prefetch = 1;  // first row chunk into L2 before the PDL wait (B200 A/B: C5 -1.5%)
     const size_t es = elem_size(I.dtype);
     const bool vec = ((uintptr_t)A % 16 == 0) && ((uintptr_t)x % 16 == 0) && ((lda * (int64_t)es) % 16 == 0);
     const uint64_t pm1 = I.p - 1;
@@ -1339,8 +1440,12 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
                 const size_t smem = (size_t)(((n + 1) / 2 + 3) & ~int64_t(3)) * 4;
                 int bps = occupancy(kern, NT, smem);
                 int64_t grid = std::min<int64_t>((rows + rpb - 1) / rpb, (int64_t)num_sms(dev) * bps);
-                kern<<<(int)std::max<int64_t>(grid, 1), NT, smem, s>>>((const uint16_t *)A, lda, (const uint16_t *)x,
-                                                                       rows, n, K, O);
+                cudaError_t le = launch_pdl(kern, dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(NT), smem, s,
+                                            (const uint16_t *)A, lda, (const uint16_t *)x, rows, n, K, O);
+                if (le != cudaSuccess) {
+                    *err = le;
+                    return GFP_E_CUDA;
+                }
                 count_launch();
                 *err = cudaGetLastError();
             } else if (per_lane * q2 <= max64) {
@@ -1412,18 +1517,19 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
 template <int OP, typename TI, typename TO>
 static cudaError_t launch_conv_t(const KParams &K, const void *in, void *out, int64_t n, const uint16_t *table,
                                  uint32_t entries, cudaStream_t s) {
-    constexpr int NT = 256;
+    constexpr int NT = 256, U = GFP_CONV_U;
     const size_t smem = table ? (size_t)entries * 2 : 0;
-    auto kern = convert_kernel<OP, TI, TO, NT>;
+    auto kern = convert_kernel<OP, TI, TO, NT, U>;
     int bps = occupancy(kern, NT, smem);
     int dev = 0;
     cudaGetDevice(&dev);
     const bool vec = ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0);
     int64_t want = (n / 8 + NT - 1) / NT + 1;
     int64_t grid = std::min<int64_t>(std::max<int64_t>(want, 1), (int64_t)num_sms(dev) * bps);
-    kern<<<(int)grid, NT, smem, s>>>((const TI *)in, (TO *)out, n, vec, K, table, entries);
+    cudaError_t e = launch_pdl(kern, dim3((unsigned)grid), dim3(NT), smem, s, (const TI *)in, (TO *)out, n, vec, K,
+                               table, entries);
     count_launch();
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 gfp_status launch_convert(const gfp_info &I, const KParams &K, int dir, gfp_dtype in_dt, const void *in,

@@ -602,3 +602,70 @@ def test_back_to_back_dots_keep_stream_order():
         g.replay()
         torch.cuda.synchronize()
         assert int(out2.cpu().to(torch.int64)[0]) == want
+
+
+def test_pdl_chains_keep_stream_order():
+    """Conversions, dots and batches are all launched with programmatic dependent launch (early signal,
+    first chunk prefetched into L2 before the wait): every producer -> consumer chain in one stream must
+    still see the producer's writes -- conversion -> dot, in-place to/from conversion, batch output as a
+    dot operand, a dot result inside the next batch's x -- in plain launches and in a CUDA graph."""
+    p = 2 ** 31 - 1
+    n = (1 << 20) + 3
+    a = cu(synth.uniform(SEED, 0, 0, n, p, np.uint32))
+    b = cu(synth.uniform(SEED, 1, 0, n, p, np.uint32))
+    want_m = oracle.to_mont(p, oracle.dot_classical(p, a.cpu().numpy(), b.cpu().numpy()))
+    q, rows, m = 65521, 4099, 512
+    A = cu(synth.uniform(SEED, 2, 0, rows * m, q, np.uint16).reshape(rows, m))
+    xb = cu(synth.uniform(SEED, 3, 0, m, q, np.uint16))
+    z = cu(synth.uniform(SEED, 4, 0, rows, q, np.uint16))
+    u, v = cu(synth.uniform(SEED, 5, 0, 1000, q, np.uint16)), cu(synth.uniform(SEED, 6, 0, 1000, q, np.uint16))
+    r_uv = oracle.dot_classical(q, u.cpu().numpy(), v.cpu().numpy())
+    xh = xb.cpu().numpy().copy()
+    xh[7] = r_uv
+    y_want = oracle.dot_batch_classical(q, A.cpu().numpy(), xh).astype(np.uint16)
+    want_yz = oracle.dot_classical(q, y_want, z.cpu().numpy())
+
+    am, bm = torch.empty_like(a), torch.empty_like(b)
+    t = torch.empty_like(a)
+    y = torch.empty(rows, dtype=torch.uint16, device=DEV)
+    out_m = torch.empty(1, dtype=torch.uint32, device=DEV)
+    out_yz = torch.empty(1, dtype=torch.uint16, device=DEV)
+    s = torch.cuda.Stream()
+
+    def chain():
+        gfp.to_rep(a, p, gfp.MONTGOMERY, out=am, stream=s)
+        gfp.to_rep(b, p, gfp.MONTGOMERY, out=bm, stream=s)
+        gfp.dot(am, bm, p, gfp.MONTGOMERY, out=out_m, stream=s)
+        t.copy_(a)
+        gfp.to_rep(t, p, gfp.MONTGOMERY, out=t, stream=s)
+        gfp.from_rep(t, p, gfp.MONTGOMERY, out=t, stream=s)
+        gfp.dot(u, v, q, gfp.CLASSICAL, out=xb[7:8], stream=s)
+        gfp.dot_batch(A, xb, q, gfp.CLASSICAL, out=y, stream=s)
+        gfp.dot(y, z, q, gfp.CLASSICAL, out=out_yz, stream=s)
+
+    def check():
+        assert int(out_m.cpu().to(torch.int64)[0]) == want_m
+        assert torch.equal(t, a)
+        assert np.array_equal(y.cpu().numpy(), y_want)
+        assert int(out_yz.cpu().to(torch.int64)[0]) == want_yz
+
+    def scrub():
+        for w in (am, bm, t, y, out_m, out_yz):
+            w.zero_()
+        xb[7] = 0
+
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            scrub()
+            chain()
+            s.synchronize()
+            check()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            chain()
+    for _ in range(5):
+        scrub()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        check()
