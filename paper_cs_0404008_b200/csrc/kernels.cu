@@ -736,12 +736,28 @@ __device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab)
     }
 }
 
+#ifndef GFP_CONV_FLAT
+#define GFP_CONV_FLAT 1  // 1: one U-chunk tile per thread, grid not capped at the resident CTAs (no table)
+#endif
+#ifndef GFP_CONV_LD
+#define GFP_CONV_LD 1  // 0: ld.global.cs (streaming), 1: ld.global.L1::no_allocate (coherent: in == out is fine)
+#endif
+#ifndef GFP_CONV_ST
+#define GFP_CONV_ST 0  // 0: st.global.cs (streaming), 1: plain st.global, 2: st.global.L1::no_allocate
+#endif
 template <typename T>
 __device__ __forceinline__ void load8(const T *p, T (&v)[8]) {
     constexpr int NV = 8 * sizeof(T) / 16;
     uint4 r[NV];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) r[i] = __ldcs(reinterpret_cast<const uint4 *>(p) + i);
+    for (int i = 0; i < NV; ++i) {
+        const uint4 *q = reinterpret_cast<const uint4 *>(p) + i;
+        if (GFP_CONV_LD == 0)
+            r[i] = __ldcs(q);
+        else
+            asm volatile("ld.global.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(r[i].x), "=r"(r[i].y), "=r"(r[i].z), "=r"(r[i].w) : "l"(q));
+    }
     memcpy(v, r, sizeof(v));
 }
 template <typename T>
@@ -750,7 +766,16 @@ __device__ __forceinline__ void store8(T *p, const T (&v)[8]) {
     uint4 r[NV];
     memcpy(r, v, sizeof(v));
 #pragma unroll
-    for (int i = 0; i < NV; ++i) __stcs(reinterpret_cast<uint4 *>(p) + i, r[i]);
+    for (int i = 0; i < NV; ++i) {
+        uint4 *q = reinterpret_cast<uint4 *>(p) + i;
+        if (GFP_CONV_ST == 0)
+            __stcs(q, r[i]);
+        else if (GFP_CONV_ST == 1)
+            *q = r[i];
+        else
+            asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};"
+                         :: "l"(q), "r"(r[i].x), "r"(r[i].y), "r"(r[i].z), "r"(r[i].w) : "memory");
+    }
 }
 
 // Elementwise conversion, streaming: each thread holds U chunks of 8 elements (all loads issued before
@@ -883,7 +908,7 @@ static int occupancy(F kernel, int block, size_t smem) {
 #define GFP_DOT_U 4
 #endif
 #ifndef GFP_CONV_U
-#define GFP_CONV_U 2  // B200 A/B: U = 1 / 2 / 4 -> 5.50 / 5.61 / 5.17 TB/s (to_montgomery, 4 GiB)
+#define GFP_CONV_U 2  // B200 A/B, flat grid: U = 1 / 2 / 4 -> 6.97 / 6.94 / 6.60 TB/s (to_montgomery, 4 GiB)
 #endif
 constexpr int kDotNT = 256, kDotU = GFP_DOT_U, kFpU = GFP_FP_U, kZechNT = 1024, kZechU = 2, kZaddNT = 1024, kZaddU = 2;
 constexpr bool kPipe = GFP_DOT_PIPE != 0;
@@ -1524,8 +1549,12 @@ static cudaError_t launch_conv_t(const KParams &K, const void *in, void *out, in
     int dev = 0;
     cudaGetDevice(&dev);
     const bool vec = ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0);
-    int64_t want = (n / 8 + NT - 1) / NT + 1;
-    int64_t grid = std::min<int64_t>(std::max<int64_t>(want, 1), (int64_t)num_sms(dev) * bps);
+    int64_t want = (n / 8 + NT * U - 1) / (NT * U) + 1;
+    // table-free conversions: one tile per thread over the whole input (B200 A/B, profiles/r01_conv_ab.txt:
+    // 6.9 TB/s read + write vs 5.6 TB/s for the resident grid-stride loop); table conversions stage the table
+    // once per CTA, so they keep a resident grid
+    const bool flat = GFP_CONV_FLAT && table == nullptr;
+    int64_t grid = std::min<int64_t>(std::max<int64_t>(want, 1), flat ? (int64_t)INT32_MAX : (int64_t)num_sms(dev) * bps);
     cudaError_t e = launch_pdl(kern, dim3((unsigned)grid), dim3(NT), smem, s, (const TI *)in, (TO *)out, n, vec, K,
                                table, entries);
     count_launch();
