@@ -208,6 +208,34 @@ def to_device(gfp, cfg, h, dev, stream):
                                              "excluded from the dot timing (P:313-320)"}
         del a, b
         return {"a": am, "b": bm}, phases
+    if rep == 3:  # Zech codes <-> residues with the tables staged in shared memory (a2), timed separately
+        res = torch.empty_like(a)
+        back = torch.empty_like(a)
+        with torch.cuda.stream(stream):
+            gfp.from_rep(a, p, rep, out=res, stream=stream)
+            gfp.to_rep(res, p, rep, out=back, stream=stream)
+            stream.synchronize()
+            if not torch.equal(back, a):
+                raise RuntimeError("Zech conversion round trip changed the codes")
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            iters = 5
+            ev[0].record(stream)
+            for _ in range(iters):
+                gfp.from_rep(a, p, rep, out=res, stream=stream)
+                gfp.from_rep(b, p, rep, out=back, stream=stream)
+            ev[1].record(stream)
+            for _ in range(iters):
+                gfp.to_rep(res, p, rep, out=back, stream=stream)
+                gfp.to_rep(res, p, rep, out=back, stream=stream)
+            ev[2].record(stream)
+        stream.synchronize()
+        nbytes = 2 * a.numel() * 2 * a.element_size()
+        for name, ms, what in [("from_zech", ev[0].elapsed_time(ev[1]) / iters, "code c -> g^c (antilog table)"),
+                               ("to_zech", ev[1].elapsed_time(ev[2]) / iters, "residue x -> log_g x (log table)")]:
+            phases[name] = {"ms_per_pair": ms, "GB/s": nbytes / ms / 1e6,
+                            "note": what + " for two operands of u16 (P:126-131), tables in shared memory; "
+                                    "excluded from the dot timing (P:313-320)"}
+        del res, back
     return {"a": a, "b": b}, phases
 
 

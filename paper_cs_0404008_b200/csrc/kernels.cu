@@ -721,7 +721,7 @@ __device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab)
         return (TO)tab[e < K.p ? e : K.p - 1];  // log table; log[0] = 0
     } else if constexpr (OP == C_FROM_ZECH_SMALL) {
         uint32_t c = (uint32_t)v;
-        return (TO)(c == 0 ? 0u : (uint32_t)tab[c]);  // antilog[c] = g^c, c <= 65535 in range
+        return (TO)(c == 0 ? 0u : (uint32_t)tab[min(c, K.qbar)]);  // antilog[c] = g^c; only [0, qbar] is staged
     } else if constexpr (OP == C_FROM_ZECH_LARGE) {
         uint32_t c = (uint32_t)v;
         return (TO)tab[c <= K.qbar ? c : K.qbar];  // antilog[0] = 0 sentinel
@@ -738,6 +738,9 @@ __device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab)
 
 #ifndef GFP_CONV_FLAT
 #define GFP_CONV_FLAT 1  // 1: one U-chunk tile per thread, grid not capped at the resident CTAs (no table)
+#endif
+#ifndef GFP_CONV_WAVES
+#define GFP_CONV_WAVES 1  // resident-grid conversions: grid = waves x the resident CTAs
 #endif
 #ifndef GFP_CONV_LD
 #define GFP_CONV_LD 1  // 0: ld.global.cs (streaming), 1: ld.global.L1::no_allocate (coherent: in == out is fine)
@@ -1542,7 +1545,10 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
 template <int OP, typename TI, typename TO>
 static cudaError_t launch_conv_t(const KParams &K, const void *in, void *out, int64_t n, const uint16_t *table,
                                  uint32_t entries, cudaStream_t s) {
-    constexpr int NT = 256, U = GFP_CONV_U;
+    // table conversions (Zech): 1024-thread CTAs, so that the one or two CTAs whose 64 KB table fits an SM
+    // still keep 2048 threads of loads in flight
+    constexpr bool kTab = OP == C_TO_ZECH || OP == C_FROM_ZECH_SMALL || OP == C_FROM_ZECH_LARGE;
+    constexpr int NT = kTab ? 1024 : 256, U = GFP_CONV_U;
     const size_t smem = table ? (size_t)entries * 2 : 0;
     auto kern = convert_kernel<OP, TI, TO, NT, U>;
     int bps = occupancy(kern, NT, smem);
@@ -1554,7 +1560,8 @@ static cudaError_t launch_conv_t(const KParams &K, const void *in, void *out, in
     // 6.9 TB/s read + write vs 5.6 TB/s for the resident grid-stride loop); table conversions stage the table
     // once per CTA, so they keep a resident grid
     const bool flat = GFP_CONV_FLAT && table == nullptr;
-    int64_t grid = std::min<int64_t>(std::max<int64_t>(want, 1), flat ? (int64_t)INT32_MAX : (int64_t)num_sms(dev) * bps);
+    int64_t grid = std::min<int64_t>(std::max<int64_t>(want, 1),
+                                     flat ? (int64_t)INT32_MAX : (int64_t)GFP_CONV_WAVES * num_sms(dev) * bps);
     cudaError_t e = launch_pdl(kern, dim3((unsigned)grid), dim3(NT), smem, s, (const TI *)in, (TO *)out, n, vec, K,
                                table, entries);
     count_launch();
@@ -1618,10 +1625,10 @@ gfp_status launch_convert(const gfp_info &I, const KParams &K, int dir, gfp_dtyp
             *err = in16 ? launch_conv_t<C_TO_ZECH, uint16_t, uint16_t>(K, in, out, n, K.logt, log_entries, s)
                         : launch_conv_t<C_TO_ZECH, uint32_t, uint16_t>(K, in, out, n, K.logt, log_entries, s);
         } else if (zech_small_layout(I.p)) {
-            *err = out16 ? launch_conv_t<C_FROM_ZECH_SMALL, uint16_t, uint16_t>(K, in, out, n, K.antilog,
-                                                                                  K.antilog_entries, s)
-                         : launch_conv_t<C_FROM_ZECH_SMALL, uint16_t, uint32_t>(K, in, out, n, K.antilog,
-                                                                                  K.antilog_entries, s);
+            // codes are in [0, qbar]: stage only that prefix of the doubled dot table (64 KB, not 128 KB)
+            const uint32_t entries = std::min<uint32_t>(K.antilog_entries, (K.qbar + 1 + 7) & ~7u);
+            *err = out16 ? launch_conv_t<C_FROM_ZECH_SMALL, uint16_t, uint16_t>(K, in, out, n, K.antilog, entries, s)
+                         : launch_conv_t<C_FROM_ZECH_SMALL, uint16_t, uint32_t>(K, in, out, n, K.antilog, entries, s);
         } else {
             *err = out16 ? launch_conv_t<C_FROM_ZECH_LARGE, uint16_t, uint16_t>(K, in, out, n, K.antilog,
                                                                                   K.antilog_entries, s)
