@@ -739,6 +739,9 @@ __device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab)
 #ifndef GFP_CONV_FLAT
 #define GFP_CONV_FLAT 1  // 1: one U-chunk tile per thread, grid not capped at the resident CTAs (no table)
 #endif
+#ifndef GFP_DOT_WAVES
+#define GFP_DOT_WAVES 16  // most waves of resident CTAs for a long table-free dot (see plan_dot)
+#endif
 #ifndef GFP_CONV_WAVES
 #define GFP_CONV_WAVES 1  // resident-grid conversions: grid = waves x the resident CTAs
 #endif
@@ -1240,9 +1243,16 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
     // at least one 16-byte vector per thread before capping at the resident grid: small inputs are
     // latency-bound, so spread them over as many SMs as possible (one DRAM round trip per thread)
     int64_t want = std::max<int64_t>((nvec + NT - 1) / NT, (head + NT - 1) / NT);
-    // (the pure-Zech kernel keeps one workspace slot per CTA after slot 0)
-    int64_t grid = std::min<int64_t>({(int64_t)dev_sms * bps, std::max<int64_t>(want, 1),
-                                      (int64_t)kMaxGrid - (pol == P_ZECH_ADD ? 1 : 0)});
+    // Long table-free streams run several waves of resident CTAs: one wave per 128 MiB of operands, up to
+    // GFP_DOT_WAVES (B200 A/B, profiles/r01_waves_ab.txt: C3's 2 GiB 301 -> 294 us with 16 waves); short
+    // streams keep one wave (C2 at 160 MB: 23.6 us with 1 wave, 24.0 with 2, 36 with 16 -- every CTA ends
+    // with two atomics on one address, and a short kernel's CTAs all end together).  Table kernels stage
+    // their table once per CTA: one wave.  The pure-Zech kernel keeps one workspace slot per CTA after slot 0.
+    const bool tab_kernel = is_zech(pol) || pol == P_ZECH_ADD;
+    const int64_t waves =
+        tab_kernel ? 1 : std::max<int64_t>(1, std::min<int64_t>(GFP_DOT_WAVES, (int64_t)(((u128)n * es * 2) >> 27)));
+    const int64_t cap = tab_kernel ? (int64_t)kMaxGrid - (pol == P_ZECH_ADD ? 1 : 0) : (int64_t)INT32_MAX;
+    int64_t grid = std::min<int64_t>({(int64_t)dev_sms * bps * waves, std::max<int64_t>(want, 1), cap});
     const int64_t threads = grid * NT;
     const int64_t iters = (nvec + threads * U - 1) / (threads * U);
     const u128 per_thread = (u128)iters * U * W + (head + threads - 1) / threads + 1;
