@@ -739,6 +739,9 @@ __device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab)
 #ifndef GFP_CONV_FLAT
 #define GFP_CONV_FLAT 1  // 1: one U-chunk tile per thread, grid not capped at the resident CTAs (no table)
 #endif
+#ifndef GFP_BATCH_WAVES
+#define GFP_BATCH_WAVES 4  // C5 batch grid: waves of resident CTAs (B200 A/B, profiles/r01_waves_ab.txt)
+#endif
 #ifndef GFP_DOT_WAVES
 #define GFP_DOT_WAVES 16  // most waves of resident CTAs for a long table-free dot (see plan_dot)
 #endif
@@ -1477,7 +1480,7 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
                 const int64_t rpb = long_rows ? NT / 32 : NT / 8;  // rows per CTA per sweep
                 const size_t smem = (size_t)(((n + 1) / 2 + 3) & ~int64_t(3)) * 4;
                 int bps = occupancy(kern, NT, smem);
-                int64_t grid = std::min<int64_t>((rows + rpb - 1) / rpb, (int64_t)num_sms(dev) * bps);
+                int64_t grid = std::min<int64_t>((rows + rpb - 1) / rpb, (int64_t)num_sms(dev) * bps * GFP_BATCH_WAVES);
                 cudaError_t le = launch_pdl(kern, dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(NT), smem, s,
                                             (const uint16_t *)A, lda, (const uint16_t *)x, rows, n, K, O);
                 if (le != cudaSuccess) {
