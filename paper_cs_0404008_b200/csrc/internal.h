@@ -23,7 +23,11 @@ struct OutSpec {
     int rep, dtype, mode;
     uint64_t *xchg;     // OUT_XCHG: this rank's exchange buffer (it holds rank, world and the peer table)
     int prefetch;       // set by the launcher: prefetch the first chunk into L2 before griddepcontrol.wait
+    int packed;         // set by the launcher from DotPlan::packed
 };
+// Packed combine: the CTA residues (< p < 2^32) are summed in bits [0, kPackShift), the CTA arrival
+// count in bits [kPackShift, 64): exact for grids below 2^(64 - kPackShift) CTAs.
+constexpr int kPackShift = 48;
 // Exchange-buffer layout (u64 words): [0] this rank's epoch, [1] rank, [2] world; flags at
 // kXFlags + parity * MAXW + r; partial slots at kXSlots + parity * MAXW + r; the peer table (every rank's
 // buffer as mapped in this process) at kXPeers + r.  Kernel parameters stay small: one pointer.
@@ -43,6 +47,7 @@ struct DotPlan {
     int acc_bits;   // m of the accumulator
     uint64_t kblk;  // products per reduction / per wrap test (0: none before the end)
     int64_t per_thread, reductions;  // bounds per thread
+    int packed;     // combine: CTA sums and the arrival count share one word (see dot_kernel)
     const char *name;
 };
 
