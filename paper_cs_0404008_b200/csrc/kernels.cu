@@ -190,7 +190,7 @@ __device__ __forceinline__ void prefetch_l2(const void *ptr) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
 }
 template <int U, int NT>
-__device__ __forceinline__ void pdl_enter(const uint4 *av, const uint4 *bv, int64_t i0, int64_t nvec, bool pf) {
+__device__ __forceinline__ void pdl_prefetch(const uint4 *av, const uint4 *bv, int64_t i0, int64_t nvec, bool pf) {
     if (GFP_PDL_PREFETCH && pf) {
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -199,9 +199,25 @@ __device__ __forceinline__ void pdl_enter(const uint4 *av, const uint4 *bv, int6
                 prefetch_l2(bv + i0 + u * NT);
             }
     }
+}
+__device__ __forceinline__ void pdl_wait() {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // stream order (no-op without a programmatic launch)
     if (GFP_PDL_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+template <int U, int NT>
+__device__ __forceinline__ void pdl_enter(const uint4 *av, const uint4 *bv, int64_t i0, int64_t nvec, bool pf) {
+    pdl_prefetch<U, NT>(av, bv, i0, nvec, pf);
+    pdl_wait();
+}
+// The Zech tables are library-owned device memory, written once (synchronously) when a (device, p) cache
+// entry is built and never by stream work: the table kernels stage them into shared memory BEFORE
+// griddepcontrol.wait, so under PDL the copy overlaps the previous kernel's drain (GFP_STAGE_EARLY).
+#ifndef GFP_STAGE_EARLY
+#define GFP_STAGE_EARLY 1
+#endif
+#ifndef GFP_ZADD_STAGE_EARLY
+#define GFP_ZADD_STAGE_EARLY 0
+#endif
 __device__ __forceinline__ void pdl_exit() {
     if (!GFP_PDL_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after the last write
 }
@@ -228,14 +244,16 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
     const uint4 *av = reinterpret_cast<const uint4 *>(a + head);
     const uint4 *bv = reinterpret_cast<const uint4 *>(b + head);
     int64_t i0 = (int64_t)blockIdx.x * (NT * U) + threadIdx.x;
-    pdl_enter<U, NT>(av, bv, i0, nvec, Prefetches<R>::value && O.prefetch != 0);
+    pdl_prefetch<U, NT>(av, bv, i0, nvec, Prefetches<R>::value && O.prefetch != 0);
+    if constexpr (R::kTable && GFP_STAGE_EARLY) stage_table(s_tab, K.antilog, K.antilog_entries);
+    pdl_wait();
     const int64_t step = (int64_t)gridDim.x * (NT * U);
     const uint16_t *tab = nullptr;
 
     // Software-pipelined stream (PIPE): the U loads of each operand for step k+1 are in flight while
     // step k computes, so every thread keeps between U and 2U 16-byte loads outstanding per operand.
-    // The first loads are issued before the Zech antilog table is staged, so the stream's DRAM latency
-    // overlaps the table copy from L2 into shared memory.
+    // Without GFP_STAGE_EARLY the first loads are issued before the Zech antilog table is staged, so the
+    // stream's DRAM latency overlaps the table copy from L2 into shared memory.
     uint4 ca[U], cb[U];
     bool have = PIPE && i0 + (U - 1) * NT < nvec;
     if (PIPE && have) {
@@ -246,7 +264,7 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
         }
     }
     if constexpr (R::kTable) {
-        stage_table(s_tab, K.antilog, K.antilog_entries);
+        if (!GFP_STAGE_EARLY) stage_table(s_tab, K.antilog, K.antilog_entries);
         __syncthreads();
         tab = s_tab;
     }
@@ -441,7 +459,12 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
     const uint4 *av = reinterpret_cast<const uint4 *>(a + head);
     const uint4 *bv = reinterpret_cast<const uint4 *>(b + head);
     int64_t i0 = (int64_t)blockIdx.x * (NT * U) + threadIdx.x;
-    pdl_enter<U, NT>(av, bv, i0, nvec, O.prefetch != 0);
+    pdl_prefetch<U, NT>(av, bv, i0, nvec, O.prefetch != 0);
+    // (staging this table before the wait, as the other table kernels do, was 1% slower here: B200 A/B,
+    // profiles/r01_pdl_ab.txt; its first loads go out before the staging instead)
+    if (GFP_ZADD_STAGE_EARLY)
+        stage_table(s_delta, FAST ? K.zplus1s : K.zplus1, FAST ? K.zplus1s_entries : K.zplus1_entries);
+    pdl_wait();
     const int64_t step = (int64_t)gridDim.x * (NT * U);
 
     // first loads in flight while the table is staged from L2
@@ -454,7 +477,8 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
             cb[u] = ld_stream(bv + i0 + u * NT);
         }
     }
-    stage_table(s_delta, FAST ? K.zplus1s : K.zplus1, FAST ? K.zplus1s_entries : K.zplus1_entries);
+    if (!GFP_ZADD_STAGE_EARLY)
+        stage_table(s_delta, FAST ? K.zplus1s : K.zplus1, FAST ? K.zplus1s_entries : K.zplus1_entries);
     const uint32_t kzero = 2u * q + 2u;  // fast path: byte offset of the "add nothing" entry
     __syncthreads();
     const uint16_t *D = s_delta;
@@ -656,12 +680,13 @@ __global__ void __launch_bounds__(NT) batch_kernel(const typename R::elem *__res
                                                    const typename R::elem *__restrict__ x, int64_t rows,
                                                    int64_t n, KParams K, OutSpec O) {
     extern __shared__ __align__(16) uint16_t s_tab[];
+    if constexpr (R::kTable && GFP_STAGE_EARLY) stage_table(s_tab, K.antilog, K.antilog_entries);  // library-owned
     batch_pdl_enter<U, LPR, NT>(A, lda * (int64_t)sizeof(typename R::elem) / 2, rows, VEC ? n / R::W : 0,
                                 O.prefetch != 0);
     const uint16_t *tab = nullptr;
     const uint32_t tab_bytes = R::kTable ? ((K.antilog_entries * 2 + 15) & ~15u) : 0;
     if constexpr (R::kTable) {
-        stage_table(s_tab, K.antilog, K.antilog_entries);
+        if (!GFP_STAGE_EARLY) stage_table(s_tab, K.antilog, K.antilog_entries);
         tab = s_tab;
     }
     // XS: x staged once per CTA in shared memory (16-byte vectors; every row reuses it)
@@ -817,11 +842,11 @@ __global__ void __launch_bounds__(NT) convert_kernel(const TI *in, TO *out, int6
     const int64_t nchunk = vec_ok ? n / 8 : 0;
     int64_t c0 = (int64_t)blockIdx.x * (NT * U) + threadIdx.x;
     const int64_t step = (int64_t)gridDim.x * (NT * U);
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // stream order (launch_pdl; no prefetch: a long stream)
-    if (GFP_PDL_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (GFP_STAGE_EARLY && table != nullptr) stage_table(s_tab, table, table_entries);  // library-owned table
+    pdl_wait();  // stream order (launch_pdl; no prefetch: a long stream)
     const uint16_t *tab = nullptr;
     if (table != nullptr) {
-        stage_table(s_tab, table, table_entries);
+        if (!GFP_STAGE_EARLY) stage_table(s_tab, table, table_entries);
         __syncthreads();
         tab = s_tab;
     }
