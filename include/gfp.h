@@ -50,6 +50,11 @@
  * on `stream` and return; results are ready in stream order.  They never
  * allocate on the hot path after the first call for a (device, p, rep,
  * stream) and are safe to capture in a CUDA graph after that first call.
+ * Kernels are launched with programmatic stream serialization (PDL): the next
+ * launch is staged while the previous kernel drains.  Before waiting on the
+ * stream's earlier work a kernel touches only library-owned tables and issues
+ * L2 prefetches (which cannot observe stale data); every load of caller memory
+ * comes after the wait, so results are exactly those of plain stream order.
  *
  * Preconditions.  Entries must be canonical elements of the representation
  * (P:49-50).  This is not checked on the hot path: non-canonical entries give
