@@ -8,8 +8,9 @@
 
 namespace gfp {
 
-// Per-(device, stream) scratch for the single-launch combine: the u64 sum of CTA contributions
-// (partials[0]) and the last-CTA-done counter, both self-resetting, so no memset per call.
+// Per-(device, stream) scratch for the single-launch combine, self-resetting (no memset per call):
+// dot_kernel packs the CTA residues and their arrival count into partials[0]; the pure-Zech kernel keeps
+// one Zech value per CTA in partials[1 ..] and counts arrivals in `counter`.
 struct Workspace {
     uint64_t *partials;
     unsigned int *counter;
@@ -23,7 +24,6 @@ struct OutSpec {
     int rep, dtype, mode;
     uint64_t *xchg;     // OUT_XCHG: this rank's exchange buffer (it holds rank, world and the peer table)
     int prefetch;       // set by the launcher: prefetch the first chunk into L2 before griddepcontrol.wait
-    int packed;         // set by the launcher from DotPlan::packed
 };
 // Packed combine: the CTA residues (< p < 2^32) are summed in bits [0, kPackShift), the CTA arrival
 // count in bits [kPackShift, 64): exact for grids below 2^(64 - kPackShift) CTAs.
@@ -47,7 +47,6 @@ struct DotPlan {
     int acc_bits;   // m of the accumulator
     uint64_t kblk;  // products per reduction / per wrap test (0: none before the end)
     int64_t per_thread, reductions;  // bounds per thread
-    int packed;     // combine: CTA sums and the arrival count share one word (see dot_kernel)
     const char *name;
 };
 

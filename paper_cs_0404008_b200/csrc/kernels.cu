@@ -319,11 +319,12 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
     // once and encodes -- "A single machine remaindering is needed at the end".
     // Exact and order-independent: integer sums, no wrap (host-checked bounds).
     const uint64_t v = block_sum(R::finish(acc, K), red);
-    if (threadIdx.x == 0 && O.packed) {
-        // Packed combine (grid < 2^(64 - kPackShift), host-checked): the CTA's sum is reduced to its residue
-        // c < p < 2^32, and ONE atomic adds c and one arrival to a single word; the CTA that sees every other
-        // arrival in the old value holds the complete total -- one L2 round trip instead of three (sum,
-        // acq_rel counter, reload).  The word holds nothing but the sums, so relaxed order suffices.
+    if (threadIdx.x == 0) {
+        // Packed combine (the plan keeps grids below 2^(64 - kPackShift) CTAs): the CTA's sum is reduced to its
+        // residue c < p < 2^32 (centered sums are signed two's complement: smod_p), and ONE atomic adds c and
+        // one arrival to a single word; the CTA that sees every other arrival in the old value holds the
+        // complete total -- one L2 round trip, where a sum atomic + acq_rel counter + reload took three.  The
+        // word holds nothing but the sums, so relaxed order suffices.
         const uint64_t c = O.rep == GFP_REP_CENTERED ? smod_p((int64_t)v, K) : mod_p(v, K.p, K.mu);
         unsigned long long *word = reinterpret_cast<unsigned long long *>(ws.partials);
         unsigned long long old;
@@ -334,22 +335,6 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
             if (O.mode == OUT_XCHG) r = xchg_allreduce(r, O.xchg, K.p, K.mu);  // fused multi-GPU combine
             write_result(r, O, K, 0);
             *word = 0;  // self-reset for the next launch on this stream
-        }
-        pdl_exit();
-    } else if (threadIdx.x == 0) {
-        unsigned long long *sum = reinterpret_cast<unsigned long long *>(ws.partials);
-        atomicAdd(sum, (unsigned long long)v);
-        unsigned int t;
-        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(ws.counter) : "memory");
-        if (t == gridDim.x - 1) {
-            unsigned long long s;
-            asm volatile("ld.relaxed.gpu.u64 %0, [%1];" : "=l"(s) : "l"(sum) : "memory");
-            // centered sums are signed (two's complement, |total| < 2^63 by the host's bound)
-            uint64_t r = O.rep == GFP_REP_CENTERED ? smod_p((int64_t)s, K) : mod_p(s, K.p, K.mu);
-            if (O.mode == OUT_XCHG) r = xchg_allreduce(r, O.xchg, K.p, K.mu);  // fused multi-GPU combine
-            write_result(r, O, K, 0);
-            *sum = 0;  // self-reset for the next launch on this stream
-            *ws.counter = 0;
         }
         pdl_exit();
     }
@@ -781,9 +766,6 @@ __device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab)
 #ifndef GFP_CONV_FLAT
 #define GFP_CONV_FLAT 1  // 1: one U-chunk tile per thread, grid not capped at the resident CTAs (no table)
 #endif
-#ifndef GFP_PACKED_COMBINE
-#define GFP_PACKED_COMBINE 1  // one-atomic combine of CTA residues and arrivals (dot_kernel)
-#endif
 #ifndef GFP_BATCH_WAVES
 #define GFP_BATCH_WAVES 4  // C5 batch grid: waves of resident CTAs (B200 A/B, profiles/r01_waves_ab.txt)
 #endif
@@ -1081,7 +1063,6 @@ cudaError_t launch_dot(const DotPlan &P, const KParams &K0, const void *a, const
         const int64_t per_sweep = (int64_t)std::max(P.grid, 1) * policy_block(P.policy) * policy_unroll(P.policy);
         O.prefetch = nvec <= kPrefetchMaxIters * per_sweep;
     }
-    O.packed = P.packed;
     switch (P.policy) {
     case P_CL32_ALL: return launch_dot_t<ClassicalU32<CL_ALL>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
     case P_CL32_THREAD: return launch_dot_t<ClassicalU32<CL_THREAD>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
@@ -1301,7 +1282,9 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
     const int64_t waves =
         tab_kernel ? 1 : std::max<int64_t>(1, std::min<int64_t>(GFP_DOT_WAVES, (int64_t)(((u128)n * es * 2) >> 27)));
     const int64_t cap = tab_kernel ? (int64_t)kMaxGrid - (pol == P_ZECH_ADD ? 1 : 0) : (int64_t)INT32_MAX;
-    int64_t grid = std::min<int64_t>({(int64_t)dev_sms * bps * waves, std::max<int64_t>(want, 1), cap});
+    // (dot_kernel's packed combine counts CTA arrivals in 64 - kPackShift bits)
+    int64_t grid = std::min<int64_t>({(int64_t)dev_sms * bps * waves, std::max<int64_t>(want, 1), cap,
+                                      ((int64_t)1 << (64 - kPackShift)) - 1});
     const int64_t threads = grid * NT;
     const int64_t iters = (nvec + threads * U - 1) / (threads * U);
     const u128 per_thread = (u128)iters * U * W + (head + threads - 1) / threads + 1;
@@ -1403,8 +1386,6 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
     P->kblk = kblk;
     P->per_thread = (int64_t)per_thread;
     P->reductions = reductions;
-    // packed one-atomic combine (dot_kernel) whenever the arrival count fits its field
-    P->packed = GFP_PACKED_COMBINE && pol != P_ZECH_ADD && grid < ((int64_t)1 << (64 - kPackShift));
     P->name = policy_name(pol);
     return GFP_OK;
 }
