@@ -291,6 +291,17 @@ int main(int argc, char **argv) {
     LDG(256, 2, 0, 80)
     LDG(256, 1, 0, 160)
     LDG(512, 4, 0, 80)
+    // waves x unroll x block (second pass)
+    LDG(256, 2, 0, 4)
+    LDG(256, 8, 0, 4)
+    LDG(256, 8, 0, 16)
+    LDG(256, 2, 0, 16)
+    LDG(512, 4, 0, 4)
+    LDG(512, 4, 0, 16)
+    LDG(128, 4, 0, 16)
+    LDG(256, 4, 0, 32)
+    LDG(256, 4, 4, 16)
+    LDG(256, 4, 2, 16)
 #define LDG256(NT, U)                                                                                     \
     {                                                                                                     \
         int bps;                                                                                          \
