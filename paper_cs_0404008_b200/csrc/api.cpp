@@ -111,7 +111,8 @@ gfp_status get_ctx(uint64_t p, gfp_rep rep, gfp_dtype dt, Ctx **out) {
         // 2 delta[e mod qbar], index 2 qbar + 1 the "add nothing" 0
         const bool scaled = zech_small_layout(p);
         const uint64_t qbar = p - 1;
-        std::vector<uint16_t> delta2(scaled ? ((2 * qbar + 2 + 7) & ~uint64_t(7)) : 0, 0);
+        // padded to 2^16 entries: any byte offset 2 L - s (L a 16-bit lane, s even) stays inside
+        std::vector<uint16_t> delta2(scaled ? 65536 : 0, 0);
         for (uint64_t e = 0; scaled && e <= 2 * qbar; ++e) {
             const uint16_t v = delta[e % qbar];
             delta2[e] = v == kZechDeltaZero ? v : (uint16_t)(2 * v);
@@ -374,7 +375,7 @@ gfp_status gfp_plan(uint64_t p, gfp_rep rep, gfp_dtype dt, int64_t n, const gfp_
     K.p = p;
     K.antilog_entries = (uint32_t)((I.table_bytes / 2 + 7) & ~uint64_t(7));
     K.zplus1_entries = (uint32_t)((p + 1 + 7) & ~uint64_t(7));  // qbar + 2 = p + 1 entries
-    K.zplus1s_entries = (uint32_t)((2 * (p - 1) + 2 + 7) & ~uint64_t(7));
+    K.zplus1s_entries = 65536;  // the fast pure-Zech table, padded (see zech context setup)
     DotPlan plan;
     const void *aligned_ptr = (const void *)(uintptr_t)4096;
     if ((st = plan_dot(I, K, aligned_ptr, aligned_ptr, n, opt, &plan)) != GFP_OK) return plan_fail(st);

@@ -394,8 +394,8 @@ __device__ __forceinline__ void zech_add_vec(uint32_t (&acc)[8], uint4 x, uint4 
 __device__ __forceinline__ uint32_t zech_fast_add(uint32_t s, uint32_t lane_sum, bool zero, uint32_t q,
                                                   uint32_t kzero, uint32_t tab) {
     uint32_t k = 2u * lane_sum - s;  // 2 (ci + cj) - s in (4 - q, 2q] for canonical codes
-    k = min(min(k, k + q), 2u * q);   // the clamp keeps non-canonical codes inside the table (gfp.h)
-    k = zero ? kzero : k;
+    k = min(k, k + q);                // in [0, 2^17 - 2] for any 16-bit lane: the staged table is padded to
+    k = zero ? kzero : k;             // 2^16 entries, so non-canonical codes never leave it (gfp.h)
     uint16_t d;
     asm("ld.shared.u16 %0, [%1];" : "=h"(d) : "r"(tab + k));
     return zadd::Ops<2>::fold(s + d, q);
@@ -474,29 +474,31 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
         acc[j] = FAST ? 0u : Z::kZ;  // fast path: start at the element 1 (v = 0), booked as -1 in corr
         if (FAST) corr = Z::add(corr, q / 2u, q, D);
     }
-    while (have) {
+    // Two register sets in ping-pong (no copies between iterations): while one set is consumed, the
+    // loads of the next step land in the other.
+    uint4 na[U], nb[U];
+    auto step_once = [&](uint4 (&cx)[U], uint4 (&cy)[U], uint4 (&nx_a)[U], uint4 (&nx_b)[U]) {
         const int64_t nx = i0 + step;
         const bool more = nx + (U - 1) * NT < nvec;
-        uint4 na[U], nb[U];
         if (more) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                na[u] = ld_stream(av + nx + u * NT);
-                nb[u] = ld_stream(bv + nx + u * NT);
+                nx_a[u] = ld_stream(av + nx + u * NT);
+                nx_b[u] = ld_stream(bv + nx + u * NT);
             }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if constexpr (FAST) zech_fast_vec(acc, corr, ca[u], cb[u], q, kzero, D);
-            else zech_add_vec<S>(acc, ca[u], cb[u], q, D);
+            if constexpr (FAST) zech_fast_vec(acc, corr, cx[u], cy[u], q, kzero, D);
+            else zech_add_vec<S>(acc, cx[u], cy[u], q, D);
         }
         i0 = nx;
         have = more;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            ca[u] = na[u];
-            cb[u] = nb[u];
-        }
+    };
+    while (have) {
+        step_once(ca, cb, na, nb);
+        if (!have) break;
+        step_once(na, nb, ca, cb);
     }
     // ragged vectors (< U per thread), scalar head and tail
     for (int u = 0; u < U; ++u) {

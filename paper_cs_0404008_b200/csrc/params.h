@@ -18,8 +18,8 @@ struct KParams {
     const uint16_t *logt;     // Zech log table (global; read once by the finaliser)
     uint32_t antilog_entries;
     const uint16_t *zplus1;   // Zech t_plus1 table in exponent form (numtheory.h zech_plus1_delta), global
-    const uint16_t *zplus1s;  // small fields: 2 delta[e mod qbar] for e in [0, 2 qbar], then one 0 entry
-    uint32_t zplus1s_entries; // 2 qbar + 2, padded to a multiple of 8
+    const uint16_t *zplus1s;  // small fields: 2 delta[e mod qbar] for e in [0, 2 qbar], then 0 entries
+    uint32_t zplus1s_entries; // 65536 (padding: any 16-bit lane sum indexes inside)
     uint32_t zplus1_entries;  // qbar + 1, padded to a multiple of 8
     // explicit-strategy kernels (gfp_dot_ex): block length for BLOCKED / HYBRID, 32-bit constants
     uint64_t kblk;
