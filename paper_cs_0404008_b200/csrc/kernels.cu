@@ -269,26 +269,27 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
         tab = s_tab;
     }
     if constexpr (PIPE) {
-        while (have) {
+        // two register sets in ping-pong: the next step's loads land in the set not being consumed
+        uint4 na[U], nb[U];
+        auto step_once = [&](uint4 (&cx)[U], uint4 (&cy)[U], uint4 (&nx_a)[U], uint4 (&nx_b)[U]) {
             const int64_t nx = i0 + step;
             const bool more = nx + (U - 1) * NT < nvec;
-            uint4 na[U], nb[U];
             if (more) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    na[u] = ld_stream(av + nx + u * NT);
-                    nb[u] = ld_stream(bv + nx + u * NT);
+                    nx_a[u] = ld_stream(av + nx + u * NT);
+                    nx_b[u] = ld_stream(bv + nx + u * NT);
                 }
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) R::vec(acc, ca[u], cb[u], K, tab);
+            for (int u = 0; u < U; ++u) R::vec(acc, cx[u], cy[u], K, tab);
             i0 = nx;
             have = more;
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                ca[u] = na[u];
-                cb[u] = nb[u];
-            }
+        };
+        while (have) {
+            step_once(ca, cb, na, nb);
+            if (!have) break;
+            step_once(na, nb, ca, cb);
         }
     }
 
