@@ -459,11 +459,22 @@ def main():
     if args.sweep:
         return prime_sweep(args)
 
+    # GFP_BENCH_PG_BACKEND=gloo with --combine nccl: a host-logic check of the multi-rank bench on a box with
+    # fewer GPUs than ranks (ranks share devices; no kernel ever waits on another rank's kernel).  Production
+    # runs use NCCL, one GPU per rank.
+    backend = os.environ.get("GFP_BENCH_PG_BACKEND", "nccl")
+    ndev = torch.cuda.device_count()
+    if local >= ndev and not (backend == "gloo" and args.combine == "nccl"):
+        raise SystemExit(f"rank {rank}: LOCAL_RANK {local} but only {ndev} GPUs visible")
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         group = dist.group.WORLD
     import paper_cs_0404008_b200 as gfp
 
