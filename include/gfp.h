@@ -286,7 +286,8 @@ gfp_status gfp_dot_host(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, co
  *
  * GFP_STRAT_AUTO (gfp_dot, gfp_dot_batch, gfp_dot_partial, gfp_dot_ex / _batch_ex / gfp_plan with a NULL
  * or all-zero gfp_options) then follows the table: among the entries with the call's (rep, dtype, kind)
- * it takes the one nearest in (log2 p, log2 n) (L1 distance; first entry on ties) and uses its strategy
+ * it takes the one nearest in (log2 p, log2 n), and log2 rows for batches (L1 distance; first entry on
+ * ties) and uses its strategy
  * if that strategy is admissible for the call's (p, n); otherwise -- or with an empty table -- the
  * built-in analytic plan.  On the first AUTO call of a process the library loads a table (gfp_tune_save
  * format) from the file the environment variable GFP_TUNE_FILE names ("" = none), or, when it is unset,

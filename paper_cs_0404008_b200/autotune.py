@@ -26,7 +26,7 @@ ZECH_PRIMES = [32749, 65521]
 
 def default_cases(quick: bool = False) -> list:
     ns = [1 << 12, 1 << 20] if quick else [1 << 12, 1 << 16, 1 << 20, 1 << 24]
-    batches = [(1 << 14, 512)] if quick else [(1 << 15, 512), (1 << 12, 4096)]
+    batches = [(1 << 14, 512)] if quick else [(1 << 15, 512), (1 << 12, 4096), (1 << 16, 4096)]
     cases = []
 
     def add(rep, primes, dtype=None, batch=True):

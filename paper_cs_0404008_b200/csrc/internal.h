@@ -75,7 +75,7 @@ cudaError_t launch_fill(void *out, int dtype, uint64_t p, uint64_t seed, int64_t
 
 // Install-time tuning table (tune.cpp): the tuned explicit options for an AUTO call of `kind` (0 dot,
 // 1 batch) with n terms (per row), or false (empty table, the built-in plan won, or tuning bypassed).
-bool tuned_options(const gfp_info &info, int kind, int64_t n, gfp_options *out);
+bool tuned_options(const gfp_info &info, int kind, int64_t n, int64_t rows, gfp_options *out);
 void count_launch();
 
 }  // namespace gfp

@@ -1237,7 +1237,7 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
                     const gfp_options *opt, DotPlan *P) {
     gfp_options tuned;  // AUTO follows the install-time table when it has an admissible entry (F4)
     if ((opt == nullptr || (opt->strategy == GFP_STRAT_AUTO && opt->acc_bits == 0)) &&
-        tuned_options(I, 0, n, &tuned) && plan_dot(I, K, a, b, n, &tuned, P) == GFP_OK)
+        tuned_options(I, 0, n, 0, &tuned) && plan_dot(I, K, a, b, n, &tuned, P) == GFP_OK)
         return GFP_OK;
     const size_t es = elem_size(I.dtype);
     const uint64_t pm1 = I.p - 1;
@@ -1471,7 +1471,7 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
     *err = cudaSuccess;
     gfp_options tuned;  // AUTO follows the install-time table when it has an admissible entry (F4)
     if ((opt == nullptr || (opt->strategy == GFP_STRAT_AUTO && opt->acc_bits == 0)) &&
-        tuned_options(I, 1, n, &tuned)) {
+        tuned_options(I, 1, n, rows, &tuned)) {
         int xpol = -1, acc_bits = 0;
         uint64_t kblk = 0;
         if (resolve_strategy(I, n, &tuned, &xpol, &kblk, &acc_bits) == GFP_OK && xpol >= 0 && xpol != P_ZECH_ADD)

@@ -129,16 +129,19 @@ void ensure_loaded() {
 }
 }  // namespace
 
-bool tuned_options(const gfp_info &I, int kind, int64_t n, gfp_options *out) {
+bool tuned_options(const gfp_info &I, int kind, int64_t n, int64_t rows, gfp_options *out) {
     if (t_bypass) return false;
     std::lock_guard<std::mutex> g(g_mu);
     ensure_loaded();
     const gfp_tune_entry *best = nullptr;
     double bd = 0;
-    const double lp = std::log2((double)I.p), ln = std::log2((double)std::max<int64_t>(n, 1));
+    auto l2 = [](int64_t v) { return std::log2((double)std::max<int64_t>(v, 1)); };
+    const double lp = std::log2((double)I.p), ln = l2(n), lr = l2(rows);
     for (const auto &e : g_table) {
         if (e.rep != I.rep || e.dtype != I.dtype || e.kind != kind) continue;
-        const double d = std::fabs(std::log2((double)e.p) - lp) + std::fabs(std::log2((double)std::max<int64_t>(e.n, 1)) - ln);
+        // nearest in (log p, log n) and, for batches, log rows (a winner at 4096 rows need not hold at 65536)
+        const double d = std::fabs(std::log2((double)e.p) - lp) + std::fabs(l2(e.n) - ln) +
+                         (kind == 1 ? std::fabs(l2(e.rows) - lr) : 0.0);
         if (!best || d < bd) {
             best = &e;
             bd = d;
