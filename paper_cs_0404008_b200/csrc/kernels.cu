@@ -769,6 +769,12 @@ __device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab)
 #ifndef GFP_CONV_FLAT
 #define GFP_CONV_FLAT 1  // 1: one U-chunk tile per thread, grid not capped at the resident CTAs (no table)
 #endif
+#ifndef GFP_ZBATCH_U
+#define GFP_ZBATCH_U 4  // 16-byte vectors per lane in flight in the Zech batch (doubled table)
+#endif
+#ifndef GFP_ZBATCH_UL
+#define GFP_ZBATCH_UL 8  // the same for the large-field (q-entry, folded index) table
+#endif
 #ifndef GFP_ZECH_U
 #define GFP_ZECH_U 2  // 16-byte vectors per operand per step of the integer Zech dot
 #endif
@@ -1557,10 +1563,12 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
             *err = launch_batch_t<Fp64<1>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
         break;
     case GFP_REP_ZECH:
+        // bound by the shared-memory gather (one random lookup per 2-byte term: ~2 T lookups/s on B200);
+        // unroll A/B (scripts/ab_zbatch.py): U = 4 for the doubled table, 8 for the folded large-field one
         if (zech_small_layout(I.p))
-            *err = launch_batch_t<Zech<true, false>, 1024, 2>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Zech<true, false>, 1024, GFP_ZBATCH_U>(K, A, lda, x, rows, n, vec, O, s);
         else
-            *err = launch_batch_t<Zech<false, false>, 1024, 2>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Zech<false, false>, 1024, GFP_ZBATCH_UL>(K, A, lda, x, rows, n, vec, O, s);
         break;
     case GFP_REP_CENTERED: {  // sec. 3.2.2: per-row sums; one reduction per lane unless a row overflows
         const u128 h = (u128)(I.p - 1) / 2, h2 = h * h, w63 = ((u128)1 << 63) - 1;
