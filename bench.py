@@ -8,8 +8,9 @@ the default workload is BASELINE.json configs[2] -- GF(2^31-1), Montgomery B = 2
 operand, sharded over N GPUs (strong scaling: the total n is fixed), converted to Montgomery form on
 device before timing (the paper excludes conversions from dot timings; the conversion is
 timed separately and reported under "phases").  At N = 1 a step is one gfp_dot launch (delayed-modulus
-streaming + last-CTA-done reduction and encoding); at N > 1 it is gfp_dot_partial, one NCCL all_reduce
-of the int64 partial residue, and gfp_finalize.
+streaming + last-CTA-done reduction and encoding); at N > 1 it is one gfp_dot_allreduce launch per rank
+(the shard dot whose last CTA exchanges the partial with the peers over NVLink peer memory and encodes;
+--combine nccl: gfp_dot_partial, one NCCL all_reduce of the int64 partial residue, and gfp_finalize).
 
 `value` = total terms / max-over-ranks device time (CUDA events on the launching stream, barrier and
 synchronize on both sides).  The inputs (1 GiB per operand at N = 1) exceed the 126 MB L2, so no flush
