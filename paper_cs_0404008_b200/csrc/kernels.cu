@@ -784,6 +784,9 @@ __device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab)
 #ifndef GFP_DOT_WAVES
 #define GFP_DOT_WAVES 16  // most waves of resident CTAs for a long table-free dot (see plan_dot)
 #endif
+#ifndef GFP_WAVE_LOG2
+#define GFP_WAVE_LOG2 25  // one wave per 2^25 bytes (32 MiB) of operands (plan_dot)
+#endif
 #ifndef GFP_CONV_WAVES
 #define GFP_CONV_WAVES 1  // resident-grid conversions: grid = waves x the resident CTAs
 #endif
@@ -1285,14 +1288,16 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
     // at least one 16-byte vector per thread before capping at the resident grid: small inputs are
     // latency-bound, so spread them over as many SMs as possible (one DRAM round trip per thread)
     int64_t want = std::max<int64_t>((nvec + NT - 1) / NT, (head + NT - 1) / NT);
-    // Long table-free streams run several waves of resident CTAs: one wave per 128 MiB of operands, up to
-    // GFP_DOT_WAVES (B200 A/B, profiles/r01_waves_ab.txt: C3's 2 GiB 301 -> 294 us with 16 waves); short
-    // streams keep one wave (C2 at 160 MB: 23.6 us with 1 wave, 24.0 with 2, 36 with 16 -- every CTA ends
-    // with two atomics on one address, and a short kernel's CTAs all end together).  Table kernels stage
-    // their table once per CTA: one wave.  The pure-Zech kernel keeps one workspace slot per CTA after slot 0.
+    // Long table-free streams run several waves of resident CTAs: one wave per 2^GFP_WAVE_LOG2 bytes of
+    // operands, up to GFP_DOT_WAVES (B200 A/B, profiles/r01_waves_ab.txt: C3's 2 GiB 301 -> 291 us with 16
+    // waves, C2's 160 MB 22.9 -> 22.1 us with 4); every CTA ends with one packed atomic on one word, so very
+    // many CTAs of a short kernel ending together would queue on it.  Centered (signed) dots finish each
+    // thread with a signed reduction and keep one wave per 128 MiB.  Table kernels stage their table once per
+    // CTA: one wave.  The pure-Zech kernel keeps one workspace slot per CTA after slot 0.
     const bool tab_kernel = is_zech(pol) || pol == P_ZECH_ADD;
+    const int wave_log2 = I.rep == GFP_REP_CENTERED ? 27 : GFP_WAVE_LOG2;
     const int64_t waves =
-        tab_kernel ? 1 : std::max<int64_t>(1, std::min<int64_t>(GFP_DOT_WAVES, (int64_t)(((u128)n * es * 2) >> 27)));
+        tab_kernel ? 1 : std::max<int64_t>(1, std::min<int64_t>(GFP_DOT_WAVES, (int64_t)(((u128)n * es * 2) >> wave_log2)));
     const int64_t cap = tab_kernel ? (int64_t)kMaxGrid - (pol == P_ZECH_ADD ? 1 : 0) : (int64_t)INT32_MAX;
     // (dot_kernel's packed combine counts CTA arrivals in 64 - kPackShift bits)
     int64_t grid = std::min<int64_t>({(int64_t)dev_sms * bps * waves, std::max<int64_t>(want, 1), cap,
