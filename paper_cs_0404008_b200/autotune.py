@@ -49,13 +49,21 @@ def main(argv=None) -> int:
     ap.add_argument("--out", default="gfp_tune.txt")
     ap.add_argument("--quick", action="store_true", help="a small grid (CI / smoke)")
     ap.add_argument("--ms", type=float, default=20.0, help="milliseconds of timing per candidate")
+    ap.add_argument("--min-gain", type=float, default=1.05,
+                    help="keep a tuned strategy only if it beats the built-in plan by this factor; below it the "
+                         "entry records AUTO, so run-to-run noise at the tuning sizes does not switch kernels")
     args = ap.parse_args(argv)
     torch.cuda.set_device(0)
     gfp.tune_clear()
     table = gfp.tune(default_cases(args.quick), ms_per_candidate=args.ms)
-    gfp.tune_save(args.out)
     for e in table:
         e["speedup_vs_builtin"] = e["us_builtin"] / e["us_best"] if e["us_best"] > 0 else None
+        e["measured_winner"] = e["strategy_name"]
+        if e["strategy"] != gfp.AUTO and (e["speedup_vs_builtin"] or 0) < args.min_gain:
+            e.update(strategy=gfp.AUTO, acc_bits=0, us_best=e["us_builtin"], strategy_name="auto")
+    gfp.tune_set(table)
+    gfp.tune_save(args.out)
+    for e in table:
         print(json.dumps(e), flush=True)
     return 0
 
