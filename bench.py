@@ -337,6 +337,19 @@ def sum_over_ranks(x, world):
     return float(t.item())
 
 
+def kernel_name(gfp, cfg, terms):
+    """The kernel AUTO runs for this workload (gfp_plan: the plan a dot of `terms` elements gets)."""
+    if cfg["kind"] == "batch":
+        return "batch_cl16_kernel" if cfg["rep"] == 0 and np.dtype(cfg["dtype"]) == np.uint16 else "batch_kernel"
+    try:
+        tdt = {np.dtype(np.uint16): torch.uint16, np.dtype(np.uint32): torch.uint32,
+               np.dtype(np.float64): torch.float64}[np.dtype(cfg["dtype"])]
+        pl = gfp.plan(cfg["p"], cfg["rep"], int(terms), dtype=tdt, strategy=cfg.get("strategy", 0))
+        return f"{pl['kernel']} (grid {pl['grid']})"
+    except Exception:  # noqa: BLE001 -- the label is informative only
+        return cfg["name"]
+
+
 # ------------------------------------------------------------------------------ oracle legs
 def host_threads():
     try:
@@ -512,7 +525,7 @@ def main():
     achieved = local_bytes / (kern_avg / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic_lookup(cfg["name"], world),
-            "kernel": "dot_kernel<Montgomery<2>>" if cfg["name"] == "C3" else cfg["name"],
+            "kernel": kernel_name(gfp, cfg, local_terms),
             "algorithmic_bytes_per_launch": local_bytes, "avg_launch_ms": round(kern_avg, 4),
             "peak_source": peak_src, "spec_8TBps_frac": round(achieved / 8000.0, 4)}
 
