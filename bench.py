@@ -358,6 +358,17 @@ def host_threads():
         return max(1, os.cpu_count() or 1)
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def oracle_slice(cfg, h, lo, hi):
     """The oracle, as it stands, on elements (rows for the batch) [lo, hi) of the sample."""
     import oracle
@@ -557,7 +568,7 @@ def main():
             cpu = {"value": mt, "unit": "terms/s", "cores": nthr, "kind": "oracle", "sample": sample,
                    "threads_note": f"the single-threaded C oracle run on {nthr} contiguous slices of the sample, "
                                    f"one host thread each; slices combined and checked: {mt_ok}",
-                   "single_thread_value": tps, "thread_scaling": mt / tps}
+                   "single_thread_value": tps, "thread_scaling": mt / tps, "cpu_model": cpu_model()}
         # parity of the GPU path on the same sample (the whole shard when the sample covers it)
         if cfg["kind"] == "batch":
             got = gfp.dot_batch(d["A"][:m], d["x"], cfg["p"], cfg["rep"]).cpu().numpy().astype(np.uint64)
@@ -860,7 +871,8 @@ def reference_arm(args, cfg, world, rank):
             "config": {"workload": cfg["workload"], "p": cfg["p"], "representation": REP_NAMES[cfg["rep"]],
                        "n_total": cfg["n"] if cfg["kind"] == "dot" else cfg["rows"] * cfg["n"]},
             "cpu_baseline": {"value": value, "unit": "terms/s", "cores": nthr, "kind": "oracle", "sample": desc,
-                             "single_thread_value": st, "threads_note": "the single-threaded C oracle on "
+                             "single_thread_value": st, "cpu_model": cpu_model(),
+                             "threads_note": "the single-threaded C oracle on "
                              f"{nthr} contiguous slices of the sample, one host thread each; combined result "
                              f"checked against one thread: {checks[0] if checks else None}"},
             "e2e": {"value": value, "unit": "terms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
