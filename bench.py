@@ -56,6 +56,13 @@ CONFIGS = {
     # blocks of k = 8 instead of 2; converted on device from the same residues (conversion timed apart)
     6: dict(name="C2-centered", workload="configs[1] in the centered representation (sec. 3.2.2), binary64, k=8",
             p=67108859, rep=4, dtype=np.float64, n=10 ** 7, bpt=16, kind="dot", inputs_of=1, host_dtype=np.uint32),
+    # the fused multi-GPU dot (gfp_dot_allreduce, a9) run as a one-rank group: the shard dot, the exchange
+    # protocol against the rank's own buffer (release/acquire flags, parity slots) and the finalize -- what the
+    # fused combine costs over a plain dot on one GPU (the NVLink hop itself needs a second GPU)
+    7: dict(name="C1-fused1", workload="configs[0] through gfp_dot_allreduce as a one-rank group", p=65521, rep=0,
+            dtype=np.uint32, n=100_000, bpt=8, kind="dot", inputs_of=0, fused1=True),
+    8: dict(name="C3-fused1", workload="configs[2] through gfp_dot_allreduce as a one-rank group", p=P31, rep=1,
+            dtype=np.uint32, n=1 << 28, bpt=8, kind="dot", inputs_of=2, fused1=True),
 }
 REP_NAMES = {0: "classical", 1: "montgomery", 2: "fp64", 3: "zech", 4: "centered"}
 DTYPE_NAMES = {np.dtype(np.uint16): "u16", np.dtype(np.uint32): "u32", np.dtype(np.float64): "f64"}
@@ -284,12 +291,12 @@ def make_step(gfp, cfg, reps, world, group, stream, xchg=None):
         if record:
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record(stream)
-        if world == 1 and cfg.get("strategy"):
+        if xchg is not None:
+            gfp_dist.dot_fused(a, b, p, rep, xchg, out=out, stream=stream)
+        elif world == 1 and cfg.get("strategy"):
             gfp.dot_ex(a, b, p, rep, strategy=cfg["strategy"], out=out, stream=stream)
         elif world == 1:
             gfp.dot(a, b, p, rep, out=out, stream=stream)
-        elif xchg is not None:
-            gfp_dist.dot_fused(a, b, p, rep, xchg, out=out, stream=stream)
         else:
             gfp.dot_partial(a, b, p, rep, out=partial, stream=stream)
         if record:
@@ -516,7 +523,7 @@ def main():
     total_terms = cfg["rows"] * cfg["n"] if cfg["kind"] == "batch" else cfg["n"]
     reps = replicas(d, local_bytes)
     xchg = None
-    if world > 1 and cfg["kind"] == "dot" and args.combine == "fused":
+    if cfg["kind"] == "dot" and ((world > 1 and args.combine == "fused") or cfg.get("fused1")):
         from paper_cs_0404008_b200 import dist as gfp_dist
         xchg = gfp_dist.PeerExchange(group)
     step, ev, out = make_step(gfp, cfg, reps, world, group, stream, xchg)
@@ -707,7 +714,11 @@ def secondary_table(gfp, args, dev, stream, exclude):
             terms = cfg["n"]
             nbytes = terms * cfg["bpt"]
         reps = replicas(d, nbytes)
-        step, ev, out = make_step(gfp, cfg, reps, 1, None, stream)
+        xchg = None
+        if cfg.get("fused1"):
+            from paper_cs_0404008_b200 import dist as gfp_dist
+            xchg = gfp_dist.PeerExchange()  # one-rank group (no process group needed)
+        step, ev, out = make_step(gfp, cfg, reps, 1, None, stream, xchg)
         # short kernels are launch-bound from Python: replay a CUDA graph of `per_graph` steps (one pass
         # over the rotating copies) and time the replays; per-step time includes the in-graph launch gaps
         per_graph = max(len(reps), 8)
@@ -738,6 +749,13 @@ def secondary_table(gfp, args, dev, stream, exclude):
                               "l2": f"{len(reps)} rotating input copies (>= 3x L2)"}
         if phases:
             table[cfg["name"]]["phases"] = phases
+        if xchg is not None:  # the fused result must equal the plain dot's
+            with torch.cuda.stream(stream):
+                plain = gfp.dot(reps[0]["a"], reps[0]["b"], cfg["p"], cfg["rep"], stream=stream)
+                fused = gfp_dist.dot_fused(reps[0]["a"], reps[0]["b"], cfg["p"], cfg["rep"], xchg, stream=stream)
+            stream.synchronize()
+            table[cfg["name"]]["equals_plain_dot"] = bool(torch.equal(plain.cpu(), fused.cpu()))
+            xchg.close()
         del d, reps, step, ev, out, g
         torch.cuda.empty_cache()
     return table

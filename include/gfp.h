@@ -220,12 +220,12 @@ gfp_status gfp_finalize(uint64_t p, gfp_rep rep, gfp_dtype dt, const uint64_t *s
  *
  * Protocol (all ranks call gfp_dot_allreduce in the same order -- the usual collective contract; the
  * state lives in device memory, so calls may be captured in CUDA graphs): the calling rank's epoch e is
- * its buffer's counter + 1; the last CTA stores its partial residue (additive form, as gfp_dot_partial)
- * into slot [e mod 2][rank] of every peer's buffer, then publishes flag [e mod 2][rank] = e on every peer
- * with a system-scope release; it waits (system-scope acquire) until its own flags [e mod 2][r] >= e for
- * every r, sums the slots, reduces mod p, encodes out[0] and stores e.  Two slot sets suffice: a rank
- * can only write epoch e + 2's slots after every rank published epoch e + 1, i.e. after every rank has
- * read epoch e's.  A peer that never arrives makes the kernel trap after about 30 s (the error surfaces
+ * its buffer's counter + 1; the last CTA stores ONE tagged 64-bit word ((e mod 2^32) << 32 | its partial
+ * residue, additive form as gfp_dot_partial, < 2^32) into slot [e mod 2][rank] of every peer's buffer --
+ * data and flag in one single-copy-atomic store, so no system-scope fence is needed -- then polls its own
+ * slots [e mod 2][r] until every one carries the tag of epoch e, sums their residues, reduces mod p,
+ * encodes out[0] and stores e.  Two slot sets suffice: a rank can only write epoch e + 2's slot after
+ * every rank published epoch e + 1, i.e. after every rank has read epoch e's.  A peer that never arrives makes the kernel trap after about 30 s (the error surfaces
  * at the next synchronisation) instead of hanging.  Every rank receives the same out[0]. */
 #define GFP_XCHG_MAX_WORLD 16
 typedef struct {

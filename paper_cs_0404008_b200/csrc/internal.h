@@ -28,9 +28,10 @@ struct OutSpec {
 // Packed combine: the CTA residues (< p < 2^32) are summed in bits [0, kPackShift), the CTA arrival
 // count in bits [kPackShift, 64): exact for grids below 2^(64 - kPackShift) CTAs.
 constexpr int kPackShift = 48;
-// Exchange-buffer layout (u64 words): [0] this rank's epoch, [1] rank, [2] world; flags at
-// kXFlags + parity * MAXW + r; partial slots at kXSlots + parity * MAXW + r; the peer table (every rank's
-// buffer as mapped in this process) at kXPeers + r.  Kernel parameters stay small: one pointer.
+// Exchange-buffer layout (u64 words): [0] this rank's epoch, [1] rank, [2] world; [kXFlags, kXSlots) unused
+// (a separate-flag protocol, replaced by tagged slots); tagged partial slots (epoch << 32 | residue) at
+// kXSlots + parity * MAXW + r; the peer table (every rank's buffer as mapped in this process) at
+// kXPeers + r.  Kernel parameters stay small: one pointer.
 constexpr int kXFlags = 8, kXSlots = 8 + 2 * GFP_XCHG_MAX_WORLD, kXPeers = 8 + 4 * GFP_XCHG_MAX_WORLD,
               kXWords = 8 + 5 * GFP_XCHG_MAX_WORLD;
 

@@ -103,40 +103,41 @@ __device__ __forceinline__ void write_result(uint64_t r, const OutSpec &O, const
 
 // ------------------------------------------------------------------------------ fused multi-GPU combine
 // gfp_dot_allreduce (gfp.h protocol): called by ONE thread of the last CTA with this rank's partial residue
-// r (additive form, < p); returns the residue of the sum over all ranks.  Peer buffers are other GPUs'
-// memory mapped over NVLink (CUDA IPC): system-scope release/acquire orders the slot stores before the
-// flag that publishes them.
+// r (additive form, < p < 2^32); returns the residue of the sum over all ranks.  Peer buffers are other
+// GPUs' memory mapped over NVLink (CUDA IPC).  Each rank stores ONE tagged word (epoch << 32 | r) into
+// slot [e mod 2][rank] of every rank's buffer and polls its own slots until every rank's word carries
+// epoch e: the data and its flag are one aligned 64-bit store (single-copy atomic), so no release /
+// acquire fence is needed at system scope -- the fences of a separate flag cost ~2.5 us per launch
+// (profiles/r01_fused_ab.txt).  Slots for epoch e + 2 are only written after every rank has published
+// e + 1, i.e. after every rank has read epoch e's slots (two parities suffice).
 __device__ __forceinline__ uint64_t xchg_allreduce(uint64_t r, uint64_t *own, uint64_t p, uint64_t mu) {
     const uint64_t e = own[0] + 1;  // this rank's epoch: only this rank's kernels touch word 0, in stream order
     const int rank = (int)own[1], world = (int)own[2];
     uint64_t *const *peers = reinterpret_cast<uint64_t *const *>(own + kXPeers);
     const int par = (int)(e & 1);
+    const uint64_t tag = e & 0xFFFFFFFFull;
+    const uint64_t word = (tag << 32) | r;
     for (int q = 0; q < world; ++q) {
         uint64_t *slot = peers[q] + kXSlots + par * GFP_XCHG_MAX_WORLD + rank;
-        asm volatile("st.relaxed.sys.u64 [%0], %1;" ::"l"(slot), "l"(r) : "memory");
-    }
-    for (int q = 0; q < world; ++q) {
-        uint64_t *flag = peers[q] + kXFlags + par * GFP_XCHG_MAX_WORLD + rank;
-        asm volatile("st.release.sys.u64 [%0], %1;" ::"l"(flag), "l"(e) : "memory");
+        asm volatile("st.relaxed.sys.u64 [%0], %1;" ::"l"(slot), "l"(word) : "memory");
     }
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     uint64_t sum = 0;
     for (int q = 0; q < world; ++q) {
-        const uint64_t *flag = own + kXFlags + par * GFP_XCHG_MAX_WORLD + q;
+        const uint64_t *slot = own + kXSlots + par * GFP_XCHG_MAX_WORLD + q;
         for (;;) {
-            uint64_t f;
-            asm volatile("ld.acquire.sys.u64 %0, [%1];" : "=l"(f) : "l"(flag) : "memory");
-            if (f >= e) break;
+            uint64_t v;
+            asm volatile("ld.relaxed.sys.u64 %0, [%1];" : "=l"(v) : "l"(slot) : "memory");
+            if ((v >> 32) == tag) {
+                sum += v & 0xFFFFFFFFull;  // world <= 16 residues < 2^32: no wrap
+                break;
+            }
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             if (t - t0 > 30000000000ull) __trap();  // a peer never arrived: fail loudly, do not hang
-            __nanosleep(64);
+            __nanosleep(32);
         }
-        uint64_t v;
-        asm volatile("ld.relaxed.sys.u64 %0, [%1];" : "=l"(v) : "l"(own + kXSlots + par * GFP_XCHG_MAX_WORLD + q)
-                     : "memory");
-        sum += v;  // world <= 16 residues < 2^32: no wrap
     }
     own[0] = e;
     return mod_p(sum, p, mu);

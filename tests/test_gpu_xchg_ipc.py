@@ -2,12 +2,12 @@
 exchange buffers -- without ranks whose kernels wait on one another.
 
 Only rank 0 runs the fused kernel (world = 2).  Rank 1 plays its peer from the host: before each of rank
-0's launches it publishes its partial residue and epoch flag into rank 0's buffer through its own IPC
-mapping; after the launch it reads its own buffer and checks that rank 0's kernel delivered rank 0's
-partial and flag there (system-scope stores into another process's memory).  Rank 0 checks the encoded
+0's launches it publishes its tagged partial (epoch << 32 | residue) into rank 0's buffer through its own
+IPC mapping; after the launch it reads its own buffer and checks that rank 0's kernel delivered rank 0's
+tagged partial there (a system-scope store into another process's memory).  Rank 0 checks the encoded
 result against the oracle: (partial_0 + partial_1) mod p in the representation.  So the whole data path
 of the fused combine -- handle exchange, gfp_xchg_open in another process, the kernel's peer stores, the
-flag acquire, the parity slots over several epochs -- runs for real; what one GPU cannot show is two
+tag polling, the parity slots over several epochs -- runs for real; what one GPU cannot show is two
 kernels spinning on each other, which the protocol model (test_xchg_protocol.py) covers.
 
 The exchange-buffer layout (word offsets) mirrors paper_cs_0404008_b200/csrc/internal.h.
@@ -25,7 +25,7 @@ import synth
 pytestmark = pytest.mark.gpu
 
 MAXW = 16
-K_FLAGS, K_SLOTS = 8, 8 + 2 * MAXW  # internal.h: kXFlags, kXSlots
+K_SLOTS = 8 + 2 * MAXW  # internal.h: kXSlots (tagged slots: epoch << 32 | residue)
 K_WORDS = 8 + 5 * MAXW
 
 
@@ -85,10 +85,8 @@ def _worker(rank, port, q):
             a0, b0 = _shard(0, p, gen, dt, n)
             a1, b1 = _shard(1, p, gen, dt, n - 5)
             r0, r1 = _additive_partial(p, rep, a0, b0), _additive_partial(p, rep, a1, b1)
-            if rank == 1:  # publish rank 1's partial, then its flag, into rank 0's buffer (peer memory)
-                peer[K_SLOTS + par * MAXW + 1] = r1
-                torch.cuda.synchronize()
-                peer[K_FLAGS + par * MAXW + 1] = e
+            if rank == 1:  # publish rank 1's tagged partial (epoch << 32 | residue) into rank 0's buffer
+                peer[K_SLOTS + par * MAXW + 1] = (e << 32) | r1
                 torch.cuda.synchronize()
             dist.barrier()
             if rank == 0:
@@ -106,9 +104,8 @@ def _worker(rank, port, q):
                 assert val == want, (e, p, rep, val, want)
                 assert int(mine[0].item()) == e, "own epoch word"
             dist.barrier()
-            if rank == 1:  # rank 0's kernel stored its partial and flag into THIS process's buffer
-                assert int(mine[K_FLAGS + par * MAXW + 0].item()) == e, (e, "flag")
-                assert int(mine[K_SLOTS + par * MAXW + 0].item()) == r0, (e, "slot")
+            if rank == 1:  # rank 0's kernel stored its tagged partial into THIS process's buffer
+                assert int(mine[K_SLOTS + par * MAXW + 0].item()) == (e << 32) | r0, (e, "slot")
                 assert int(mine[0].item()) == 0, "a peer never writes the epoch word"
             dist.barrier()
         torch.cuda.synchronize()

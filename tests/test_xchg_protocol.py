@@ -17,30 +17,33 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-MAXW, XFLAGS = 16, 8
+MAXW = 16
 XSLOTS = 8 + 2 * MAXW
 
 
 def model_allreduce(bufs, rank, world, r, p, jitter):
-    """The kernel's xchg_allreduce on Python lists (one list of words per rank's buffer)."""
+    """The kernel's xchg_allreduce on Python lists (one list of words per rank's buffer): one tagged word
+    (epoch << 32 | residue) per slot, written in a single store, polled until the tag matches."""
     own = bufs[rank]
     e = own[0] + 1
     par = e & 1
+    tag = e & 0xFFFFFFFF
+    assert 0 <= r < 2 ** 32
     for q in range(world):
         jitter()
-        bufs[q][XSLOTS + par * MAXW + rank] = r
-    for q in range(world):
-        jitter()
-        bufs[q][XFLAGS + par * MAXW + rank] = e  # release: after every slot store of this rank
+        bufs[q][XSLOTS + par * MAXW + rank] = (tag << 32) | r  # one single-copy-atomic 64-bit store
     total = 0
     for q in range(world):
         deadline = time.time() + 20
-        while own[XFLAGS + par * MAXW + q] < e:
+        while True:
+            v = own[XSLOTS + par * MAXW + q]
+            if v >> 32 == tag:
+                break
             if time.time() > deadline:
                 raise TimeoutError(f"rank {rank} epoch {e}: peer {q} never arrived")
             time.sleep(0)
         jitter()
-        total += own[XSLOTS + par * MAXW + q]
+        total += v & 0xFFFFFFFF
     own[0] = e
     return total % p
 
