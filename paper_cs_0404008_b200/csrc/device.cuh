@@ -18,6 +18,7 @@
 #include "params.h"
 
 
+
 namespace gfp {
 namespace dev {
 
@@ -140,7 +141,6 @@ struct Montgomery {
     using elem = uint32_t;
     static constexpr int W = 4;
     static constexpr bool kTable = false;
-    static constexpr bool kNoPrefetch = true;  // long streams (C3): see pdl_enter (kernels.cu)
     struct Acc { uint64_t S; };
     __device__ __forceinline__ static void init(Acc &A) { A.S = 0; }
     __device__ __forceinline__ static void term(Acc &A, uint32_t x, uint32_t y, const KParams &K,

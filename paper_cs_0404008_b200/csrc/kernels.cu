@@ -172,13 +172,14 @@ __device__ __forceinline__ void stage_table(uint16_t *dst, const uint16_t *src, 
 // launch is staged while this one runs.  Each kernel waits (griddepcontrol.wait: every earlier kernel in
 // the stream has completed and its writes are visible) before its first load, so memory order is the
 // stream order, and each CTA signals its dependents after its last global write.
-// Short streams (the launcher sets O.prefetch) first prefetch the thread's first chunk of both operands
-// into L2, so the DRAM round trip of the first loads overlaps the previous kernel's drain (its last CTA's
-// combine and the memory flush).  An L2 prefetch cannot observe stale data: L2 is the device's point of
-// coherence and nothing is loaded into registers or L1 before the wait.  A/B on the B200
-// (scripts/ab_secondary.sh, profiles/r01_pdl_ab.txt): prefetch -6% at C2, -1.5% at C4 / F3 / C5; for long
-// streams (C3, conversions) it costs ~1% and is off.  Signalling the dependents at CTA entry instead
-// (GFP_PDL_EARLY=1) was slower on every config.
+// Dots whose threads stream at most kPrefetchMaxIters chunks (the launcher sets O.prefetch) and batches
+// first prefetch the thread's first chunk of both operands into L2, so the DRAM round trip of the first
+// loads overlaps the previous kernel's drain (its last CTA's combine and the memory flush).  An L2
+// prefetch cannot observe stale data: L2 is the device's point of coherence and nothing is loaded into
+// registers or L1 before the wait.  A/B on the B200 (scripts/ab_secondary.sh, scripts/ab_head.sh,
+// profiles/r01_pdl_ab.txt): prefetch -6% at C2, -1.5% at C4 / F3 / C5, -0.2% at C3 (16 waves: ~5 chunks
+// per thread); conversions are flat grids with one tile per thread and no prefetch.  Signalling the
+// dependents at CTA entry instead (GFP_PDL_EARLY=1) was slower on every config.
 #ifndef GFP_PDL_EARLY
 #define GFP_PDL_EARLY 0
 #endif
@@ -224,12 +225,6 @@ __device__ __forceinline__ void pdl_exit() {
 }
 
 // ------------------------------------------------------------------------------ single dot
-// Policies whose dots are long streams in practice (R::kNoPrefetch, Montgomery at C3) carry no prefetch
-// code at all: the register allocation of their streaming loop stays as A/B-tuned.
-template <class R, class = void>
-struct Prefetches { static constexpr bool value = true; };
-template <class R>
-struct Prefetches<R, std::void_t<decltype(R::kNoPrefetch)>> { static constexpr bool value = !R::kNoPrefetch; };
 
 template <class R, int NT, int U, bool PIPE>
 __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restrict__ a,
@@ -245,7 +240,7 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
     const uint4 *av = reinterpret_cast<const uint4 *>(a + head);
     const uint4 *bv = reinterpret_cast<const uint4 *>(b + head);
     int64_t i0 = (int64_t)blockIdx.x * (NT * U) + threadIdx.x;
-    pdl_prefetch<U, NT>(av, bv, i0, nvec, Prefetches<R>::value && O.prefetch != 0);
+    pdl_prefetch<U, NT>(av, bv, i0, nvec, O.prefetch != 0);
     if constexpr (R::kTable && GFP_STAGE_EARLY) stage_table(s_tab, K.antilog, K.antilog_entries);
     pdl_wait();
     const int64_t step = (int64_t)gridDim.x * (NT * U);
