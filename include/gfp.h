@@ -50,6 +50,10 @@
  * on `stream` and return; results are ready in stream order.  They never
  * allocate on the hot path after the first call for a (device, p, rep,
  * stream) and are safe to capture in a CUDA graph after that first call.
+ * Each (device, stream) owns a small self-resetting combine workspace, so
+ * calls are ordered by their stream; a captured graph keeps using the
+ * capturing stream's workspace -- do not replay it concurrently with other
+ * library calls on that stream's workspace (e.g. two replays on two streams).
  * Kernels are launched with programmatic stream serialization (PDL): the next
  * launch is staged while the previous kernel drains.  Before waiting on the
  * stream's earlier work a kernel touches only library-owned tables and issues

@@ -161,7 +161,10 @@ gfp_status get_ws(cudaStream_t s, Workspace *ws) {
     cudaError_t e = cudaMalloc(&mem, bytes);
     if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? fail(GFP_E_NOMEM, "workspace") : cuda_fail(e, "workspace");
     e = cudaMemset(mem, 0, bytes);
-    if (e != cudaSuccess) return cuda_fail(e, "workspace memset");
+    if (e != cudaSuccess) {
+        cudaFree(mem);
+        return cuda_fail(e, "workspace memset");
+    }
     Workspace w;
     w.partials = (uint64_t *)mem;
     w.counter = (unsigned int *)((char *)mem + kMaxGrid * sizeof(uint64_t));
