@@ -1315,6 +1315,15 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
                 reductions = 0;
             } else if (per_thread * q2 <= max64) {
                 pol = I.dtype == GFP_U16 ? P_CL16_THREAD : P_CL32_THREAD;
+            } else if (const uint64_t lam = (uint64_t)std::min<u128>(max64 / ((u128)I.p * pm1), UINT64_MAX);
+                       lam >= 4) {
+                // sec. 3.4 hybrid, Eq. (2): one wrap test per block of lambda products, lambda p (p-1) < 2^64
+                // (B200: 1.07x (dot) / 1.4x (DIM=512 batch) over a test per product at lambda = 4; slower at 2)
+                pol = cs_policy(true, true, GFP_STRAT_HYBRID);
+                acc = GFP_ACC_OVERFLOW;
+                strat = GFP_STRAT_HYBRID;
+                kblk = lam;
+                reductions = (int64_t)(per_thread / lam) + 1;
             } else {
                 pol = P_CL32_OVF;  // sec. 3.3 overflow detection (u16 products never need it)
                 acc = GFP_ACC_OVERFLOW;
@@ -1542,10 +1551,16 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
                 return GFP_E_UNSUPPORTED;
             }
         } else {
+            const uint64_t lam = (uint64_t)std::min<u128>(max64 / ((u128)I.p * pm1), UINT64_MAX);
+            KParams K2 = K;
+            K2.kblk = lam;
             if ((u128)n * q2 <= max64)
                 *err = launch_batch_t<ClassicalU32<CL_ALL>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
             else if (per_lane * q2 <= max64)
                 *err = launch_batch_t<ClassicalU32<CL_THREAD>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
+            else if (lam >= 4)  // sec. 3.4 hybrid (Eq. (2)), as in plan_dot
+                *err = launch_batch_t<ClassicalS<uint64_t, uint32_t, S_HYBRID>, 256, kBatchU>(K2, A, lda, x, rows, n,
+                                                                                            vec, O, s);
             else
                 *err = launch_batch_t<ClassicalU32<CL_OVERFLOW>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
         }
