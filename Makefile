@@ -53,3 +53,6 @@ $(PKG)/libgfp_pipe.so: $(GFP_SRCS) $(GFP_HDRS)
 # generic A/B variant: make variant NAME=x VFLAGS="-DGFP_CONV_U=2 ..." -> $(PKG)/libgfp_x.so
 variant:
 	$(NVCC) $(NVFLAGS) $(VFLAGS) -shared -o $(PKG)/libgfp_$(NAME).so $(GFP_SRCS) -lcudart 2> /dev/null
+tune: scripts/tune_zech
+scripts/tune_zech: scripts/tune_zech.cu $(CSRC)/device.cuh $(CSRC)/params.h
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -I$(CSRC) -Iinclude -o $@ $<
