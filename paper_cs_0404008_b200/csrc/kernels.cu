@@ -945,9 +945,10 @@ static int occupancy(F kernel, int block, size_t smem) {
     return bps;
 }
 
-// Measured on B200 (scripts/ab_bench.sh, scripts/tune_*.cu): unpipelined U=4 (40 regs, 6 CTAs/SM)
-// beats the register-pipelined variant (80 regs) by 2% on C3; fp64 is best at U=2; Zech (1024
-// threads, 64-register cap) needs the pipeline to keep loads in flight across its table lookups.
+// Measured on B200 (scripts/ab_bench.sh, scripts/ab_head.sh, scripts/tune_*.cu): unpipelined loads beat
+// the register-pipelined variant (80 regs) by 2% on C3 (U = 2 with multi-wave grids; U = 4 was best with
+// one wave); fp64 is best at U = 2; Zech (1024 threads, 64-register cap) needs the pipeline to keep
+// loads in flight across its table lookups.
 #ifndef GFP_DOT_PIPE
 #define GFP_DOT_PIPE 0
 #endif
@@ -955,7 +956,7 @@ static int occupancy(F kernel, int block, size_t smem) {
 #define GFP_FP_U 2
 #endif
 #ifndef GFP_DOT_U
-#define GFP_DOT_U 4
+#define GFP_DOT_U 2  // with the multi-wave grids (B200 A/B, scripts/ab_head.sh): U 2 290.6 -> 289.4 us at C3, 2.39 -> 2.30 us at C1
 #endif
 #ifndef GFP_CONV_U
 #define GFP_CONV_U 2  // B200 A/B, flat grid: U = 1 / 2 / 4 -> 6.97 / 6.94 / 6.60 TB/s (to_montgomery, 4 GiB)
