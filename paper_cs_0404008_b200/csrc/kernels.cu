@@ -956,11 +956,15 @@ static int occupancy(F kernel, int block, size_t smem) {
 #define GFP_FP_U 2
 #endif
 #ifndef GFP_DOT_U
-#define GFP_DOT_U 2  // with the multi-wave grids (B200 A/B, scripts/ab_head.sh): U 2 290.6 -> 289.4 us at C3, 2.39 -> 2.30 us at C1
+#define GFP_DOT_U 2  // Montgomery and explicit strategies; with the multi-wave grids U 2: 290.6 -> 289.4 us at C3
 #endif
+#ifndef GFP_CL_U
+#define GFP_CL_U 4  // built-in classical dots: 4 loads per operand in flight serve C1's DRAM-latency-bound 10^5
+#endif          // terms from fewer CTAs (2.68 vs 2.84 us with U 2; scripts/ab_sec2.sh)
 #ifndef GFP_CONV_U
 #define GFP_CONV_U 2  // B200 A/B, flat grid: U = 1 / 2 / 4 -> 6.97 / 6.94 / 6.60 TB/s (to_montgomery, 4 GiB)
 #endif
+constexpr int kClU = GFP_CL_U;  // built-in classical dots
 constexpr int kDotNT = 256, kDotU = GFP_DOT_U, kFpU = GFP_FP_U, kZechNT = GFP_ZECH_NT, kZechU = GFP_ZECH_U, kZaddNT = 1024, kZaddU = 2;
 constexpr bool kPipe = GFP_DOT_PIPE != 0;
 
@@ -988,6 +992,7 @@ static int policy_block(int pol) { return pol == P_ZECH_ADD ? kZaddNT : (is_zech
 static int policy_unroll(int pol) {
     if (pol == P_ZECH_ADD) return kZaddU;
     if (is_fc(pol)) return kFpU;
+    if (pol >= P_CL32_ALL && pol <= P_CL16_THREAD) return kClU;
     return is_zech(pol) ? kZechU : ((pol >= P_FP_THREAD && pol <= P_FP_K2) ? kFpU : kDotU);
 }
 static int policy_width(int pol) {
@@ -1041,11 +1046,11 @@ static int policy_width(int pol) {
 
 static int policy_occupancy(int pol, size_t smem) {
     switch (pol) {
-    case P_CL32_ALL: return dot_occupancy<ClassicalU32<CL_ALL>, kDotNT, kDotU, kPipe>(smem);
-    case P_CL32_THREAD: return dot_occupancy<ClassicalU32<CL_THREAD>, kDotNT, kDotU, kPipe>(smem);
-    case P_CL32_OVF: return dot_occupancy<ClassicalU32<CL_OVERFLOW>, kDotNT, kDotU, kPipe>(smem);
-    case P_CL16_ALL: return dot_occupancy<ClassicalU16<CL_ALL>, kDotNT, kDotU, kPipe>(smem);
-    case P_CL16_THREAD: return dot_occupancy<ClassicalU16<CL_THREAD>, kDotNT, kDotU, kPipe>(smem);
+    case P_CL32_ALL: return dot_occupancy<ClassicalU32<CL_ALL>, kDotNT, kClU, kPipe>(smem);
+    case P_CL32_THREAD: return dot_occupancy<ClassicalU32<CL_THREAD>, kDotNT, kClU, kPipe>(smem);
+    case P_CL32_OVF: return dot_occupancy<ClassicalU32<CL_OVERFLOW>, kDotNT, kClU, kPipe>(smem);
+    case P_CL16_ALL: return dot_occupancy<ClassicalU16<CL_ALL>, kDotNT, kClU, kPipe>(smem);
+    case P_CL16_THREAD: return dot_occupancy<ClassicalU16<CL_THREAD>, kDotNT, kClU, kPipe>(smem);
     case P_MONT1: return dot_occupancy<Montgomery<1>, kDotNT, kDotU, kPipe>(smem);
     case P_MONT2: return dot_occupancy<Montgomery<2>, kDotNT, kDotU, kPipe>(smem);
     case P_MONT4: return dot_occupancy<Montgomery<4>, kDotNT, kDotU, kPipe>(smem);
@@ -1079,11 +1084,11 @@ cudaError_t launch_dot(const DotPlan &P, const KParams &K0, const void *a, const
         O.prefetch = nvec <= kPrefetchMaxIters * per_sweep;
     }
     switch (P.policy) {
-    case P_CL32_ALL: return launch_dot_t<ClassicalU32<CL_ALL>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
-    case P_CL32_THREAD: return launch_dot_t<ClassicalU32<CL_THREAD>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
-    case P_CL32_OVF: return launch_dot_t<ClassicalU32<CL_OVERFLOW>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
-    case P_CL16_ALL: return launch_dot_t<ClassicalU16<CL_ALL>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
-    case P_CL16_THREAD: return launch_dot_t<ClassicalU16<CL_THREAD>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
+    case P_CL32_ALL: return launch_dot_t<ClassicalU32<CL_ALL>, kDotNT, kClU, kPipe>(P, K, a, b, n, ws, O, s);
+    case P_CL32_THREAD: return launch_dot_t<ClassicalU32<CL_THREAD>, kDotNT, kClU, kPipe>(P, K, a, b, n, ws, O, s);
+    case P_CL32_OVF: return launch_dot_t<ClassicalU32<CL_OVERFLOW>, kDotNT, kClU, kPipe>(P, K, a, b, n, ws, O, s);
+    case P_CL16_ALL: return launch_dot_t<ClassicalU16<CL_ALL>, kDotNT, kClU, kPipe>(P, K, a, b, n, ws, O, s);
+    case P_CL16_THREAD: return launch_dot_t<ClassicalU16<CL_THREAD>, kDotNT, kClU, kPipe>(P, K, a, b, n, ws, O, s);
     case P_MONT1: return launch_dot_t<Montgomery<1>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
     case P_MONT2: return launch_dot_t<Montgomery<2>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
     case P_MONT4: return launch_dot_t<Montgomery<4>, kDotNT, kDotU, kPipe>(P, K, a, b, n, ws, O, s);
