@@ -84,6 +84,16 @@ def test_classical_u32_large_primes_overflow_path(p):
     w = np.full(3 * 10 ** 6 + 1, p - 1, np.uint32)  # every add wraps the u64 when (p-1)^2 ~ 2^64
     assert result_int(gfp.dot(cu(w), cu(w), p, CL)) == (3 * 10 ** 6 + 1) % p
     assert info["k"] >= 1
+    # the built-in plan: Eq. (2) hybrid while lambda = floor((2^64-1)/(p(p-1))) >= 4, else a test per product
+    lam = (2 ** 64 - 1) // (p * (p - 1))
+    pl = gfp.plan(p, CL, 3 * 10 ** 6 + 1, dtype=torch.uint32)
+    if pl["strategy"] != gfp.AUTO and "ALL" not in pl["kernel"] and "THREAD" not in pl["kernel"]:
+        assert pl["strategy"] == (gfp.HYBRID if lam >= 4 else gfp.OVERFLOW), (p, pl)
+    # worst-case batches through the same built-in choice (rows of 4096 overflow a lane's u64 sum)
+    rows, n = 37, 4096
+    W = np.full((rows, n), p - 1, np.uint32)
+    got = gfp.dot_batch(cu(W), cu(W[0]), p, CL).cpu().to(torch.int64).numpy()
+    assert (got == n % p).all(), (p, "batch worst case")
 
 
 def test_misaligned_and_ragged():
