@@ -777,6 +777,9 @@ __device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab)
 #ifndef GFP_ZECH_U
 #define GFP_ZECH_U 2  // 16-byte vectors per operand per step of the integer Zech dot
 #endif
+#ifndef GFP_CL16_U
+#define GFP_CL16_U 16  // C5 batch: 16-byte A vectors per lane in flight (long rows)
+#endif
 #ifndef GFP_BATCH_WAVES
 #define GFP_BATCH_WAVES 4  // C5 batch grid: waves of resident CTAs (B200 A/B, profiles/r01_waves_ab.txt)
 #endif
@@ -1536,7 +1539,7 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
             if (vec && (u128)n * q2 <= max64 && n <= 96 * 1024) {
                 constexpr int NT = 256;
                 const bool long_rows = n / 8 >= 256;
-                auto kern = long_rows ? batch_cl16_kernel<NT, 16, 32> : batch_cl16_kernel<NT, 8, 8>;
+                auto kern = long_rows ? batch_cl16_kernel<NT, GFP_CL16_U, 32> : batch_cl16_kernel<NT, 8, 8>;
                 const int64_t rpb = long_rows ? NT / 32 : NT / 8;  // rows per CTA per sweep
                 const size_t smem = (size_t)(((n + 1) / 2 + 3) & ~int64_t(3)) * 4;
                 int bps = occupancy(kern, NT, smem);
