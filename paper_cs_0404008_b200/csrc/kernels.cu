@@ -771,6 +771,9 @@ __device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab)
 #ifndef GFP_ZBATCH_UL
 #define GFP_ZBATCH_UL 8  // the same for the large-field (q-entry, folded index) table
 #endif
+#ifndef GFP_ZADD_U
+#define GFP_ZADD_U 2  // 16-byte vectors per operand per step of the pure-Zech dot
+#endif
 #ifndef GFP_ZECH_NT
 #define GFP_ZECH_NT 1024  // threads per CTA of the integer Zech dot (one CTA per SM: the table fills smem)
 #endif
@@ -968,7 +971,7 @@ static int occupancy(F kernel, int block, size_t smem) {
 #define GFP_CONV_U 2  // B200 A/B, flat grid: U = 1 / 2 / 4 -> 6.97 / 6.94 / 6.60 TB/s (to_montgomery, 4 GiB)
 #endif
 constexpr int kClU = GFP_CL_U;  // built-in classical dots
-constexpr int kDotNT = 256, kDotU = GFP_DOT_U, kFpU = GFP_FP_U, kZechNT = GFP_ZECH_NT, kZechU = GFP_ZECH_U, kZaddNT = 1024, kZaddU = 2;
+constexpr int kDotNT = 256, kDotU = GFP_DOT_U, kFpU = GFP_FP_U, kZechNT = GFP_ZECH_NT, kZechU = GFP_ZECH_U, kZaddNT = 1024, kZaddU = GFP_ZADD_U;
 constexpr bool kPipe = GFP_DOT_PIPE != 0;
 
 template <class R, int NT, int U, bool PIPE>
