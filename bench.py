@@ -77,6 +77,39 @@ def dist_env():
     return world, rank, local
 
 
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_plan(gpus, env, device_count):
+    """How this invocation must run `--gpus N` (one process per GPU): ("run", None) in the current process,
+    ("spawn", argv-prefix) to re-exec under torchrun with N ranks, or ("fail", reason).
+
+    - WORLD_SIZE set (the driver's torchrun form): it must equal --gpus.
+    - WORLD_SIZE unset and --gpus N > 1: self-launch N ranks (torch.distributed.run, 127.0.0.1).
+    - N must not exceed the visible GPUs, except in the host-logic check mode GFP_BENCH_PG_BACKEND=gloo,
+      where ranks may share devices (or run without one under --dry-run)."""
+    if gpus < 1:
+        return "fail", f"--gpus {gpus}: need at least 1"
+    gloo = env.get("GFP_BENCH_PG_BACKEND", "nccl") == "gloo"
+    ws = env.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != gpus:
+            return "fail", f"WORLD_SIZE={ws} but --gpus {gpus}: launch one rank per GPU (torchrun --nproc-per-node {gpus})"
+        return "run", None
+    if not gloo and gpus > device_count:
+        return "fail", f"--gpus {gpus} but only {device_count} CUDA device(s) visible"
+    if gpus == 1:
+        return "run", None
+    return "spawn", [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+                     "--master-addr", "127.0.0.1", f"--master-port={free_port()}"]
+
+
 def peak_hbm():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -482,8 +515,21 @@ def main():
                     help="SURVEY 8(f) F1: paper-shaped prime sweep of DIM=512 batched dots per strategy, "
                          "written to OUT.jsonl (one GPU)")
     ap.add_argument("--sweep-rows", type=int, default=1 << 19)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check: set up the N ranks and their process group, print one JSON line with the "
+                         "ranks that ran, no GPU work (CPU-testable with GFP_BENCH_PG_BACKEND=gloo)")
     args = ap.parse_args()
+    if not args.sweep and args.impl == "ours":  # the reference arm is host-only (rank 0 works, others exit)
+        ndev = torch.cuda.device_count()
+        how, what = launch_plan(args.gpus, os.environ, ndev)
+        if how == "fail":
+            print(f"bench.py: {what}", file=sys.stderr, flush=True)
+            raise SystemExit(2)
+        if how == "spawn":  # one process per GPU: re-exec this command under torchrun
+            os.execv(what[0], what + [os.path.abspath(__file__)] + sys.argv[1:])
     world, rank, local = dist_env()
+    if args.dry_run:
+        return dry_run(args, world, rank)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
         args.warmup = 3
@@ -602,7 +648,11 @@ def main():
             parity_terms, cpu = cpu["parity_checked_terms"], None
 
     # ---------------------------------------------------------------- end to end (host buffers)
-    e2e = e2e_leg(gfp, cfg, d, world, args.e2e_steps, stream, dev)
+    want = None  # the whole-group result of the device path, for the e2e leg's check
+    if cfg["kind"] == "dot":
+        r = ref if world > 1 else gfp.dot(reps[0]["a"], reps[0]["b"], cfg["p"], cfg["rep"])
+        want = r.cpu()[0].item() if r.dtype == torch.float64 else int(r.cpu().to(torch.int64)[0])
+    e2e = e2e_leg(gfp, cfg, d, world, args.e2e_steps, stream, dev, want)
 
     # ---------------------------------------------------------------- secondary configs (kernel only)
     secondary = None
@@ -638,7 +688,29 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e_leg(gfp, cfg, d, world, steps, stream, dev):
+def dry_run(args, world, rank):
+    """--dry-run: the rank set-up of a real run (process group over the backend the bench would use) and one
+    all_gather of (rank, LOCAL_RANK, pid); rank 0 prints what ran."""
+    backend = os.environ.get("GFP_BENCH_PG_BACKEND", "nccl")
+    _, _, local = dist_env()
+    me = {"rank": rank, "local_rank": local, "pid": os.getpid()}
+    seen = [me]
+    if world > 1:
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+        seen = [None] * world
+        dist.all_gather_object(seen, me)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "gpus_arg": args.gpus, "backend": backend if world > 1 else None,
+                          "ranks": seen}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_leg(gfp, cfg, d, world, steps, stream, dev, want=None):
     """Same metric through the public API from pinned HOST buffers: per step, the host->device copy of
     the inputs, the kernels, and the device->host read of the result are inside the timed region."""
     if steps <= 0:
@@ -662,20 +734,28 @@ def e2e_leg(gfp, cfg, d, world, steps, stream, dev):
     else:
         a = d["a"].cpu().pin_memory()
         b = d["b"].cpu().pin_memory()
-        h2d = 2 * a.numel() * a.element_size()
-        d2h = a.element_size()
+        h2d = 2 * a.numel() * a.element_size() + (8 if world > 1 else 0)
+        d2h = a.element_size() + (8 if world > 1 else 0)
+        part_h = torch.empty(1, dtype=torch.int64).pin_memory()
         part = torch.empty(1, dtype=torch.int64, device=dev)
         fin = torch.empty(1, dtype=a.dtype, device=dev)
+        fin_h = torch.empty(1, dtype=a.dtype).pin_memory()
 
         def one():
-            r = gfp.dot_host(a, b, p, rep, stream=stream)
-            if world > 1:  # combine the per-rank results (additive in every rep but Zech; centered -> residue)
-                part.fill_(int(r) % p)
+            if world == 1:
+                return gfp.dot_host(a, b, p, rep, stream=stream)
+            # N > 1: this rank's partial residue in the representation's ADDITIVE form from host buffers
+            # (gfp_dot_host_partial: never a Zech code), summed over ranks, then mod p + encode on the device
+            part_h[0] = gfp.dot_host_partial(a, b, p, rep, stream=stream)
+            with torch.cuda.stream(stream):
+                part.copy_(part_h, non_blocking=True)
                 dist.all_reduce(part)
                 gfp.finalize(part, p, rep, a.dtype, out=fin, stream=stream)
-                fin.cpu()
+                fin_h.copy_(fin, non_blocking=True)
+            stream.synchronize()
+            return fin_h[0].item()
         terms = a.numel()
-    one()
+    first = one()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -699,7 +779,11 @@ def e2e_leg(gfp, cfg, d, world, steps, stream, dev):
     link = 4 * probe.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9
     del probe, dprobe
     achieved = h2d * steps / dt / 1e9
+    equal = None
+    if want is not None and first is not None:  # the end-to-end result vs the device path's (whole-group) result
+        equal = bool(first == want)
     return {"value": total * steps / dt, "unit": "terms/s", "h2d_bytes_per_step": int(h2d),
+            "result_equals_device_path": equal,
             "d2h_bytes_per_step": int(d2h), "steps": steps,
             "h2d_GBps": round(achieved, 2), "h2d_copy_peak_GBps": round(link, 2),
             "link_frac": round(achieved / link, 3),

@@ -131,10 +131,18 @@ typedef enum {
  * DELAYED, BLOCKED}; Zech x {AUTO, ZECH_ADD}; centered x {AUTO, DELAYED, BLOCKED} (the signed overflow trick,
  * P:441-457, and hybrid centered, are not offered: the paper finds the first too costly and
  * shows the second cannot work).  Anything else: GFP_E_UNSUPPORTED; a strategy whose bound the
- * (p, n) pair violates: GFP_E_BOUND. */
+ * (p, n) pair violates: GFP_E_BOUND.
+ * lanes_per_row (gfp_dot_batch_ex only; 0 for dots): how many threads share one row's accumulation --
+ * 0 = the library's choice (32 for rows of >= 256 16-byte vectors or table representations, else 8), or
+ * 1, 8, 32.  1 is the paper's own loop: ONE accumulator walks the whole row, so a row of
+ * DIM terms reaches the block bound k of Eq. (1) exactly where the paper's scalar loop does (the DIM = 512,
+ * m = 32 step after p = 2897); with L lanes each accumulator sees about DIM / L terms and the
+ * step moves to the prime where (DIM / L)(p-1)^2 crosses 2^m.  1 is offered for integer storage only
+ * (classical, Montgomery, centered int16 / int32); anything else is GFP_E_INVAL / GFP_E_UNSUPPORTED. */
 typedef struct {
     int32_t strategy;  /* gfp_strategy */
     int32_t acc_bits;
+    int32_t lanes_per_row;
 } gfp_options;
 
 /* What a call would run (gfp_plan): kernel, grid, the strategy and its block length, and per-thread
@@ -271,6 +279,12 @@ gfp_status gfp_plan(uint64_t p, gfp_rep rep, gfp_dtype dt, int64_t n, const gfp_
  * written. */
 gfp_status gfp_dot_host(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
                         void *out, void *stream);
+/* The same from HOST buffers, but *partial (HOST, 8-byte aligned uint64) receives this shard's partial
+ * residue in the representation's additive form, exactly as gfp_dot_partial writes it (classical value,
+ * Montgomery form, fp64 integer, the classical value of a Zech sum -- never a code): the multi-GPU
+ * end-to-end path sums these across ranks and calls gfp_finalize, as for device shards. */
+gfp_status gfp_dot_host_partial(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
+                                uint64_t *partial, void *stream);
 
 /* ---- Install-time tuning (the paper's conclusion: an optimal dot "should
  * switch from block methods to a floating point representation according to the vector and prime size

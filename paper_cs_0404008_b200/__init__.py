@@ -20,7 +20,7 @@ import torch
 __all__ = [
     "CLASSICAL", "MONTGOMERY", "FP64", "ZECH", "CENTERED", "AUTO", "DELAYED", "BLOCKED", "OVERFLOW", "HYBRID", "ZECH_ADD", "CARRY",
     "GfpError", "lib", "query", "plan", "dot", "dot_ex", "dot_batch", "dot_batch_ex",
-    "dot_partial", "finalize", "to_rep", "from_rep", "dot_host", "launch_count", "release_caches",
+    "dot_partial", "finalize", "to_rep", "from_rep", "dot_host", "dot_host_partial", "launch_count", "release_caches",
     "rep_dtype", "tune", "tune_entries", "tune_set", "tune_save", "tune_load", "tune_clear",
 ]
 
@@ -50,7 +50,7 @@ class GfpInfo(ctypes.Structure):
 
 
 class GfpOptions(ctypes.Structure):
-    _fields_ = [("strategy", ctypes.c_int32), ("acc_bits", ctypes.c_int32)]
+    _fields_ = [("strategy", ctypes.c_int32), ("acc_bits", ctypes.c_int32), ("lanes_per_row", ctypes.c_int32)]
 
 
 class GfpPlanInfo(ctypes.Structure):
@@ -91,6 +91,7 @@ _SIGS = {
     "gfp_dot_partial": [_u64, _int, _int, _vp, _vp, _i64, _vp, _vp],
     "gfp_finalize": [_u64, _int, _int, _vp, _vp, _vp],
     "gfp_dot_host": [_u64, _int, _int, _vp, _vp, _i64, _vp, _vp],
+    "gfp_dot_host_partial": [_u64, _int, _int, _vp, _vp, _i64, _vp, _vp],
     "gfp_dot_ex": [_u64, _int, _int, _vp, _vp, _i64, ctypes.POINTER(GfpOptions), _vp, _vp],
     "gfp_dot_batch_ex": [_u64, _int, _int, _vp, _i64, _vp, _i64, _i64, ctypes.POINTER(GfpOptions), _vp, _vp],
     "gfp_plan": [_u64, _int, _int, _i64, ctypes.POINTER(GfpOptions), ctypes.POINTER(GfpPlanInfo)],
@@ -204,8 +205,8 @@ def dot(a: torch.Tensor, b: torch.Tensor, p: int, rep: int = CLASSICAL, out: tor
     return out
 
 
-def _opts(strategy, acc_bits):
-    return ctypes.byref(GfpOptions(strategy, acc_bits))
+def _opts(strategy, acc_bits, lanes_per_row=0):
+    return ctypes.byref(GfpOptions(strategy, acc_bits, lanes_per_row))
 
 
 def plan(p: int, rep: int, n: int, dtype: torch.dtype | None = None, strategy: int = AUTO,
@@ -260,27 +261,49 @@ def finalize(summed: torch.Tensor, p: int, rep: int, dtype: torch.dtype, out: to
     return out
 
 
-def dot_batch(A: torch.Tensor, x: torch.Tensor, p: int, rep: int = CLASSICAL, out: torch.Tensor | None = None,
-              rows: int | None = None, n: int | None = None, lda: int | None = None, stream=None) -> torch.Tensor:
-    """out[r] = A[r, :n] . x over GF(p): many independent dots / a matrix-vector product."""
+def _batch_args(A: torch.Tensor, x: torch.Tensor, out: torch.Tensor | None, rows, n, lda):
+    """Validate a batch call against the tensors' storage (so that no kernel reads or writes out of bounds)
+    and return (rows, n, lda, out)."""
     if not (A.is_cuda and x.is_cuda):
         raise ValueError("A and x must be CUDA tensors")
-    if A.dtype != x.dtype:
-        raise ValueError("A and x must have the same dtype")
+    if A.dtype != x.dtype or A.device != x.device:
+        raise ValueError("A and x must have the same dtype and device")
     if A.dim() == 2:
         if A.shape[1] > 1 and A.stride(1) != 1:
             raise ValueError("A must be row-major with unit column stride")
         rows = A.shape[0] if rows is None else rows
         n = A.shape[1] if n is None else n
         lda = A.stride(0) if lda is None else lda
-    else:
+    elif A.dim() == 1:
         if rows is None or n is None:
             raise ValueError("flat A needs rows and n")
+        if A.numel() > 1 and A.stride(0) != 1:
+            raise ValueError("flat A must be contiguous")
         lda = n if lda is None else lda
-    if not x.is_contiguous():
-        raise ValueError("x must be contiguous")
+    else:
+        raise ValueError("A must be 1-D (flat, with rows and n) or 2-D")
+    rows, n, lda = int(rows), int(n), int(lda)
+    if rows < 0 or n < 0 or lda < n:
+        raise ValueError("need rows >= 0, n >= 0 and lda >= n")
+    # elements reachable from A's data pointer within its storage
+    avail = A.untyped_storage().nbytes() // A.element_size() - A.storage_offset()
+    if rows > 0 and n > 0 and (rows - 1) * lda + n > avail:
+        raise ValueError(f"A holds {avail} elements from its data pointer; rows={rows}, n={n}, lda={lda} "
+                         f"needs {(rows - 1) * lda + n}")
+    if not x.is_contiguous() or x.numel() < n:
+        raise ValueError("x must be contiguous with at least n elements")
     if out is None:
         out = torch.empty(rows, dtype=A.dtype, device=A.device)
+    elif (not out.is_cuda or out.device != A.device or out.dtype != A.dtype or not out.is_contiguous()
+          or out.numel() < rows):
+        raise ValueError("out must be a contiguous CUDA tensor of A's dtype and device with >= rows elements")
+    return rows, n, lda, out
+
+
+def dot_batch(A: torch.Tensor, x: torch.Tensor, p: int, rep: int = CLASSICAL, out: torch.Tensor | None = None,
+              rows: int | None = None, n: int | None = None, lda: int | None = None, stream=None) -> torch.Tensor:
+    """out[r] = A[r, :n] . x over GF(p): many independent dots / a matrix-vector product."""
+    rows, n, lda, out = _batch_args(A, x, out, rows, n, lda)
     with torch.cuda.device(A.device):
         _check(lib.gfp_dot_batch(p, rep, _dt(A, rep), A.data_ptr(), lda, x.data_ptr(), rows, n, out.data_ptr(),
                                  _stream(A, stream)))
@@ -289,22 +312,13 @@ def dot_batch(A: torch.Tensor, x: torch.Tensor, p: int, rep: int = CLASSICAL, ou
 
 def dot_batch_ex(A: torch.Tensor, x: torch.Tensor, p: int, rep: int = CLASSICAL, strategy: int = AUTO,
                  acc_bits: int = 0, out: torch.Tensor | None = None, rows: int | None = None, n: int | None = None,
-                 lda: int | None = None, stream=None) -> torch.Tensor:
-    """dot_batch with an explicit accumulation strategy (sec. 3) and accumulator width."""
-    if not (A.is_cuda and x.is_cuda) or A.dtype != x.dtype:
-        raise ValueError("A and x must be CUDA tensors of the same dtype")
-    if A.dim() == 2:
-        rows = A.shape[0] if rows is None else rows
-        n = A.shape[1] if n is None else n
-        lda = A.stride(0) if lda is None else lda
-    elif rows is None or n is None:
-        raise ValueError("flat A needs rows and n")
-    lda = n if lda is None else lda
-    if out is None:
-        out = torch.empty(rows, dtype=A.dtype, device=A.device)
+                 lda: int | None = None, stream=None, lanes_per_row: int = 0) -> torch.Tensor:
+    """dot_batch with an explicit accumulation strategy (sec. 3), accumulator width and lanes per row
+    (1 = one accumulator walks the whole row, as in the paper's loop; gfp.h)."""
+    rows, n, lda, out = _batch_args(A, x, out, rows, n, lda)
     with torch.cuda.device(A.device):
         _check(lib.gfp_dot_batch_ex(p, rep, _dt(A, rep), A.data_ptr(), lda, x.data_ptr(), rows, n,
-                                    _opts(strategy, acc_bits), out.data_ptr(), _stream(A, stream)))
+                                    _opts(strategy, acc_bits, lanes_per_row), out.data_ptr(), _stream(A, stream)))
     return out
 
 
@@ -344,6 +358,20 @@ def dot_host(a: torch.Tensor, b: torch.Tensor, p: int, rep: int = CLASSICAL, str
     s = _stream(None, stream) if stream is not None else torch.cuda.current_stream().cuda_stream
     _check(lib.gfp_dot_host(p, rep, _dt(a, rep), a.data_ptr(), b.data_ptr(), a.numel(), res.data_ptr(), s))
     return res.item() if a.dtype == torch.float64 else int(res.to(torch.int64).item())
+
+
+def dot_host_partial(a: torch.Tensor, b: torch.Tensor, p: int, rep: int = CLASSICAL, stream=None) -> int:
+    """dot_host for one shard of a multi-GPU dot: the shard's partial residue in the representation's
+    additive form (sum it over ranks, then `finalize`), as a Python int."""
+    if a.is_cuda or b.is_cuda:
+        raise ValueError("dot_host_partial takes host tensors")
+    a, b = a.contiguous().reshape(-1), b.contiguous().reshape(-1)
+    if a.numel() != b.numel() or a.dtype != b.dtype:
+        raise ValueError("a and b must have the same length and dtype")
+    res = ctypes.c_uint64(0)
+    s = _stream(None, stream) if stream is not None else torch.cuda.current_stream().cuda_stream
+    _check(lib.gfp_dot_host_partial(p, rep, _dt(a, rep), a.data_ptr(), b.data_ptr(), a.numel(), ctypes.byref(res), s))
+    return int(res.value)
 
 
 def launch_count(reset: bool = False) -> int:

@@ -425,8 +425,10 @@ gfp_status gfp_from_rep(uint64_t p, gfp_rep rep, gfp_dtype in_dt, const void *in
     return convert(p, rep, 1, in_dt, in, out_dt, out, n, stream);
 }
 
-gfp_status gfp_dot_host(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n, void *out,
-                        void *stream) {
+// gfp_dot_host / gfp_dot_host_partial: partial_only writes the additive-form residue (u64) instead of the
+// encoded element.
+static gfp_status dot_host_common(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
+                                  void *out, void *stream, bool partial_only) {
     gfp_status st = check_dot_args(dt, a, b, n, out, 1);
     if (st != GFP_OK) return st;
     Ctx *c;
@@ -482,13 +484,27 @@ gfp_status gfp_dot_host(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, co
         e = launch_dot(plan, c->K, S->buf[slot][0], S->buf[slot][1], std::max<int64_t>(len, 0), ws, o, s);
         if (e == cudaSuccess) e = cudaEventRecord(S->consumed[slot], s);
     }
-    if (e == cudaSuccess) {
+    if (e == cudaSuccess && !partial_only) {
         OutSpec o{S->d_out, (int)rep, (int)dt, OUT_ENCODE};
         e = launch_finalize(c->K, S->d_partial, 1, o, s);
     }
-    if (e == cudaSuccess) e = cudaMemcpyAsync(out, S->d_out, es, cudaMemcpyDeviceToHost, s);
+    // the chunks' partials are residues < p summed over at most n / chunk + 1 chunks: no wrap
+    if (e == cudaSuccess)
+        e = partial_only ? cudaMemcpyAsync(out, S->d_partial, 8, cudaMemcpyDeviceToHost, s)
+                         : cudaMemcpyAsync(out, S->d_out, es, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     return e == cudaSuccess ? GFP_OK : cuda_fail(e, "gfp_dot_host");
+}
+
+gfp_status gfp_dot_host(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n, void *out,
+                        void *stream) {
+    return dot_host_common(p, rep, dt, a, b, n, out, stream, false);
+}
+
+gfp_status gfp_dot_host_partial(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
+                                uint64_t *partial, void *stream) {
+    if (partial != nullptr && !aligned(partial, 8)) return fail(GFP_E_INVAL, "partial not 8-byte aligned");
+    return dot_host_common(p, rep, dt, a, b, n, partial, stream, true);
 }
 
 uint64_t gfp_launch_count(int reset) { return launches(reset); }

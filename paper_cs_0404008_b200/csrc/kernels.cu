@@ -538,9 +538,11 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
         if (O.mode == OUT_ENCODE) {
             ((uint16_t *)O.out)[0] = (uint16_t)Z::to_code(v, K.qbar);  // already a Zech code: no log lookup
         } else {  // additive (classical) form for the multi-GPU sum: g^(u+1) from the antilog table
-            const uint64_t r = v == Z::kZ ? 0 : K.antilog[Z::code_nz(v, K.qbar)];  // g^code, both layouts
-            if (O.mode == OUT_PARTIAL) ((uint64_t *)O.out)[0] = r;
-            else ((uint64_t *)O.out)[0] += r;
+            uint64_t r = v == Z::kZ ? 0 : K.antilog[Z::code_nz(v, K.qbar)];  // g^code, both layouts
+            // fused multi-GPU combine: exchange the classical value with the peers, then encode the sum
+            // (write_result: log table) -- the group's sum of Zech elements is not a sum of codes
+            if (O.mode == OUT_XCHG) r = xchg_allreduce(r, O.xchg, K.p, K.mu);
+            write_result(r, O, K, 0);
         }
         *ws.counter = 0;
         pdl_exit();
@@ -657,6 +659,21 @@ __global__ void __launch_bounds__(NT) batch_cl16_kernel(const uint16_t *__restri
 }
 
 // ------------------------------------------------------------------------------ batch: generic
+// Row loads: with L >= 8 lanes per row a warp's 16-byte loads cover whole 128-byte lines (streamed past L1);
+// with one lane per row each lane walks its own row, so its loads may allocate in L1: the second half of a
+// 32-byte sector is then served from L1 instead of a second L2 request.
+template <int LPR>
+__device__ __forceinline__ uint4 ld_row(const uint4 *ptr) {
+    if constexpr (LPR == 1) {
+        uint4 r;
+        asm("ld.global.nc.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+            : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr));
+        return r;
+    } else {
+        return ld_stream(ptr);
+    }
+}
+
 // Warp per row with policy R.  x read through the read-only path (L1-resident, reused by every
 // row).  VEC: rows and x are 16-byte aligned (A, lda*sizeof, x) -> 16-byte loads.
 template <class R, int NT, int U, bool VEC, int LPR, bool XS>
@@ -704,7 +721,7 @@ __global__ void __launch_bounds__(NT) batch_kernel(const typename R::elem *__res
                 for (; v0 + LPR * (U - 1) < nvec; v0 += LPR * U) {
                     uint4 ra[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) ra[u] = ld_stream(av + v0 + u * LPR);
+                    for (int u = 0; u < U; ++u) ra[u] = ld_row<LPR>(av + v0 + u * LPR);
 #pragma unroll
                     for (int u = 0; u < U; ++u) R::vec(acc, ra[u], XS ? xv[v0 + u * LPR] : __ldg(xv + v0 + u * LPR), K, tab);
                 }
@@ -712,7 +729,7 @@ __global__ void __launch_bounds__(NT) batch_kernel(const typename R::elem *__res
                     uint4 ra[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u)
-                        if (v0 + u * LPR < nvec) ra[u] = ld_stream(av + v0 + u * LPR);
+                        if (v0 + u * LPR < nvec) ra[u] = ld_row<LPR>(av + v0 + u * LPR);
 #pragma unroll
                     for (int u = 0; u < U; ++u)
                         if (v0 + u * LPR < nvec)
@@ -932,17 +949,21 @@ static cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cud
 template <typename F>
 static int occupancy(F kernel, int block, size_t smem) {
     static std::mutex mu;
-    static std::unordered_map<std::string, int> cache;     // per (kernel, dynamic smem)
-    static std::unordered_map<uintptr_t, size_t> allowed;  // per kernel: the dynamic smem opt-in so far
+    static std::unordered_map<std::string, int> cache;       // per (device, kernel, dynamic smem)
+    static std::unordered_map<std::string, size_t> allowed;  // per (device, kernel): the smem opt-in so far
     std::lock_guard<std::mutex> g(mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
     const uintptr_t kp = (uintptr_t)reinterpret_cast<const void *>(kernel);
-    // the opt-in is a per-function attribute: only ever raise it (a kernel launched with several table
-    // sizes, e.g. Zech at several primes, must keep the largest one it has been allowed)
-    if (smem > 48 * 1024 && smem > allowed[kp]) {
+    const std::string fkey = std::to_string(dev) + ":" + std::to_string(kp);
+    // the opt-in is a per-function attribute of the current device's context: only ever raise it (a kernel
+    // launched with several table sizes, e.g. Zech at several primes, must keep the largest one it has been
+    // allowed), and once per device (a process driving several GPUs opts in on each)
+    if (smem > 48 * 1024 && smem > allowed[fkey]) {
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        allowed[kp] = smem;
+        allowed[fkey] = smem;
     }
-    const std::string key = std::to_string(kp) + ":" + std::to_string(smem);
+    const std::string key = fkey + ":" + std::to_string(smem);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     int bps = 0;
@@ -1258,7 +1279,8 @@ static const char *policy_name(int pol) {
 
 gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const void *b, int64_t n,
                     const gfp_options *opt, DotPlan *P) {
-    gfp_options tuned;  // AUTO follows the install-time table when it has an admissible entry (F4)
+    if (opt != nullptr && opt->lanes_per_row != 0) return GFP_E_INVAL;  // a batch option (gfp.h)
+    gfp_options tuned{};  // AUTO follows the install-time table when it has an admissible entry (F4)
     if ((opt == nullptr || (opt->strategy == GFP_STRAT_AUTO && opt->acc_bits == 0)) &&
         tuned_options(I, 0, n, 0, &tuned) && plan_dot(I, K, a, b, n, &tuned, P) == GFP_OK)
         return GFP_OK;
@@ -1484,12 +1506,34 @@ static cudaError_t launch_batch_shape(const KParams &K, const void *A, int64_t l
     return launch_batch_lpr<R, NT, U, LPR>(K, A, lda, x, rows, n, vec, grid, O, s);
 }
 
+// Lanes per row of the generic batch kernel: the caller's gfp_options.lanes_per_row, else a full warp per
+// long row (>= 256 vectors) or per table-kernel row, else 8 lanes (4 rows per warp).
+static int batch_lanes(int64_t n, int W, bool table, int want) {
+    if (want != 0) return want;
+    return (n / W >= 256 || table) ? 32 : 8;
+}
+// Upper bound on the terms ONE lane of a row sums in batch_kernel with L lanes per row: vectors g, g + L, ...
+// of W terms each plus every L-th scalar tail term, or (unvectorised rows) every L-th term.  The built-in
+// plan's per-lane overflow tests (Eq. (1) per accumulator) use it with the L the launch will use.
+static u128 batch_per_lane(int64_t n, int W, int L) {
+    const int64_t nvec = n / W;
+    const u128 v = (u128)((nvec + L - 1) / L) * W + (u128)((n - nvec * W + L - 1) / L);
+    return std::max<u128>(v, (u128)((n + L - 1) / L));
+}
+// policies a single lane may own a whole row for (integer storage; gfp.h lanes_per_row = 1)
+template <class R>
+constexpr bool kOneLaneOk = !R::kTable && !std::is_same<typename R::elem, double>::value;
+
 template <class R, int NT, int U>
 static cudaError_t launch_batch_t(const KParams &K, const void *A, int64_t lda, const void *x, int64_t rows,
-                                  int64_t n, bool vec, OutSpec O, cudaStream_t s) {
-    // a full warp per long row (>= 256 vectors) or per table kernel row, else 8 lanes (4 rows per warp)
-    if (n / R::W >= 256 || R::kTable) return launch_batch_shape<R, NT, U, 32>(K, A, lda, x, rows, n, vec, O, s);
-    return launch_batch_shape<R, NT, U, 8>(K, A, lda, x, rows, n, vec, O, s);
+                                  int64_t n, bool vec, int lanes, OutSpec O, cudaStream_t s) {
+    switch (batch_lanes(n, R::W, R::kTable, lanes)) {
+    case 1:
+        if constexpr (kOneLaneOk<R>) return launch_batch_shape<R, NT, U, 1>(K, A, lda, x, rows, n, vec, O, s);
+        return cudaErrorInvalidValue;  // excluded by launch_batch
+    case 8: return launch_batch_shape<R, NT, U, 8>(K, A, lda, x, rows, n, vec, O, s);
+    default: return launch_batch_shape<R, NT, U, 32>(K, A, lda, x, rows, n, vec, O, s);
+    }
 }
 
 gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int64_t lda, const void *x, int64_t rows,
@@ -1499,12 +1543,17 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
     const bool vec = ((uintptr_t)A % 16 == 0) && ((uintptr_t)x % 16 == 0) && ((lda * (int64_t)es) % 16 == 0);
     const uint64_t pm1 = I.p - 1;
     const u128 q2 = (u128)pm1 * pm1, max64 = ~(u128)0 >> 64;
-    const u128 per_lane = (u128)(n + 31) / 32 + 16;
+    const int lanes = opt ? opt->lanes_per_row : 0;
+    if (lanes != 0 && lanes != 1 && lanes != 8 && lanes != 32) return GFP_E_INVAL;
+    // one lane per row: integer storage only (no table, no binary64), gfp.h
+    if (lanes == 1 && (I.rep == GFP_REP_ZECH || I.rep == GFP_REP_FP64 || I.dtype == GFP_F64)) return GFP_E_UNSUPPORTED;
+    // terms one accumulator sums for a policy of W elements per vector (batch_lanes / batch_per_lane)
+    auto per_lane = [&](int W) { return batch_per_lane(n, W, batch_lanes(n, W, false, lanes)); };
     int dev = 0;
     cudaGetDevice(&dev);
     *err = cudaSuccess;
-    gfp_options tuned;  // AUTO follows the install-time table when it has an admissible entry (F4)
-    if ((opt == nullptr || (opt->strategy == GFP_STRAT_AUTO && opt->acc_bits == 0)) &&
+    gfp_options tuned{};  // AUTO follows the install-time table when it has an admissible entry (F4)
+    if ((opt == nullptr || (opt->strategy == GFP_STRAT_AUTO && opt->acc_bits == 0 && opt->lanes_per_row == 0)) &&
         tuned_options(I, 1, n, rows, &tuned)) {
         int xpol = -1, acc_bits = 0;
         uint64_t kblk = 0;
@@ -1521,14 +1570,14 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
             K2.kblk = kblk;
             switch (xpol) {
 #define GFP_BATCH(pol, ...) \
-    case pol: *err = launch_batch_t<__VA_ARGS__, 256, kBatchU>(K2, A, lda, x, rows, n, vec, O, s); break;
+    case pol: *err = launch_batch_t<__VA_ARGS__, 256, kBatchU>(K2, A, lda, x, rows, n, vec, lanes, O, s); break;
                 GFP_CS_CASES(GFP_BATCH)
 #undef GFP_BATCH
-            case P_FP_THREAD: *err = launch_batch_t<Fp64<0>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, O, s); break;
-            case P_FP_K2: *err = launch_batch_t<Fp64<2>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, O, s); break;
-            case P_FP_K1: *err = launch_batch_t<Fp64<1>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, O, s); break;
+            case P_FP_THREAD: *err = launch_batch_t<Fp64<0>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, lanes, O, s); break;
+            case P_FP_K2: *err = launch_batch_t<Fp64<2>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, lanes, O, s); break;
+            case P_FP_K1: *err = launch_batch_t<Fp64<1>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, lanes, O, s); break;
 #define GFP_BATCH_FC(pol, ...) \
-    case pol: *err = launch_batch_t<__VA_ARGS__, 256, kBatchU>(K2, A, lda, x, rows, n, vec, O, s); break;
+    case pol: *err = launch_batch_t<__VA_ARGS__, 256, kBatchU>(K2, A, lda, x, rows, n, vec, lanes, O, s); break;
                 GFP_FC_CASES(GFP_BATCH_FC)
 #undef GFP_BATCH_FC
             default: return GFP_E_UNSUPPORTED;
@@ -1539,7 +1588,7 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
     switch (I.rep) {
     case GFP_REP_CLASSICAL:
         if (I.dtype == GFP_U16) {
-            if (vec && (u128)n * q2 <= max64 && n <= 96 * 1024) {
+            if (vec && lanes == 0 && (u128)n * q2 <= max64 && n <= 96 * 1024) {
                 constexpr int NT = 256;
                 const bool long_rows = n / 8 >= 256;
                 auto kern = long_rows ? batch_cl16_kernel<NT, GFP_CL16_U, 32> : batch_cl16_kernel<NT, 8, 8>;
@@ -1555,10 +1604,10 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
                 }
                 count_launch();
                 *err = cudaGetLastError();
-            } else if (per_lane * q2 <= max64) {
+            } else if (per_lane(8) * q2 <= max64) {
                 *err = (u128)n * q2 <= max64
-                           ? launch_batch_t<ClassicalU16<CL_ALL>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s)
-                           : launch_batch_t<ClassicalU16<CL_THREAD>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
+                           ? launch_batch_t<ClassicalU16<CL_ALL>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s)
+                           : launch_batch_t<ClassicalU16<CL_THREAD>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s);
             } else {
                 return GFP_E_UNSUPPORTED;
             }
@@ -1567,60 +1616,60 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
             KParams K2 = K;
             K2.kblk = lam;
             if ((u128)n * q2 <= max64)
-                *err = launch_batch_t<ClassicalU32<CL_ALL>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
-            else if (per_lane * q2 <= max64)
-                *err = launch_batch_t<ClassicalU32<CL_THREAD>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
+                *err = launch_batch_t<ClassicalU32<CL_ALL>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s);
+            else if (per_lane(4) * q2 <= max64)
+                *err = launch_batch_t<ClassicalU32<CL_THREAD>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s);
             else if (lam >= 4)  // sec. 3.4 hybrid (Eq. (2)), as in plan_dot
                 *err = launch_batch_t<ClassicalS<uint64_t, uint32_t, S_HYBRID>, 256, kBatchU>(K2, A, lda, x, rows, n,
-                                                                                            vec, O, s);
+                                                                                            vec, lanes, O, s);
             else
-                *err = launch_batch_t<ClassicalU32<CL_OVERFLOW>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
+                *err = launch_batch_t<ClassicalU32<CL_OVERFLOW>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s);
         }
         break;
     case GFP_REP_MONTGOMERY:
         if (I.mont_kr >= 4)
-            *err = launch_batch_t<Montgomery<4>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Montgomery<4>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s);
         else if (I.mont_kr >= 2)
-            *err = launch_batch_t<Montgomery<2>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Montgomery<2>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s);
         else
-            *err = launch_batch_t<Montgomery<1>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Montgomery<1>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s);
         break;
     case GFP_REP_FP64:
-        if (per_lane * q2 < ((u128)1 << 53))
-            *err = launch_batch_t<Fp64<0>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
+        if (per_lane(2) * q2 < ((u128)1 << 53))
+            *err = launch_batch_t<Fp64<0>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s);
         else if (I.k >= 2)
-            *err = launch_batch_t<Fp64<2>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Fp64<2>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s);
         else
-            *err = launch_batch_t<Fp64<1>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Fp64<1>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s);
         break;
     case GFP_REP_ZECH:
         // bound by the shared-memory gather (one random lookup per 2-byte term: ~2 T lookups/s on B200);
         // unroll A/B (scripts/ab_zbatch.py): U = 4 for the doubled table, 8 for the folded large-field one
         if (zech_small_layout(I.p))
-            *err = launch_batch_t<Zech<true, false>, 1024, GFP_ZBATCH_U>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Zech<true, false>, 1024, GFP_ZBATCH_U>(K, A, lda, x, rows, n, vec, lanes, O, s);
         else
-            *err = launch_batch_t<Zech<false, false>, 1024, GFP_ZBATCH_UL>(K, A, lda, x, rows, n, vec, O, s);
+            *err = launch_batch_t<Zech<false, false>, 1024, GFP_ZBATCH_UL>(K, A, lda, x, rows, n, vec, lanes, O, s);
         break;
     case GFP_REP_CENTERED: {  // sec. 3.2.2: per-row sums; one reduction per lane unless a row overflows
         const u128 h = (u128)(I.p - 1) / 2, h2 = h * h, w63 = ((u128)1 << 63) - 1;
         KParams K2 = K;
         K2.kblk = I.k;
         if (I.dtype == GFP_F64) {
-            if (per_lane * h2 + h < ((u128)1 << 53))
-                *err = launch_batch_t<Fp64C<0>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s);
+            if (per_lane(2) * h2 + h < ((u128)1 << 53))
+                *err = launch_batch_t<Fp64C<0>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s);
             else
                 switch (fc_policy(I.k)) {
-                case P_FC8: *err = launch_batch_t<Fp64C<8>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s); break;
-                case P_FC4: *err = launch_batch_t<Fp64C<4>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s); break;
-                case P_FC2: *err = launch_batch_t<Fp64C<2>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s); break;
-                default: *err = launch_batch_t<Fp64C<1>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s); break;
+                case P_FC8: *err = launch_batch_t<Fp64C<8>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s); break;
+                case P_FC4: *err = launch_batch_t<Fp64C<4>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s); break;
+                case P_FC2: *err = launch_batch_t<Fp64C<2>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s); break;
+                default: *err = launch_batch_t<Fp64C<1>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s); break;
                 }
         } else if (I.dtype == GFP_U16) {
-            *err = (u128)n * h2 + h <= w63 ? launch_batch_t<CenteredI<int16_t, CE_ALL>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s)
-                                          : launch_batch_t<CenteredI<int16_t, CE_BLOCKED>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, O, s);
+            *err = (u128)n * h2 + h <= w63 ? launch_batch_t<CenteredI<int16_t, CE_ALL>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s)
+                                          : launch_batch_t<CenteredI<int16_t, CE_BLOCKED>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, lanes, O, s);
         } else {
-            *err = (u128)n * h2 + h <= w63 ? launch_batch_t<CenteredI<int32_t, CE_ALL>, 256, kBatchU>(K, A, lda, x, rows, n, vec, O, s)
-                                          : launch_batch_t<CenteredI<int32_t, CE_BLOCKED>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, O, s);
+            *err = (u128)n * h2 + h <= w63 ? launch_batch_t<CenteredI<int32_t, CE_ALL>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s)
+                                          : launch_batch_t<CenteredI<int32_t, CE_BLOCKED>, 256, kBatchU>(K2, A, lda, x, rows, n, vec, lanes, O, s);
         }
         break;
     }

@@ -125,10 +125,16 @@ def dot_fused(a_shard: torch.Tensor, b_shard: torch.Tensor, p: int, rep: int, xc
 
 def dot(a_shard: torch.Tensor, b_shard: torch.Tensor, p: int, rep: int, group=None,
         out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """Exact dot of the globally sharded vectors; every rank receives the result (device, 1 element)."""
-    partial = _dot_partial(a_shard, b_shard, p, rep, stream=stream)
-    combine_partials(partial, group)
-    return _finalize(partial, p, rep, a_shard.dtype, out=out, stream=stream)
+    """Exact dot of the globally sharded vectors; every rank receives the result (device, 1 element).
+
+    With `stream`, the three steps run on it: the all_reduce is issued while `stream` is torch's current
+    stream, so NCCL orders itself after the partial kernel and the finalize kernel after the reduction."""
+    if stream is None:
+        stream = torch.cuda.current_stream(a_shard.device)
+    with torch.cuda.stream(stream):
+        partial = _dot_partial(a_shard, b_shard, p, rep, stream=stream)
+        combine_partials(partial, group)
+        return _finalize(partial, p, rep, a_shard.dtype, out=out, stream=stream)
 
 
 def dot_batch(A_rows: torch.Tensor, x: torch.Tensor, p: int, rep: int, group=None, gather: bool = False,

@@ -61,3 +61,58 @@ def test_reference_arm_runs_on_the_host():
     assert line["cpu_baseline"]["cores"] == bench.host_threads()
     assert line["e2e"]["h2d_bytes_per_step"] == 0
     assert "True" in line["cpu_baseline"]["threads_note"]
+
+
+# ------------------------------------------------------------------------------ --gpus N launcher
+def _env(**kw):
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT", "GFP_BENCH_PG_BACKEND")}
+    env.update(kw)
+    return env
+
+
+def test_launch_plan_rules():
+    # the driver's torchrun form: WORLD_SIZE must equal --gpus
+    assert bench.launch_plan(8, {"WORLD_SIZE": "8"}, 8) == ("run", None)
+    how, why = bench.launch_plan(8, {"WORLD_SIZE": "1"}, 8)
+    assert how == "fail" and "WORLD_SIZE=1" in why
+    # no WORLD_SIZE: one process at N = 1, self-launch N ranks at N > 1
+    assert bench.launch_plan(1, {}, 1) == ("run", None)
+    how, argv = bench.launch_plan(4, {}, 8)
+    assert how == "spawn" and "torch.distributed.run" in argv and "--nproc-per-node=4" in argv
+    assert "127.0.0.1" in argv
+    # more ranks than visible GPUs: fail loudly (never time fewer GPUs than asked for)
+    how, why = bench.launch_plan(2, {}, 1)
+    assert how == "fail" and "only 1 CUDA device" in why
+    # host-logic check mode: ranks may share (or lack) devices
+    assert bench.launch_plan(2, {"GFP_BENCH_PG_BACKEND": "gloo"}, 0)[0] == "spawn"
+    assert bench.launch_plan(0, {}, 8)[0] == "fail"
+
+
+def test_gpus2_self_launches_two_ranks_over_gloo():
+    """`python bench.py --gpus 2` (the driver's plain form, no torchrun) must run TWO ranks: the launcher
+    re-execs itself under torch.distributed.run; --dry-run stops after the process group is up."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                       env=_env(GFP_BENCH_PG_BACKEND="gloo"), capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    line = lines[0]
+    assert line["n_gpus"] == 2 and line["gpus_arg"] == 2 and line["backend"] == "gloo"
+    assert sorted(x["rank"] for x in line["ranks"]) == [0, 1]
+    assert len({x["pid"] for x in line["ranks"]}) == 2  # two processes, not one
+
+
+def test_gpus2_without_enough_gpus_fails_loudly():
+    """On a box with fewer GPUs than --gpus (here: none), the bench refuses instead of timing one GPU and
+    printing n_gpus: 1."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       env=_env(), capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode != 0
+    assert "CUDA device" in r.stderr
+    assert not [x for x in r.stdout.splitlines() if x.startswith("{")]
+    # and a torchrun world that disagrees with --gpus
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                       env=_env(WORLD_SIZE="1", RANK="0", LOCAL_RANK="0"), capture_output=True, text=True,
+                       timeout=300, cwd=ROOT)
+    assert r.returncode != 0 and "WORLD_SIZE=1" in r.stderr
