@@ -63,6 +63,16 @@ CONFIGS = {
             dtype=np.uint32, n=100_000, bpt=8, kind="dot", inputs_of=0, fused1=True),
     8: dict(name="C3-fused1", workload="configs[2] through gfp_dot_allreduce as a one-rank group", p=P31, rep=1,
             dtype=np.uint32, n=1 << 28, bpt=8, kind="dot", inputs_of=2, fused1=True),
+    # configs[4]'s shape over Zech codes (sec. 2.4; 10% zero codes as in configs[3]): the Zech matrix-vector
+    # product, bound by the shared-memory gather (one random table lookup per term) -- secondary lines only
+    9: dict(name="C5-zech32749", workload="configs[4] shape, 65536x4096 Zech u16 codes over GF(32749)", p=32749,
+            rep=3, dtype=np.uint16, rows=65536, n=4096, bpt=2, kind="batch"),
+    10: dict(name="C5-zech65521", workload="configs[4] shape, 65536x4096 Zech u16 codes over GF(65521)", p=65521,
+             rep=3, dtype=np.uint16, rows=65536, n=4096, bpt=2, kind="batch"),
+    # configs[2]'s size at the largest word-size prime: (p-1)^2 ~ 2^64, so a thread's sum wraps on
+    # nearly every product -- the sec. 3.3 carry word (the carry flag of each 64-bit add counted)
+    11: dict(name="C3-p4294967291", workload="configs[2] size, GF(4294967291) classical u32 dot, n=2^28",
+             p=4294967291, rep=0, dtype=np.uint32, n=1 << 28, bpt=8, kind="dot"),
 }
 REP_NAMES = {0: "classical", 1: "montgomery", 2: "fp64", 3: "zech", 4: "centered"}
 DTYPE_NAMES = {np.dtype(np.uint16): "u16", np.dtype(np.uint32): "u32", np.dtype(np.float64): "f64"}
@@ -194,8 +204,12 @@ def host_inputs(cfg, rank, world, limit=None):
         n = cfg["n"]
         if limit is not None:
             r1 = min(r1, r0 + max(1, limit // n))
-        A = synth.uniform(seed, synth.STREAM_MAT, r0 * n, (r1 - r0) * n, p, cfg["dtype"])
-        x = synth.uniform(seed, synth.STREAM_X, 0, n, p, cfg["dtype"])
+        if cfg["rep"] == 3:
+            A = synth.zech_codes(seed, synth.STREAM_MAT, r0 * n, (r1 - r0) * n, p - 1)
+            x = synth.zech_codes(seed, synth.STREAM_X, 0, n, p - 1)
+        else:
+            A = synth.uniform(seed, synth.STREAM_MAT, r0 * n, (r1 - r0) * n, p, cfg["dtype"])
+            x = synth.uniform(seed, synth.STREAM_X, 0, n, p, cfg["dtype"])
         return {"A": A.reshape(r1 - r0, n), "x": x, "rows": r1 - r0}
     s0, s1 = shard(cfg["n"], rank, world)
     if limit is not None:
@@ -792,6 +806,23 @@ def e2e_leg(gfp, cfg, d, world, steps, stream, dev, want=None):
             "clock": "host wall clock around synchronous calls, max over ranks"}
 
 
+def lookup_wavefronts(A, lanes=32, per_vec=8, sample_rows=64):
+    """Shared-memory wavefronts per warp-wide lookup for the Zech matrix-vector kernel on these codes: lane l
+    of a warp decodes code k of its 16-byte vector (codes 8 (v0 + l) + k of the row), i.e. 32 codes 8 apart;
+    T[c] is the u16 at byte 2c, so bank (c >> 1) & 31, and a warp lookup takes as many wavefronts as the
+    most distinct 32-bit words any one bank is asked for (distinct lanes reading the same word share it)."""
+    A = np.asarray(A[:sample_rows], dtype=np.int64)
+    n = A.shape[1] // (lanes * per_vec) * (lanes * per_vec)
+    c = A[:, :n].reshape(-1, lanes, per_vec).transpose(0, 2, 1).reshape(-1, lanes)  # (warp lookups, lanes)
+    words = c >> 1
+    key = np.sort(((words & 31) << 20) | words, axis=1)
+    new = np.ones_like(key, dtype=bool)
+    new[:, 1:] = key[:, 1:] != key[:, :-1]
+    counts = np.zeros((key.shape[0], 32), dtype=np.int64)
+    np.add.at(counts, (np.repeat(np.arange(key.shape[0]), lanes)[new.reshape(-1)], (key >> 20)[new]), 1)
+    return float(counts.max(axis=1).mean())
+
+
 def secondary_table(gfp, args, dev, stream, exclude):
     """Kernel-only throughput of every other config (1 GPU), with roofline fraction."""
     peak, _ = peak_hbm()
@@ -843,6 +874,17 @@ def secondary_table(gfp, args, dev, stream, exclude):
                               "l2": f"{len(reps)} rotating input copies (>= 3x L2)"}
         if phases:
             table[cfg["name"]]["phases"] = phases
+        if cfg["kind"] == "batch" and cfg["rep"] == 3:
+            # second roofline: the shared-memory gather (one random lookup per term, 1 wavefront per clock per SM)
+            wf = lookup_wavefronts(h["A"])
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            clk = (ClockSampler(dev.index).max_mhz or 1965) * 1e6
+            roof_us = terms / 32 * wf / (sms * clk) * 1e6
+            table[cfg["name"]]["gather_roofline"] = {
+                "bound": "smem_gather", "lookups": terms, "wavefronts_per_warp_lookup": round(wf, 3),
+                "sms": sms, "clock_mhz": clk / 1e6, "us": round(roof_us, 2), "frac": round(roof_us / (avg * 1e3), 4),
+                "note": "one random antilog lookup per term; wavefronts = the most distinct 32-bit words any bank "
+                        "serves per warp lookup, from these codes; 1 shared-memory wavefront per clock per SM"}
         if xchg is not None:  # the fused result must equal the plain dot's
             with torch.cuda.stream(stream):
                 plain = gfp.dot(reps[0]["a"], reps[0]["b"], cfg["p"], cfg["rep"], stream=stream)
@@ -869,8 +911,11 @@ def sweep_primes(gfp):
         while x > 2 and not prime(x):
             x -= 1
         return x
+    # landmarks: the paper's 2897 step (512 (p-1)^2 < 2^32, one accumulator per row) with its
+    # neighbours 2887 / 2903, the same step for the default 8-lane kernel (64 terms per accumulator: 64 (p-1)^2
+    # < 2^32 up to 8191, not at 8209), and the primes the paper names
     small = sorted({prev_prime(int(round(3 * (65521 / 3) ** (i / 47)))) for i in range(48)} |
-                   {3, 2887, 2897, 2903, 32749, 40009, 40499, 46337, 65521})
+                   {3, 2887, 2897, 2903, 8191, 8209, 32749, 40009, 40499, 46337, 65521})
     large = [65537, prev_prime(1 << 20), prev_prime(1 << 24), prev_prime(1 << 28), 2 ** 31 - 1, 3037000493,
              4294967291]
     return small, large
@@ -889,10 +934,14 @@ def prime_sweep(args):
     rows, n = args.sweep_rows, 512
     peak, _ = peak_hbm()
     # "auto": AUTO with the install-time table (F4); "builtin": AUTO with the table cleared (the analytic plan)
-    strategies = [("auto", gfp.AUTO, 0), ("builtin", gfp.AUTO, 0), ("blocked32", gfp.BLOCKED, 32),
-                  ("overflow32", gfp.OVERFLOW, 32), ("hybrid32", gfp.HYBRID, 32), ("carry32", gfp.CARRY, 32),
-                  ("blocked64", gfp.BLOCKED, 64), ("overflow64", gfp.OVERFLOW, 64), ("hybrid64", gfp.HYBRID, 64),
-                  ("carry64", gfp.CARRY, 64)]
+    # (column, strategy, m, lanes per row): lanes 0 = the library's choice (8 lanes for DIM = 512 rows, 64 terms
+    # per accumulator); lanes 1 = ONE accumulator walks the whole row, the paper's own loop
+    strategies = [("auto", gfp.AUTO, 0, 0), ("builtin", gfp.AUTO, 0, 0), ("blocked32", gfp.BLOCKED, 32, 0),
+                  ("overflow32", gfp.OVERFLOW, 32, 0), ("hybrid32", gfp.HYBRID, 32, 0), ("carry32", gfp.CARRY, 32, 0),
+                  ("blocked64", gfp.BLOCKED, 64, 0), ("overflow64", gfp.OVERFLOW, 64, 0), ("hybrid64", gfp.HYBRID, 64, 0),
+                  ("carry64", gfp.CARRY, 64, 0),
+                  ("blocked32_1lane", gfp.BLOCKED, 32, 1), ("hybrid32_1lane", gfp.HYBRID, 32, 1),
+                  ("delayed64_1lane", gfp.DELAYED, 64, 1)]
     table = gfp.tune_entries()
     cells = []
     out = open(args.sweep, "w")
@@ -904,7 +953,7 @@ def prime_sweep(args):
         torch.cuda.synchronize()
         ref = gfp.dot_batch(A, x, p, gfp.CLASSICAL)
         nbytes = A.numel() * A.element_size() + n * A.element_size() + rows * A.element_size()
-        for name, strat, m in strategies:
+        for name, strat, m, lanes in strategies:
             if name == "builtin":
                 gfp.tune_clear()
             elif name == "blocked32":
@@ -915,13 +964,15 @@ def prime_sweep(args):
                 continue
             o = torch.empty(rows, dtype=dt_t, device=dev)
             with torch.cuda.stream(stream):
-                gfp.dot_batch_ex(A, x, p, gfp.CLASSICAL, strategy=strat, acc_bits=m, out=o, stream=stream)
+                gfp.dot_batch_ex(A, x, p, gfp.CLASSICAL, strategy=strat, acc_bits=m, out=o, stream=stream,
+                                 lanes_per_row=lanes)
                 stream.synchronize()
                 ok = bool(torch.equal(o, ref))
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=stream):
                     for _ in range(4):
-                        gfp.dot_batch_ex(A, x, p, gfp.CLASSICAL, strategy=strat, acc_bits=m, out=o, stream=stream)
+                        gfp.dot_batch_ex(A, x, p, gfp.CLASSICAL, strategy=strat, acc_bits=m, out=o, stream=stream,
+                                         lanes_per_row=lanes)
                 g.replay()
                 stream.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -932,10 +983,13 @@ def prime_sweep(args):
                 stream.synchronize()
             us = e0.elapsed_time(e1) * 1e3 / 20
             blk = pl["block"] if pl["block"] else None
-            cell = {"p": p, "strategy": name, "acc_bits": pl["acc_bits"], "block_k": blk,
+            # lanes the batch kernel gives a DIM = 512 row: the caller's choice, else 8 (n / W < 256 vectors)
+            L = lanes if lanes else 8
+            tpl = -(-n // L)  # terms one accumulator sums
+            cell = {"p": p, "strategy": name, "acc_bits": pl["acc_bits"], "block_k": blk, "lanes_per_row": L,
                     "reductions_per_dim512_sequential": (None if not blk else -(-n // blk)) if name != "auto" else 1,
-                    "terms_per_lane": n // 32,
-                    "reductions_per_lane": (None if not blk else -(-(n // 32) // blk)),
+                    "terms_per_lane": tpl,
+                    "reductions_per_lane": (None if not blk else -(-tpl // blk)),
                     "us": us, "terms_per_s": rows * n / (us / 1e6), "GB/s": nbytes / (us / 1e6) / 1e9,
                     "frac_of_measured_hbm": nbytes / (us / 1e6) / 1e9 / peak, "equal_to_default": ok}
             cells.append(cell)

@@ -71,6 +71,28 @@ __device__ __forceinline__ double ntl_reduce(double T, double P, double invP) {
     return T;
 }
 
+// ------------------------------------------------------------------------------ carry-flag accumulation
+// The carry word of sec. 3.3 ("division on demand") with the hardware carry flag: the product x y
+// is added to the accumulator with add-with-carry instructions and the carry out of the top word is counted
+// in c -- no compare, no branch, no correction inside the loop; the thread's value c 2^m + s is reduced once
+// at the end (c (2^m mod p) + s).  m = 64: s += x y as mad.lo.cc / madc.hi.cc on the two 32-bit halves of s
+// (the multiply and the 64-bit add are one pair of multiply-adds), then c += carry.
+__device__ __forceinline__ void mac_carry64(uint64_t &s, uint32_t &c, uint32_t x, uint32_t y) {
+    asm("{\n\t.reg .u32 lo, hi;\n\t"
+        "mov.b64 {lo, hi}, %0;\n\t"
+        "mad.lo.cc.u32 lo, %2, %3, lo;\n\t"
+        "madc.hi.cc.u32 hi, %2, %3, hi;\n\t"
+        "addc.u32 %1, %1, 0;\n\t"
+        "mov.b64 %0, {lo, hi};\n\t}"
+        : "+l"(s), "+r"(c) : "r"(x), "r"(y));
+}
+// m = 32 (the product fits 32 bits: (p-1)^2 < 2^32, host-checked): s += x y with carry out, c += carry.
+__device__ __forceinline__ void mac_carry32(uint32_t &s, uint32_t &c, uint32_t x, uint32_t y) {
+    asm("mad.lo.cc.u32 %0, %2, %3, %0;\n\t"
+        "addc.u32 %1, %1, 0;"
+        : "+r"(s), "+r"(c) : "r"(x), "r"(y));
+}
+
 // ------------------------------------------------------------------------------ policies
 enum ClassicalMode { CL_ALL = 0, CL_THREAD = 1, CL_OVERFLOW = 2 };
 
@@ -463,7 +485,8 @@ struct Ops {
 //   S_OVERFLOW sec. 3.3 listing P:414-422: sum += product; if (sum < product) sum += CORR
 //   S_HYBRID   sec. 3.4, Eq. (2): one wrap test per block of K.kblk = lambda products,
 //              lambda p (p-1) < 2^m; the block sum cannot wrap twice nor re-wrap after CORR
-//   S_CARRY    sec. 3.3 with the correction deferred: carry += (sum < product) counts the wraps;
+//   S_CARRY    sec. 3.3 with the correction deferred: the carry flag of the m-bit addition is counted in a
+//              second word (mac_carry64 / mac_carry32; Acc::cnt holds the count);
 //              the thread's value is carry 2^m + sum = carry (2^m mod p) + sum (mod p)
 enum Strategy { S_DELAYED = 1, S_BLOCKED = 2, S_OVERFLOW = 3, S_HYBRID = 4, S_CARRY = 6 };
 
@@ -505,9 +528,9 @@ struct ClassicalS {
         } else if (STRAT == S_OVERFLOW) {
             A.s += prod;
             if (A.s < prod) A.s += corr(K);
-        } else if (STRAT == S_CARRY) {
-            A.s += prod;
-            A.base += A.s < prod;  // `base` holds the wrap count (carry word)
+        } else if (STRAT == S_CARRY) {  // carry flag of the m-bit add counted in cnt (the carry word)
+            if constexpr (sizeof(ACC) == 8) mac_carry64(A.s, A.cnt, x, y);
+            else mac_carry32(A.s, A.cnt, x, y);
         } else {  // S_HYBRID: close the block (its one wrap test) before it would exceed lambda products
             if (A.cnt >= K.kblk) {
                 if (A.s < A.base) A.s += corr(K);
@@ -570,7 +593,7 @@ struct ClassicalS {
     }
     __device__ __forceinline__ static uint64_t finish(Acc &A, const KParams &K) {
         if (STRAT == S_CARRY) {  // carry 2^m + s: carry < 2^32 terms per thread, (2^m mod p) < p < 2^32
-            const uint64_t c = mod_p((uint64_t)A.base, K.p, K.mu) * (sizeof(ACC) == 4 ? (uint64_t)K.corr32 : K.corr);
+            const uint64_t c = mod_p((uint64_t)A.cnt, K.p, K.mu) * (sizeof(ACC) == 4 ? (uint64_t)K.corr32 : K.corr);
             return mod_p(mod_p(c, K.p, K.mu) + (uint64_t)reduce(A.s, K), K.p, K.mu);
         }
         if (STRAT == S_HYBRID && A.s < A.base) A.s += corr(K);  // the last, partial block
@@ -614,13 +637,11 @@ struct MontgomeryCarry {
     using elem = uint32_t;
     static constexpr int W = 4;
     static constexpr bool kTable = false;
-    struct Acc { uint64_t S, carry; };
+    struct Acc { uint64_t S; uint32_t carry; };
     __device__ __forceinline__ static void init(Acc &A) { A.S = 0; A.carry = 0; }
     __device__ __forceinline__ static void term(Acc &A, uint32_t x, uint32_t y, const KParams &,
                                                 const uint16_t * = nullptr) {
-        const uint64_t prod = (uint64_t)x * y;
-        A.S += prod;
-        A.carry += A.S < prod;
+        mac_carry64(A.S, A.carry, x, y);  // carry flag of the 64-bit add counted (sec. 3.3 carry word)
     }
     __device__ __forceinline__ static void vec(Acc &A, uint4 x, uint4 y, const KParams &K, const uint16_t *) {
         term(A, x.x, y.x, K);

@@ -658,6 +658,115 @@ __global__ void __launch_bounds__(NT) batch_cl16_kernel(const uint16_t *__restri
     pdl_exit();
 }
 
+// ------------------------------------------------------------------------------ batch: Zech matrix-vector
+// Zech codes (sec. 2.4), A row-major, x shared by every row.  The product of g^i and g^j costs ONE
+// shared-memory lookup per term in either design; this kernel decodes instead of adding indices: each code c
+// of A is decoded with one lookup T[c] (T = the antilog table on [0, qbar], T[0] = 0 for the zero element), x
+// is decoded once per CTA and staged byte-split as in batch_cl16, and each pair of decoded terms costs two
+// DP2A (as C5).  The table holds q entries instead of the 2q - 1 an index sum needs, and there is no zero test
+// and no index add or fold per term (the large-field index-add kernel was ALU-bound, 89% ALU pipe).  A warp
+// walks RP rows at once, so each staged x read serves RP rows (x reads are a quarter-warp LDS.128: 4
+// wavefronts per 256 terms, against ~27 for the random lookups).  The shared-memory gather is the binding
+// ceiling.  Row value = sum lo + 256 sum hi, one mod p, log-table encoding.
+template <int NT, int U, int MINB, int RP>
+__global__ void __launch_bounds__(NT, MINB) batch_zech_kernel(const uint16_t *__restrict__ A, int64_t lda,
+                                                              const uint16_t *__restrict__ x, int64_t rows, int64_t n,
+                                                              KParams K, OutSpec O, uint32_t tab_entries) {
+    extern __shared__ __align__(16) uint16_t s_tab[];
+    stage_table(s_tab, K.antilog, tab_entries);  // library-owned table: staged before the PDL wait
+    batch_pdl_enter<U, 32, NT>(A, lda, rows, n / 8, O.prefetch != 0);
+    uint32_t *s_xw = reinterpret_cast<uint32_t *>(s_tab + tab_entries);  // tab_entries: a multiple of 8
+    __syncthreads();
+    if (threadIdx.x == 0) s_tab[0] = 0;  // code 0 is the zero element (the doubled layout holds g^0 there)
+    __syncthreads();
+    const uint32_t qbar = K.qbar, qq = qbar | (qbar << 16);
+    // x decoded and byte-split: w_j = (x_{2j} lo, x_{2j+1} lo, x_{2j} hi, x_{2j+1} hi) of the decoded values
+    const int64_t nw = (n + 1) / 2, nwpad = (nw + 3) & ~int64_t(3);
+    for (int64_t j = threadIdx.x; j < nwpad; j += NT) {
+        const uint32_t c0 = 2 * j < n ? min((uint32_t)x[2 * j], qbar) : 0u;
+        const uint32_t c1 = 2 * j + 1 < n ? min((uint32_t)x[2 * j + 1], qbar) : 0u;
+        const uint32_t x0 = s_tab[c0], x1 = s_tab[c1];
+        s_xw[j] = (x0 & 0xFFu) | ((x1 & 0xFFu) << 8) | ((x0 >> 8) << 16) | ((x1 >> 8) << 24);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nvec = n / 8;
+    const uint4 *xv = reinterpret_cast<const uint4 *>(s_xw);
+    // two decoded codes of one 32-bit word (clamped: non-canonical codes never leave the table) -> packed u16 pair
+    auto dec2 = [&](uint32_t w) -> uint32_t {
+        const uint32_t c = __vminu2(w, qq);
+        return (uint32_t)s_tab[c & 0xFFFFu] | ((uint32_t)s_tab[c >> 16] << 16);
+    };
+    // one 16-byte vector of 8 codes against the staged x words: 2 DP2A per pair of terms
+    auto vec8 = [&](const uint4 a, const uint4 w, uint32_t &lo, uint32_t &hi) {
+        uint32_t d = dec2(a.x);
+        lo = __dp2a_lo(d, w.x, lo);
+        hi = __dp2a_hi(d, w.x, hi);
+        d = dec2(a.y);
+        lo = __dp2a_lo(d, w.y, lo);
+        hi = __dp2a_hi(d, w.y, hi);
+        d = dec2(a.z);
+        lo = __dp2a_lo(d, w.z, lo);
+        hi = __dp2a_hi(d, w.z, hi);
+        d = dec2(a.w);
+        lo = __dp2a_lo(d, w.w, lo);
+        hi = __dp2a_hi(d, w.w, hi);
+    };
+    const int64_t warp0 = (int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
+    const int64_t wstride = (int64_t)gridDim.x * (NT / 32);
+    for (int64_t r0 = warp0 * RP; r0 < rows; r0 += wstride * RP) {
+        const uint4 *av[RP];
+        uint64_t tot[RP];
+#pragma unroll
+        for (int k = 0; k < RP; ++k) {
+            av[k] = reinterpret_cast<const uint4 *>(A + (r0 + k < rows ? r0 + k : r0) * lda);
+            tot[k] = 0;
+        }
+        int64_t v0 = lane;
+        // full chunks: U 16-byte loads per row per lane in flight, then the lookups; x read once per RP rows
+        for (; v0 + 32 * (U - 1) < nvec; v0 += 32 * U) {
+            uint4 ra[RP][U];
+#pragma unroll
+            for (int k = 0; k < RP; ++k)
+#pragma unroll
+                for (int u = 0; u < U; ++u) ra[k][u] = ld_stream(av[k] + v0 + u * 32);
+            uint32_t lo[RP], hi[RP];  // <= 4U dp2a of < 2^25 each: no wrap for U <= 32
+#pragma unroll
+            for (int k = 0; k < RP; ++k) lo[k] = hi[k] = 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint4 w = xv[v0 + u * 32];
+#pragma unroll
+                for (int k = 0; k < RP; ++k) vec8(ra[k][u], w, lo[k], hi[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < RP; ++k) tot[k] += (uint64_t)lo[k] + ((uint64_t)hi[k] << 8);
+        }
+        for (; v0 < nvec; v0 += 32) {  // remaining vectors of the rows
+            const uint4 w = xv[v0];
+#pragma unroll
+            for (int k = 0; k < RP; ++k) {
+                uint32_t lo = 0, hi = 0;
+                vec8(ld_stream(av[k] + v0), w, lo, hi);
+                tot[k] += (uint64_t)lo + ((uint64_t)hi << 8);
+            }
+        }
+        for (int64_t j = nvec * 8 + lane; j < n; j += 32) {  // scalar tail: decoded x from the byte-split words
+            const uint32_t w = s_xw[j >> 1], sh = (j & 1) * 8;
+            const uint32_t xvj = ((w >> sh) & 0xFFu) | (((w >> (16 + sh)) & 0xFFu) << 8);
+#pragma unroll
+            for (int k = 0; k < RP; ++k)
+                tot[k] += (uint64_t)s_tab[min((uint32_t)reinterpret_cast<const uint16_t *>(av[k])[j], qbar)] * xvj;
+        }
+#pragma unroll
+        for (int k = 0; k < RP; ++k) {
+            const uint64_t t = warp_sum(tot[k]);  // row total < n (p-1)^2 < 2^64 (host-checked)
+            if (lane == 0 && r0 + k < rows) write_result(mod_p(t, K.p, K.mu), O, K, r0 + k);
+        }
+    }
+    pdl_exit();
+}
+
 // ------------------------------------------------------------------------------ batch: generic
 // Row loads: with L >= 8 lanes per row a warp's 16-byte loads cover whole 128-byte lines (streamed past L1);
 // with one lane per row each lane walks its own row, so its loads may allocate in L1: the second half of a
@@ -784,6 +893,15 @@ __device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab)
 #endif
 #ifndef GFP_ZBATCH_U
 #define GFP_ZBATCH_U 4  // 16-byte vectors per lane in flight in the Zech batch (doubled table)
+#endif
+#ifndef GFP_ZBATCH_DECODE
+#define GFP_ZBATCH_DECODE 1  // 1: Zech matrix-vector by decode + DP2A (batch_zech_kernel); 0: index-add batch_kernel
+#endif
+#ifndef GFP_ZDEC_RP
+#define GFP_ZDEC_RP 2  // rows a warp of the decode batch walks at once (each staged x read serves RP rows)
+#endif
+#ifndef GFP_ZDEC_U
+#define GFP_ZDEC_U 4  // 16-byte A vectors per row and lane in flight in the decode batch
 #endif
 #ifndef GFP_ZBATCH_UL
 #define GFP_ZBATCH_UL 8  // the same for the large-field (q-entry, folded index) table
@@ -1359,10 +1477,13 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
                 kblk = lam;
                 reductions = (int64_t)(per_thread / lam) + 1;
             } else {
-                pol = P_CL32_OVF;  // sec. 3.3 overflow detection (u16 products never need it)
+                // sec. 3.3 division on demand with the carry word (lambda < 4: p > ~2^31.5, u32 storage): the
+                // carry flag of each 64-bit add counted, one reduction per thread (B200: replaces a wrap test
+                // + CORR per product, 1.15 T terms/s at p = 4294967291)
+                pol = cs_policy(true, true, GFP_STRAT_CARRY);
                 acc = GFP_ACC_OVERFLOW;
-                strat = GFP_STRAT_OVERFLOW;
-                reductions = (int64_t)per_thread;  // one wrap test per term
+                strat = GFP_STRAT_CARRY;
+                reductions = 1;
             }
             break;
         case GFP_REP_MONTGOMERY:
@@ -1428,9 +1549,11 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
               : (strat == GFP_STRAT_BLOCKED ? GFP_ACC_BLOCKED : GFP_ACC_DELAYED);
         if (pol == P_FP_K2 || pol == P_FP_K1) kblk = pol == P_FP_K2 ? 2 : 1;
         if (is_fc(pol)) kblk = fc_block(pol);
-        if (strat == GFP_STRAT_OVERFLOW || strat == GFP_STRAT_ZECH_ADD || strat == GFP_STRAT_CARRY) {
+        if (strat == GFP_STRAT_OVERFLOW || strat == GFP_STRAT_ZECH_ADD) {
             reductions = (int64_t)per_thread;  // one wrap test / one Zech addition (table lookup) per term
             if (pol == P_ZECH_ADD) acc_bits = 0;
+        } else if (strat == GFP_STRAT_CARRY) {
+            reductions = 1;  // the carry flag is counted, never tested: one reduction per thread at the end
         } else if (strat == GFP_STRAT_BLOCKED || strat == GFP_STRAT_HYBRID)
             reductions = (int64_t)(kblk ? per_thread / kblk : 0) + 1;
     }
@@ -1622,8 +1745,9 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
             else if (lam >= 4)  // sec. 3.4 hybrid (Eq. (2)), as in plan_dot
                 *err = launch_batch_t<ClassicalS<uint64_t, uint32_t, S_HYBRID>, 256, kBatchU>(K2, A, lda, x, rows, n,
                                                                                             vec, lanes, O, s);
-            else
-                *err = launch_batch_t<ClassicalU32<CL_OVERFLOW>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s);
+            else  // lambda < 4: the carry word (as plan_dot)
+                *err = launch_batch_t<ClassicalS<uint64_t, uint32_t, S_CARRY>, 256, kBatchU>(K, A, lda, x, rows, n, vec,
+                                                                                           lanes, O, s);
         }
         break;
     case GFP_REP_MONTGOMERY:
@@ -1642,14 +1766,36 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
         else
             *err = launch_batch_t<Fp64<1>, 256, kBatchU>(K, A, lda, x, rows, n, vec, lanes, O, s);
         break;
-    case GFP_REP_ZECH:
-        // bound by the shared-memory gather (one random lookup per 2-byte term: ~2 T lookups/s on B200);
+    case GFP_REP_ZECH: {
+        // decode kernel (batch_zech_kernel) for aligned rows: one lookup per term in a q-entry table; the row
+        // total n (p-1)^2 must fit the u64 (always for n < 2^32)
+        const uint32_t zentries = (uint32_t)((I.p + 7) & ~7ull);  // codes [0, qbar] = p entries
+        const size_t zsmem = (size_t)zentries * 2 + (size_t)(((n + 1) / 2 + 3) & ~int64_t(3)) * 4;
+        if (GFP_ZBATCH_DECODE && vec && lanes == 0 && (u128)n * q2 <= max64 && zsmem <= kBatchSmemX) {
+            const uint32_t entries = zentries;
+            const size_t smem = zsmem;
+            // one 1024-thread CTA per SM (64 registers: U = 4 vectors per row and lane for RP = 2 rows in flight);
+            // B200 A/B (scripts/ab_zbatch.py, GF(32749) / GF(65521)): three 512-thread CTAs at 40 registers
+            // (U = 2) 152.7 / - us, RP = 1 137.8 / 138.1, RP = 4 (U = 1) 148.7 / 149.1, this 130.7 (65521);
+            // a register ping-pong pipeline over (row, chunk) spilled and ran 173-190 us
+            auto kern = batch_zech_kernel<1024, GFP_ZDEC_U, 1, GFP_ZDEC_RP>;
+            const int bps = occupancy(kern, 1024, smem);
+            const int64_t rpb = 32 * GFP_ZDEC_RP;  // rows per CTA per sweep (a warp per RP rows)
+            const int64_t grid = std::min<int64_t>((rows + rpb - 1) / rpb, (int64_t)num_sms(dev) * bps);
+            cudaError_t le = launch_pdl(kern, dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(1024), smem, s,
+                                        (const uint16_t *)A, lda, (const uint16_t *)x, rows, n, K, O, entries);
+            count_launch();
+            *err = le != cudaSuccess ? le : cudaGetLastError();
+            break;
+        }
+        // index-add kernel (batch_kernel<Zech>): unaligned rows or an explicit lanes_per_row.
         // unroll A/B (scripts/ab_zbatch.py): U = 4 for the doubled table, 8 for the folded large-field one
         if (zech_small_layout(I.p))
             *err = launch_batch_t<Zech<true, false>, 1024, GFP_ZBATCH_U>(K, A, lda, x, rows, n, vec, lanes, O, s);
         else
             *err = launch_batch_t<Zech<false, false>, 1024, GFP_ZBATCH_UL>(K, A, lda, x, rows, n, vec, lanes, O, s);
         break;
+    }
     case GFP_REP_CENTERED: {  // sec. 3.2.2: per-row sums; one reduction per lane unless a row overflows
         const u128 h = (u128)(I.p - 1) / 2, h2 = h * h, w63 = ((u128)1 << 63) - 1;
         KParams K2 = K;

@@ -1,19 +1,50 @@
 #!/usr/bin/env python
-"""Render a bench.py --sweep JSONL file as a text table (terms/s in units of 10^12 per strategy)."""
+"""Render a bench.py --sweep JSONL file as a text table (terms/s in units of 10^12 per strategy), plus the
+cost of one reduction per row fitted from the one-lane blocked32 column."""
 import collections
 import json
 import sys
+
+import numpy as np
 
 cells = [json.loads(line) for line in open(sys.argv[1])]
 by = collections.defaultdict(dict)
 for c in cells:
     by[c["p"]][c["strategy"]] = c
-names = ["auto", "builtin", "blocked32", "overflow32", "hybrid32", "carry32", "blocked64", "overflow64", "hybrid64", "carry64"]
-print("# F1 prime sweep (bench.py --sweep): DIM=512 dots, 2^19 rows per cell; terms/s / 1e12 per strategy (auto = AUTO with the shipped install-time table, builtin = AUTO without it); k32 = blocked "
-      "block length at m=32; red/lane32 = reductions per lane (16 terms); all cells bit-equal to the default plan: %s"
-      % all(c["equal_to_default"] for c in cells))
-print("p".rjust(11), *[n.rjust(10) for n in names], "k32".rjust(11), "red/lane32".rjust(10))
+names = ["auto", "builtin", "blocked32", "hybrid32", "blocked32_1lane", "hybrid32_1lane", "delayed64_1lane",
+         "overflow32", "carry32", "blocked64", "overflow64", "hybrid64", "carry64"]
+short = {"blocked32_1lane": "blk32_1L", "hybrid32_1lane": "hyb32_1L", "delayed64_1lane": "del64_1L"}
+print("# F1 prime sweep (bench.py --sweep): DIM=512 dots, %d rows per cell; terms/s / 1e12 per strategy" % cells[0].get("rows", 0)
+      if "rows" in cells[0] else "# F1 prime sweep (bench.py --sweep): DIM=512 dots; terms/s / 1e12 per strategy")
+print("# auto = AUTO with the shipped install-time table, builtin = AUTO without it; columns without _1L run the "
+      "library's 8 lanes per row (64 terms per accumulator), _1L one accumulator per row (the paper's loop, 512 terms)")
+print("# k32 = blocked block length at m=32; red/row1L = reductions per row with one lane (ceil(512/k32)); "
+      "red/lane8 = reductions per accumulator with 8 lanes (ceil(64/k32))")
+print("# all cells bit-equal to the default plan: %s" % all(c["equal_to_default"] for c in cells))
+print("p".rjust(11), *[short.get(n, n).rjust(10) for n in names], "k32".rjust(11), "red/row1L".rjust(10),
+      "red/lane8".rjust(10))
 for p in sorted(by):
-    row = [f"{by[p][n]['terms_per_s'] / 1e12:10.2f}" if n in by[p] else " " * 10 for n in names]
+    row = [f"{by[p][n]['terms_per_s'] / 1e12:10.3f}" if n in by[p] else " " * 10 for n in names]
     b = by[p].get("blocked32", {})
-    print(str(p).rjust(11), *row, str(b.get("block_k", "")).rjust(11), str(b.get("reductions_per_lane", "")).rjust(10))
+    b1 = by[p].get("blocked32_1lane", {})
+    print(str(p).rjust(11), *row, str(b.get("block_k", "")).rjust(11), str(b1.get("reductions_per_lane", "")).rjust(10),
+          str(b.get("reductions_per_lane", "")).rjust(10))
+
+# cost of one reduction per row (one lane): time per row = t0 + c * reductions, least squares over the primes
+pts = [(c["reductions_per_lane"], c["us"]) for c in cells if c["strategy"] == "blocked32_1lane" and c["reductions_per_lane"]]
+if len(pts) > 3:
+    r = np.array([x for x, _ in pts], float)
+    t = np.array([y for _, y in pts], float)
+    A = np.stack([np.ones_like(r), r], 1)
+    (t0, cost), *_ = np.linalg.lstsq(A, t, rcond=None)
+    one = t[r == 1]
+    print("\n# one-lane blocked32: time per launch = %.2f us + %.3f us x (reductions per row)   [least squares, %d primes]"
+          % (t0, cost, len(pts)))
+    if len(one) > 1:
+        print("# spread of the launches with ONE reduction per row (p <= 2897): %.2f .. %.2f us (sd %.3f us)"
+              % (one.min(), one.max(), one.std()))
+    print("# predicted step 2897 -> 2903 (1 -> 2 reductions per row): +%.3f us = %.2f%% of %.2f us" % (cost, 100 * cost / t0, t0))
+    for p in (2887, 2897, 2903):
+        c = by.get(p, {}).get("blocked32_1lane")
+        if c:
+            print("#   p = %d: %.3f us, %d reduction(s) per row" % (p, c["us"], c["reductions_per_lane"]))

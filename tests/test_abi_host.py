@@ -236,12 +236,13 @@ def test_tuned_auto_follows_nearest_case(clean_table):
     ("switching thresholds"), only when admissible; otherwise the built-in plan."""
     P = gfp.plan
     # built-in plan when a thread's sum can wrap: Eq. (2) hybrid while lambda = floor((2^64-1)/(p(p-1))) >= 4,
-    # the per-product overflow test (sec. 3.3) below (lambda = 1 at 4294967291)
+    # the carry word (sec. 3.3, the carry flag counted) below (lambda = 1 at 4294967291)
     builtin = P(2 ** 31 - 1, CL, 10 ** 6)
     assert builtin["kernel"] == "ClassicalS<u64acc,u32,HYBRID>"
     assert builtin["block"] == (2 ** 64 - 1) // ((2 ** 31 - 1) * (2 ** 31 - 2)) == 4
     builtin = builtin["kernel"]
-    assert P(4294967291, CL, 10 ** 6)["kernel"] == "dot_kernel<ClassicalU32<OVERFLOW>>"
+    assert P(4294967291, CL, 10 ** 6)["kernel"] == "ClassicalS<u64acc,u32,CARRY>"
+    assert P(4294967291, CL, 10 ** 6)["reductions_per_thread"] == 1
     gfp.tune_set([_entry(CL, U32, 0, 2 ** 31 - 1, 1 << 20, gfp.CARRY, 64),
                   _entry(CL, U32, 0, 65537, 1 << 20, gfp.BLOCKED, 64),
                   _entry(CL, U16, 0, 2897, 1 << 12, gfp.DELAYED, 32)])

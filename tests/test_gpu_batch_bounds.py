@@ -38,7 +38,7 @@ def cu(x):
 
 
 ROWS = 67
-LENS = [17, 255, 449, 511, 1000, 1023]  # all below 256 vectors of u16 / u32 / f64
+LENS = [17, 255, 449, 511, 512, 1000, 1023]  # all below 256 vectors of u16 / u32 / f64
 
 
 @pytest.mark.parametrize("p", [prev_prime(2 ** 29), prev_prime(2 ** 31), 3037000493, 4294967291])
@@ -139,3 +139,25 @@ def test_batch_argument_validation():
     with pytest.raises(ValueError):
         gfp.dot_batch(A.view(10, 10), x[:10], 65521, out=cu(np.zeros(10, np.uint32)))  # out dtype
     gfp.dot_batch(A.view(10, 10)[1:], x[:10], 65521)  # a view with a storage offset is fine
+
+
+@pytest.mark.parametrize("p,k", [(2887, 515), (2897, 512), (2903, 509)])
+@pytest.mark.parametrize("strategy", ["BLOCKED", "HYBRID", "OVERFLOW", "CARRY"])
+@pytest.mark.parametrize("lanes", [1, 8, 0])
+def test_f1_dim512_m32_at_the_2897_step(p, k, strategy, lanes):
+    """SURVEY 8(f) F1 / P:470-478: DIM = 512 dots with 32-bit accumulators.  With one accumulator per row
+    (lanes 1, the paper's loop) the block length k = floor((2^32 - 1 - (p-1)) / (p-1)^2) is 515 / 512 / 509 at
+    p = 2887 / 2897 / 2903: one final reduction per row up to 2897, two from 2903 -- and an all-(p-1) row of
+    512 terms (512 * 2902^2 > 2^32) is wrong unless that second reduction happens."""
+    strat = getattr(gfp, strategy)
+    if strategy == "BLOCKED":
+        assert gfp.plan(p, CL, 512, dtype=torch.uint16, strategy=strat, acc_bits=32)["block"] == k
+    rows, n = 1000, 512
+    A = synth.uniform(synth.BASE_SEED + 5, synth.STREAM_MAT, 0, rows * n, p, np.uint16)
+    A[: 64 * n] = p - 1  # worst-case rows first
+    x = synth.uniform(synth.BASE_SEED + 5, synth.STREAM_X, 0, n, p, np.uint16)
+    x[:] = np.where(np.arange(n) % 3 == 0, x, p - 1)
+    for xx in (x, np.full(n, p - 1, np.uint16)):
+        want = oracle.dot_batch_classical(p, A.reshape(rows, n), xx)
+        got = gfp.dot_batch_ex(cu(A).view(rows, n), cu(xx), p, CL, strategy=strat, acc_bits=32, lanes_per_row=lanes)
+        assert np.array_equal(got.cpu().numpy().astype(np.uint64), want), (p, strategy, lanes)

@@ -76,7 +76,7 @@ def test_classical_c1_config():
 
 @pytest.mark.parametrize("p", [4294967291, 3037000493, 2 ** 31 - 1, 65537])
 def test_classical_u32_large_primes_overflow_path(p):
-    """k is tiny here, so the kernel takes the sec. 3.3 overflow-detection path (CORR on wrap)."""
+    """k is tiny here, so the kernel takes a sec. 3.3 path (the Eq. (2) hybrid, or the carry word)."""
     info = gfp.query(p, CL, torch.uint32)
     for n in [1, 3, 4, 5, 17, 1000, 100003, 2 ** 21 + 5]:
         a, b = residues(p, n, 0, np.uint32, SEED + 7), residues(p, n, 1, np.uint32, SEED + 7)
@@ -84,16 +84,30 @@ def test_classical_u32_large_primes_overflow_path(p):
     w = np.full(3 * 10 ** 6 + 1, p - 1, np.uint32)  # every add wraps the u64 when (p-1)^2 ~ 2^64
     assert result_int(gfp.dot(cu(w), cu(w), p, CL)) == (3 * 10 ** 6 + 1) % p
     assert info["k"] >= 1
-    # the built-in plan: Eq. (2) hybrid while lambda = floor((2^64-1)/(p(p-1))) >= 4, else a test per product
+    # the built-in plan: Eq. (2) hybrid while lambda = floor((2^64-1)/(p(p-1))) >= 4, else the carry word
     lam = (2 ** 64 - 1) // (p * (p - 1))
     pl = gfp.plan(p, CL, 3 * 10 ** 6 + 1, dtype=torch.uint32)
     if pl["strategy"] != gfp.AUTO and "ALL" not in pl["kernel"] and "THREAD" not in pl["kernel"]:
-        assert pl["strategy"] == (gfp.HYBRID if lam >= 4 else gfp.OVERFLOW), (p, pl)
+        assert pl["strategy"] == (gfp.HYBRID if lam >= 4 else gfp.CARRY), (p, pl)
     # worst-case batches through the same built-in choice (rows of 4096 overflow a lane's u64 sum)
     rows, n = 37, 4096
     W = np.full((rows, n), p - 1, np.uint32)
     got = gfp.dot_batch(cu(W), cu(W[0]), p, CL).cpu().to(torch.int64).numpy()
     assert (got == n % p).all(), (p, "batch worst case")
+
+
+def test_classical_u32_largest_prime_full_size():
+    """bench.py C3-p4294967291: n = 2^28 at p = 4294967291 through the built-in plan (the carry word: the
+    carry flag of every 64-bit add counted), against the oracle; and an all-(p-1) vector (closed form n mod p,
+    a carry on nearly every product)."""
+    p, n = 4294967291, 1 << 28
+    a = synth.uniform(SEED + 11, synth.STREAM_A, 0, n, p, np.uint32)
+    b = synth.uniform(SEED + 11, synth.STREAM_B, 0, n, p, np.uint32)
+    assert result_int(gfp.dot(cu(a), cu(b), p, CL)) == oracle.dot_classical(p, a, b)
+    w = cu(np.full(n, p - 1, np.uint32))
+    assert result_int(gfp.dot(w, w, p, CL)) == n % p
+    for strat in (gfp.CARRY, gfp.OVERFLOW):
+        assert result_int(gfp.dot_ex(w, w, p, CL, strategy=strat)) == n % p
 
 
 def test_misaligned_and_ragged():
