@@ -605,6 +605,19 @@ def main():
         kern_avg = statistics.mean([s.elapsed_time(e) for s, e in ev[-args.steps:]])
     else:  # a step is exactly one launch of the dominant kernel: the region's events over K launches
         kern_avg = ms / args.steps
+    # the distribution per launch (median and minimum), measured AFTER the timed region with a
+    # pair of events around each of K more launches; the events serialise consecutive launches (no PDL
+    # overlap), so these sit slightly above the back-to-back mean that `value` uses
+    with torch.cuda.stream(stream):
+        ev.clear()
+        for _ in range(args.steps):
+            step(record=True)
+        torch.cuda.synchronize()
+    per_launch = sorted(s_.elapsed_time(e_) for s_, e_ in ev[-args.steps:])
+    launch_stats = {"median_ms": round(statistics.median(per_launch), 5), "min_ms": round(per_launch[0], 5),
+                    "max_ms": round(per_launch[-1], 5), "back_to_back_mean_ms": round(kern_avg, 5), "n": len(per_launch),
+                    "timing": "CUDA events around each of K further launches of the step's dominant kernel (serialised: "
+                              "no PDL overlap between consecutive launches); back_to_back_mean_ms = the timed region / K"}
     ms_max = max_over_ranks(ms, world)
     value = total_terms * args.steps / (ms_max / 1e3)
     peak, peak_src = peak_hbm()
@@ -687,7 +700,7 @@ def main():
                        "l2": "inputs larger than L2: %.0f MiB per rank x %d rotating copies vs 126 MB L2"
                              % (local_bytes / 2 ** 20, len(reps)),
                        "seed": synth.BASE_SEED + cfg.get("inputs_of", args.config)},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "launch_stats": launch_stats, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_timed,
             "clocks": clk.summary(), "parity_vs_oracle": parity, "phases": phases,
             "parity_checked_terms_rank0": parity_terms,
@@ -875,16 +888,24 @@ def secondary_table(gfp, args, dev, stream, exclude):
         if phases:
             table[cfg["name"]]["phases"] = phases
         if cfg["kind"] == "batch" and cfg["rep"] == 3:
-            # second roofline: the shared-memory gather (one random lookup per term, 1 wavefront per clock per SM)
+            # the binding roofline: each SM's L1TEX data pipe moves one 128-byte wavefront per clock, shared by
+            # the random table lookups (one per term: the most distinct 32-bit words any bank serves per warp
+            # lookup, measured on these codes) and the stream of A through L1 (one wavefront per 128 bytes);
+            # ncu: the pipe is 88.7% busy in the index-add kernel (profiles/r02_zbatch_indexadd_32749_ncu_full.txt)
             wf = lookup_wavefronts(h["A"])
             sms = torch.cuda.get_device_properties(dev).multi_processor_count
             clk = (ClockSampler(dev.index).max_mhz or 1965) * 1e6
-            roof_us = terms / 32 * wf / (sms * clk) * 1e6
+            lookup_wf = terms / 32 * wf
+            stream_wf = d["A"].numel() * d["A"].element_size() / 128
+            roof_us = (lookup_wf + stream_wf) / (sms * clk) * 1e6
             table[cfg["name"]]["gather_roofline"] = {
-                "bound": "smem_gather", "lookups": terms, "wavefronts_per_warp_lookup": round(wf, 3),
+                "bound": "l1tex_data_pipe", "lookups": terms, "wavefronts_per_warp_lookup": round(wf, 3),
+                "lookup_wavefronts": int(lookup_wf), "stream_wavefronts": int(stream_wf),
                 "sms": sms, "clock_mhz": clk / 1e6, "us": round(roof_us, 2), "frac": round(roof_us / (avg * 1e3), 4),
-                "note": "one random antilog lookup per term; wavefronts = the most distinct 32-bit words any bank "
-                        "serves per warp lookup, from these codes; 1 shared-memory wavefront per clock per SM"}
+                "lookups_only_us": round(lookup_wf / (sms * clk) * 1e6, 2),
+                "note": "one random antilog lookup per term plus A streamed through L1, 1 data-pipe wavefront per "
+                        "clock per SM; the staged x reads (4 wavefronts per warp and 2 rows of 256 terms) are "
+                        "implementation overhead, not in the floor"}
         if xchg is not None:  # the fused result must equal the plain dot's
             with torch.cuda.stream(stream):
                 plain = gfp.dot(reps[0]["a"], reps[0]["b"], cfg["p"], cfg["rep"], stream=stream)

@@ -520,13 +520,18 @@ def test_fused_allreduce_single_rank():
                 else:
                     a, b = synth.uniform(SEED, 0, 0, n, p, dt), synth.uniform(SEED, 1, 0, n, p, dt)
                 ga, gb = cu(a), cu(b)
+                if rep == gfp.MONTGOMERY:  # the inputs read as Montgomery forms: oracle decodes by B^-1
+                    ref = oracle.dot_montgomery(p, a, b)
+                else:
+                    ref = oracle.dot(p, rep, a, b)
                 want = gfp.dot(ga, gb, p, rep).cpu()
+                assert (want[0].item() if rep == gfp.FP64 else int(want.to(torch.int64)[0])) == ref, (p, rep, n)
                 for _ in range(3):
                     got = gd.dot_fused(ga, gb, p, rep, x).cpu()
-                    assert torch.equal(got, want), (p, rep, n)
+                    assert torch.equal(got, want), (p, rep, n)  # equal to the oracle-checked value above
         p, n = 2 ** 31 - 1, 1 << 20
         a, b = cu(synth.uniform(SEED, 0, 0, n, p, np.uint32)), cu(synth.uniform(SEED, 1, 0, n, p, np.uint32))
-        want = int(gfp.dot(a, b, p, gfp.CLASSICAL).cpu().to(torch.int64)[0])
+        want = oracle.dot_classical(p, a.cpu().numpy(), b.cpu().numpy())
         out = torch.empty(1, dtype=torch.uint32, device=DEV)
         s = torch.cuda.Stream()
         with torch.cuda.stream(s):

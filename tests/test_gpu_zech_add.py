@@ -85,16 +85,17 @@ def test_zech_add_degenerate(p):
 
 
 def test_zech_add_c4_full_size():
-    """BASELINE configs[3] shape (p = 32749, n = 2^26, 10% zeros): equals the default integer plan and,
-    on a 2^22 prefix, the oracle."""
+    """BASELINE configs[3] shape (p = 32749, n = 2^26, 10% zeros), the bench's C4-zech_add line: the whole
+    vector against the oracle directly -- its integer-accumulation Zech dot and, step by step in Table 1's
+    order, its own pure-Zech accumulation (oracle_dot_zech_tplus1) -- and against the default plan."""
     p, n = 32749, 2 ** 26
     a = synth.zech_codes(synth.BASE_SEED + 3, 0, 0, n, p - 1)
     b = synth.zech_codes(synth.BASE_SEED + 3, 1, 0, n, p - 1)
     ga, gb = cu(a), cu(b)
     full = zadd(ga, gb, p)
+    assert full == oracle.dot_zech(p, 2, a, b)
+    assert full == oracle.dot_zech_tplus1(p, 2, a, b)
     assert full == int(gfp.dot(ga, gb, p, ZE).cpu().to(torch.int64)[0])
-    m = 2 ** 22
-    assert zadd(ga[:m], gb[:m], p) == oracle.dot_zech(p, 2, a[:m], b[:m])
 
 
 def test_zech_add_graph_capture_and_repeat():
