@@ -771,6 +771,12 @@ __global__ void __launch_bounds__(NT, MINB) batch_zech_kernel(const uint16_t *__
 // Row loads: with L >= 8 lanes per row a warp's 16-byte loads cover whole 128-byte lines (streamed past L1);
 // with one lane per row each lane walks its own row, so its loads may allocate in L1: the second half of a
 // 32-byte sector is then served from L1 instead of a second L2 request.
+// 32-byte load (LDG.E.256) of two consecutive 16-byte vectors (32-byte aligned): one lane walking its own row
+// fetches a whole sector per request
+__device__ __forceinline__ void ld_row256(const uint4 *ptr, uint4 &a, uint4 &b) {
+    asm("ld.global.nc.L1::no_allocate.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(ptr));
+}
 template <int LPR>
 __device__ __forceinline__ uint4 ld_row(const uint4 *ptr) {
     if constexpr (LPR == 1) {
@@ -827,10 +833,17 @@ __global__ void __launch_bounds__(NT) batch_kernel(const typename R::elem *__res
                 const uint4 *av = reinterpret_cast<const uint4 *>(Ar);
                 const uint4 *xv = XS ? xs : reinterpret_cast<const uint4 *>(x);
                 int64_t v0 = g;
+                // one lane per row: 32-byte loads when the row is 32-byte aligned (v0 advances by U vectors)
+                const bool wide = LPR == 1 && U % 2 == 0 && ((uintptr_t)av & 31) == 0;
                 for (; v0 + LPR * (U - 1) < nvec; v0 += LPR * U) {
                     uint4 ra[U];
+                    if (LPR == 1 && U % 2 == 0 && wide) {
 #pragma unroll
-                    for (int u = 0; u < U; ++u) ra[u] = ld_row<LPR>(av + v0 + u * LPR);
+                        for (int u = 0; u < U; u += 2) ld_row256(av + v0 + u, ra[u], ra[u + 1]);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) ra[u] = ld_row<LPR>(av + v0 + u * LPR);
+                    }
 #pragma unroll
                     for (int u = 0; u < U; ++u) R::vec(acc, ra[u], XS ? xv[v0 + u * LPR] : __ldg(xv + v0 + u * LPR), K, tab);
                 }
@@ -929,6 +942,13 @@ __device__ __forceinline__ TO conv1(TI v, const KParams &K, const uint16_t *tab)
 #endif
 #ifndef GFP_CONV_WAVES
 #define GFP_CONV_WAVES 1  // resident-grid conversions: grid = waves x the resident CTAs
+#endif
+#ifndef GFP_CONV_TAB_U
+#define GFP_CONV_TAB_U 4  // table (Zech) conversions: 8-element chunks per thread in flight
+#endif
+#ifndef GFP_CONV_TAB_NT
+#define GFP_CONV_TAB_NT 512  // table (Zech) conversions: threads per CTA (B200 A/B, scripts/ab_zconv.py: C4's two
+                              // operands from_zech / to_zech 95.0 / 94.1 us at 1024 threads x U = 2, 88.8 / 90.4 here)
 #endif
 #ifndef GFP_CONV_LD
 #define GFP_CONV_LD 1  // 0: ld.global.cs (streaming), 1: ld.global.L1::no_allocate (coherent: in == out is fine)
@@ -1830,7 +1850,7 @@ static cudaError_t launch_conv_t(const KParams &K, const void *in, void *out, in
     // table conversions (Zech): 1024-thread CTAs, so that the one or two CTAs whose 64 KB table fits an SM
     // still keep 2048 threads of loads in flight
     constexpr bool kTab = OP == C_TO_ZECH || OP == C_FROM_ZECH_SMALL || OP == C_FROM_ZECH_LARGE;
-    constexpr int NT = kTab ? 1024 : 256, U = GFP_CONV_U;
+    constexpr int NT = kTab ? GFP_CONV_TAB_NT : 256, U = kTab ? GFP_CONV_TAB_U : GFP_CONV_U;
     const size_t smem = table ? (size_t)entries * 2 : 0;
     auto kern = convert_kernel<OP, TI, TO, NT, U>;
     int bps = occupancy(kern, NT, smem);
