@@ -224,6 +224,27 @@ def host_inputs(cfg, rank, world, limit=None):
     return {"a": a, "b": b}
 
 
+def graph_ms(fn, stream, per_graph=5, replays=4):
+    """Milliseconds per call of fn() (device work on `stream`), timed as CUDA-graph replays of per_graph calls
+    with CUDA events on the stream (no host launch gaps between the calls)."""
+    with torch.cuda.stream(stream):
+        fn()
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(per_graph):
+                fn()
+        g.replay()
+        stream.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(replays):
+            g.replay()
+        e1.record(stream)
+        stream.synchronize()
+    return e0.elapsed_time(e1) / (per_graph * replays)
+
+
 def to_device(gfp, cfg, h, dev, stream):
     """Device tensors in the representation; Montgomery conversion timed here (phase a2)."""
     p, rep = cfg["p"], cfg["rep"]
@@ -240,18 +261,8 @@ def to_device(gfp, cfg, h, dev, stream):
                np.dtype(np.uint16): torch.uint16}[np.dtype(cfg["dtype"])] if rep == 1 else torch.float64
         am = torch.empty(a.numel(), dtype=tdt, device=a.device)
         bm = torch.empty(b.numel(), dtype=tdt, device=b.device)
-        with torch.cuda.stream(stream):
-            for _ in range(2):  # warm
-                gfp.to_rep(a, p, rep, out=am, stream=stream)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            iters = 5
-            e0.record(stream)
-            for _ in range(iters):
-                gfp.to_rep(a, p, rep, out=am, stream=stream)
-                gfp.to_rep(b, p, rep, out=bm, stream=stream)
-            e1.record(stream)
-        stream.synchronize()
-        ms = e0.elapsed_time(e1) / iters
+        ms = graph_ms(lambda: (gfp.to_rep(a, p, rep, out=am, stream=stream),
+                               gfp.to_rep(b, p, rep, out=bm, stream=stream)), stream)
         nbytes = 2 * a.numel() * (a.element_size() + am.element_size())  # read + write per element per operand
         if rep == 1:
             phases["to_montgomery"] = {"ms_per_pair": ms, "GB/s": nbytes / ms / 1e6,
@@ -272,25 +283,21 @@ def to_device(gfp, cfg, h, dev, stream):
             stream.synchronize()
             if not torch.equal(back, a):
                 raise RuntimeError("Zech conversion round trip changed the codes")
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-            iters = 5
-            ev[0].record(stream)
-            for _ in range(iters):
-                gfp.from_rep(a, p, rep, out=res, stream=stream)
-                gfp.from_rep(b, p, rep, out=back, stream=stream)
-            ev[1].record(stream)
-            for _ in range(iters):
-                gfp.to_rep(res, p, rep, out=back, stream=stream)
-                gfp.to_rep(res, p, rep, out=back, stream=stream)
-            ev[2].record(stream)
-        stream.synchronize()
+        res_b = torch.empty_like(b)
+        back_b = torch.empty_like(b)
+        ms_from = graph_ms(lambda: (gfp.from_rep(a, p, rep, out=res, stream=stream),
+                                    gfp.from_rep(b, p, rep, out=res_b, stream=stream)), stream)
+        ms_to = graph_ms(lambda: (gfp.to_rep(res, p, rep, out=back, stream=stream),
+                                  gfp.to_rep(res_b, p, rep, out=back_b, stream=stream)), stream)
+        if not (torch.equal(back, a) and torch.equal(back_b, b)):
+            raise RuntimeError("Zech conversion round trip changed the codes")
         nbytes = 2 * a.numel() * 2 * a.element_size()
-        for name, ms, what in [("from_zech", ev[0].elapsed_time(ev[1]) / iters, "code c -> g^c (antilog table)"),
-                               ("to_zech", ev[1].elapsed_time(ev[2]) / iters, "residue x -> log_g x (log table)")]:
+        for name, ms, what in [("from_zech", ms_from, "code c -> g^c (antilog table)"),
+                               ("to_zech", ms_to, "residue x -> log_g x (log table)")]:
             phases[name] = {"ms_per_pair": ms, "GB/s": nbytes / ms / 1e6,
                             "note": what + " for two operands of u16 (P:126-131), tables in shared memory; "
-                                    "excluded from the dot timing (P:313-320)"}
-        del res, back
+                                    "excluded from the dot timing (P:313-320); CUDA-graph replay"}
+        del res, back, res_b, back_b
     return {"a": a, "b": b}, phases
 
 
@@ -426,12 +433,21 @@ def cpu_model():
     return None
 
 
+def oracle_batch(p, rep, A, x):
+    """The oracle's rows of A . x: classical residues, or Zech codes (one oracle Zech dot per row)."""
+    import oracle
+    if rep == 3:
+        g = oracle.primitive_root(p)
+        return np.array([oracle.dot_zech(p, g, A[r], x) for r in range(A.shape[0])], dtype=np.uint64)
+    return oracle.dot_batch_classical(p, A, x)
+
+
 def oracle_slice(cfg, h, lo, hi):
     """The oracle, as it stands, on elements (rows for the batch) [lo, hi) of the sample."""
     import oracle
     p, rep = cfg["p"], cfg["rep"]
     if cfg["kind"] == "batch":
-        return oracle.dot_batch_classical(p, h["A"][lo:hi], h["x"])
+        return oracle_batch(p, rep, h["A"][lo:hi], h["x"])
     a, b = h["a"][lo:hi], h["b"][lo:hi]
     if rep == 0:
         return oracle.dot_classical(p, a, b)
@@ -475,7 +491,7 @@ def oracle_time(cfg, h, budget_s=10.0, full_ok=True):
         A, x = h["A"], h["x"]
 
         def run(rows):
-            return oracle.dot_batch_classical(p, A[:rows], x)
+            return oracle_batch(p, rep, A[:rows], x)
         t0 = time.perf_counter()
         run(64)
         per_row = (time.perf_counter() - t0) / 64

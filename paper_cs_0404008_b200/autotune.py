@@ -18,7 +18,8 @@ import paper_cs_0404008_b200 as gfp
 
 # primes: the paper's landmarks and the representation bounds (sec. 2), the switching points of sec. 3
 U16_PRIMES = [3, 257, 2897, 2903, 16381, 32749, 46337, 65521]
-U32_PRIMES = [65537, 1048573, 16777213, 268435399, 2 ** 31 - 1, 3037000493, 4294967291]
+# (65521 in u32 storage: configs[0]'s own case, a u16-size prime stored in 32-bit words)
+U32_PRIMES = [65521, 65537, 1048573, 16777213, 268435399, 2 ** 31 - 1, 3037000493, 4294967291]
 MONT_PRIMES = [40499, 65521, 2 ** 31 - 1, 2654435761]
 FP_PRIMES = [32749, 65521, 67108859, 94906249]
 ZECH_PRIMES = [32749, 65521]

@@ -3,8 +3,8 @@
 # The .ncu-rep files are summarised ON THE BOX (scripts/ncu_summary.py) and removed, so gpurun_out/ stays
 # under gpurun's 64 MiB copy-back limit; KEEP_REP="2" keeps the reports of the listed configs.
 mkdir -p gpurun_out
-TAG=${TAG:-r01}
-NAMES=(C1 C2 C3 C4 C5 C4-zech_add C2-centered)
+TAG=${TAG:-r02}
+NAMES=(C1 C2 C3 C4 C5 C4-zech_add C2-centered C1-fused1 C3-fused1 C5-zech32749 C5-zech65521 C3-p4294967291)
 export TRAFFIC_JSON=gpurun_out/${TAG}_traffic.json
 for C in ${CONFIGS:-0 1 3 4}; do
   CMD="python bench.py --config $C --steps 3 --warmup 3 --no-secondary --no-cpu --e2e-steps 0"

@@ -549,6 +549,43 @@ def test_fused_allreduce_single_rank():
         x.close()
 
 
+def test_fused_allreduce_pure_zech_plan():
+    """an install-time table entry may route an AUTO Zech dot to the pure-Zech kernel (F3); through
+    gfp_dot_allreduce that kernel must exchange the classical value of its sum and encode the group's sum --
+    never store a code through the 8-byte partial path."""
+    from paper_cs_0404008_b200 import dist as gd
+    p, n = 32749, 1_000_003
+    a, b = synth.zech_codes(SEED, 0, 0, n, p - 1), synth.zech_codes(SEED, 1, 0, n, p - 1)
+    want = oracle.dot_zech(p, 2, a, b)
+    gfp.tune_set([{"rep": ZE, "dtype": 0, "kind": 0, "strategy": gfp.ZECH_ADD, "acc_bits": 0, "p": p, "n": n,
+                   "rows": 0, "us_best": 1.0, "us_builtin": 2.0}])
+    x = gd.PeerExchange()
+    try:
+        assert "zech_add" in gfp.plan(p, ZE, n)["kernel"]
+        ga, gb = cu(a), cu(b)
+        for _ in range(3):
+            assert result_int(gd.dot_fused(ga, gb, p, ZE, x)) == want
+        part = gfp.dot_partial(ga, gb, p, ZE)
+        assert int(part.cpu()[0]) == oracle.zech_decode(p, 2, want)  # additive form: the classical value
+    finally:
+        torch.cuda.synchronize()
+        x.close()
+        gfp.tune_clear()
+
+
+def test_dist_dot_on_a_side_stream():
+    """dist.dot(stream=s) with s not the current stream orders partial -> combine -> finalize on s."""
+    from paper_cs_0404008_b200 import dist as gd
+    p, n = 2 ** 31 - 1, 1 << 22
+    a, b = synth.uniform(SEED, 0, 0, n, p, np.uint32), synth.uniform(SEED, 1, 0, n, p, np.uint32)
+    ga, gb = cu(a), cu(b)
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    out = gd.dot(ga, gb, p, CL, stream=s)
+    s.synchronize()
+    assert result_int(out) == oracle.dot_classical(p, a, b)
+
+
 def test_fused_allreduce_rejects_bad_groups():
     xs = gfp.GfpXchg()
     xs.rank, xs.world = 0, 0
