@@ -544,7 +544,11 @@ def main():
     ap.add_argument("--sweep", default=None, metavar="OUT.jsonl",
                     help="SURVEY 8(f) F1: paper-shaped prime sweep of DIM=512 batched dots per strategy, "
                          "written to OUT.jsonl (one GPU)")
-    ap.add_argument("--sweep-rows", type=int, default=1 << 19)
+    ap.add_argument("--sweep-rows", type=int, default=1 << 19,
+                    help="rows per cell (2^19 x 512 u16 = 512 MiB streams from HBM; 2^15 = 32 MiB stays in L2, the "
+                         "paper's cache-resident regime, where the kernels are bound by issue, not memory)")
+    ap.add_argument("--sweep-graph", type=int, default=4, help="calls per captured CUDA graph")
+    ap.add_argument("--sweep-reps", type=int, default=5, help="timed graph replays per cell (median reported)")
     ap.add_argument("--dry-run", action="store_true",
                     help="launcher check: set up the N ranks and their process group, print one JSON line with the "
                          "ranks that ran, no GPU work (CPU-testable with GFP_BENCH_PG_BACKEND=gloo)")
@@ -1007,18 +1011,20 @@ def prime_sweep(args):
                 ok = bool(torch.equal(o, ref))
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=stream):
-                    for _ in range(4):
+                    for _ in range(args.sweep_graph):
                         gfp.dot_batch_ex(A, x, p, gfp.CLASSICAL, strategy=strat, acc_bits=m, out=o, stream=stream,
                                          lanes_per_row=lanes)
                 g.replay()
+                g.replay()
                 stream.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                for _ in range(5):
+                evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.sweep_reps + 1)]
+                evs[0].record(stream)
+                for r_ in range(args.sweep_reps):
                     g.replay()
-                e1.record(stream)
+                    evs[r_ + 1].record(stream)
                 stream.synchronize()
-            us = e0.elapsed_time(e1) * 1e3 / 20
+            per_call = sorted(evs[r_].elapsed_time(evs[r_ + 1]) * 1e3 / args.sweep_graph for r_ in range(args.sweep_reps))
+            us = statistics.median(per_call)
             blk = pl["block"] if pl["block"] else None
             # lanes the batch kernel gives a DIM = 512 row: the caller's choice, else 8 (n / W < 256 vectors)
             L = lanes if lanes else 8
@@ -1027,7 +1033,8 @@ def prime_sweep(args):
                     "reductions_per_dim512_sequential": (None if not blk else -(-n // blk)) if name != "auto" else 1,
                     "terms_per_lane": tpl,
                     "reductions_per_lane": (None if not blk else -(-tpl // blk)),
-                    "us": us, "terms_per_s": rows * n / (us / 1e6), "GB/s": nbytes / (us / 1e6) / 1e9,
+                    "us": us, "us_min": per_call[0], "us_max": per_call[-1], "rows": rows,
+                    "terms_per_s": rows * n / (us / 1e6), "GB/s": nbytes / (us / 1e6) / 1e9,
                     "frac_of_measured_hbm": nbytes / (us / 1e6) / 1e9 / peak, "equal_to_default": ok}
             cells.append(cell)
             out.write(json.dumps(cell) + "\n")

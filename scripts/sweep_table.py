@@ -30,21 +30,40 @@ for p in sorted(by):
     print(str(p).rjust(11), *row, str(b.get("block_k", "")).rjust(11), str(b1.get("reductions_per_lane", "")).rjust(10),
           str(b.get("reductions_per_lane", "")).rjust(10))
 
-# cost of one reduction per row (one lane): time per row = t0 + c * reductions, least squares over the primes
-pts = [(c["reductions_per_lane"], c["us"]) for c in cells if c["strategy"] == "blocked32_1lane" and c["reductions_per_lane"]]
-if len(pts) > 3:
+# cost of one reduction per accumulator, least squares over the primes: time per launch = t0 + c * reductions;
+# and the two steps side by side -- the paper's (one lane, 2897 -> 2903) and the 8-lane kernel's (8191 -> 8209)
+def fit(strategy):
+    pts = [(c["reductions_per_lane"], c["us"]) for c in cells if c["strategy"] == strategy and c["reductions_per_lane"]]
+    if len(pts) < 4:
+        return None
     r = np.array([x for x, _ in pts], float)
     t = np.array([y for _, y in pts], float)
-    A = np.stack([np.ones_like(r), r], 1)
-    (t0, cost), *_ = np.linalg.lstsq(A, t, rcond=None)
-    one = t[r == 1]
-    print("\n# one-lane blocked32: time per launch = %.2f us + %.3f us x (reductions per row)   [least squares, %d primes]"
-          % (t0, cost, len(pts)))
-    if len(one) > 1:
-        print("# spread of the launches with ONE reduction per row (p <= 2897): %.2f .. %.2f us (sd %.3f us)"
-              % (one.min(), one.max(), one.std()))
-    print("# predicted step 2897 -> 2903 (1 -> 2 reductions per row): +%.3f us = %.2f%% of %.2f us" % (cost, 100 * cost / t0, t0))
-    for p in (2887, 2897, 2903):
-        c = by.get(p, {}).get("blocked32_1lane")
-        if c:
-            print("#   p = %d: %.3f us, %d reduction(s) per row" % (p, c["us"], c["reductions_per_lane"]))
+    (t0, cost), *_ = np.linalg.lstsq(np.stack([np.ones_like(r), r], 1), t, rcond=None)
+    return t0, cost, len(pts)
+
+
+def step(strategy, lo, hi):
+    a, b = by.get(lo, {}).get(strategy), by.get(hi, {}).get(strategy)
+    if not (a and b):
+        return
+    d = b["us"] - a["us"]
+    sep = b.get("us_min", b["us"]) > a.get("us_max", a["us"])
+    print("#   %s %d -> %d: reductions per accumulator %s -> %s; median %.3f -> %.3f us (%+.2f%%); replay ranges "
+          "[%.3f, %.3f] / [%.3f, %.3f]%s" % (strategy, lo, hi, a["reductions_per_lane"], b["reductions_per_lane"],
+                                             a["us"], b["us"], 100 * d / a["us"], a.get("us_min", a["us"]),
+                                             a.get("us_max", a["us"]), b.get("us_min", b["us"]), b.get("us_max", b["us"]),
+                                             " -- separated" if sep else " -- overlapping"))
+
+
+print()
+for strat in ("blocked32_1lane", "blocked32"):
+    f = fit(strat)
+    if f:
+        t0, cost, k = f
+        print("# %s: time per launch = %.3f us + %.4f us x (reductions per accumulator)   [least squares, %d primes]"
+              % (strat, t0, cost, k))
+step("blocked32_1lane", 2887, 2897)
+step("blocked32_1lane", 2897, 2903)
+step("hybrid32_1lane", 2897, 2903)
+step("blocked32", 2897, 2903)
+step("blocked32", 8191, 8209)
