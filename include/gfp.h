@@ -298,9 +298,11 @@ gfp_status gfp_dot_host_partial(uint64_t p, gfp_rep rep, gfp_dtype dt, const voi
  * ZECH_ADD) on synthetic canonical inputs generated on the device, checks that every candidate returns
  * the same field element(s) (GFP_E_CUDA with a message otherwise: an exactness failure), and records
  * the fastest in the library's tuning table (one entry per case; a re-tuned case replaces its entry).
- * Each candidate is timed with CUDA events over about ms_per_candidate milliseconds (at least 3 calls,
- * after 2 warm-up calls), rotating through enough input sets that >= 3x the L2 is streamed between two
- * uses of a set (at most 64 sets / 1 GiB).  Device memory is allocated and freed inside the call.
+ * Each candidate is timed with CUDA events over about ms_per_candidate milliseconds of replays of a CUDA
+ * graph that holds 8-64 calls (after 2 warm-up calls; device time per call, as the bench measures, not the
+ * host's launch rate), rotating through enough input sets that >= 3x the L2 is streamed between two uses
+ * of a set (at most 64 sets / 1 GiB).  The calls run on a private stream after `stream` has drained.
+ * Device memory is allocated and freed inside the call.
  *
  * GFP_STRAT_AUTO (gfp_dot, gfp_dot_batch, gfp_dot_partial, gfp_dot_ex / _batch_ex / gfp_plan with a NULL
  * or all-zero gfp_options) then follows the table: among the entries with the call's (rep, dtype, kind)
