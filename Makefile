@@ -56,3 +56,6 @@ variant:
 tune: scripts/tune_zech
 scripts/tune_zech: scripts/tune_zech.cu $(CSRC)/device.cuh $(CSRC)/params.h
 	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -I$(CSRC) -Iinclude -o $@ $<
+tune: scripts/gather_peak
+scripts/gather_peak: scripts/gather_peak.cu
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -o $@ $<

@@ -129,6 +129,16 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def gather_peak():
+    """Achievable L1TEX data-pipe wavefronts per SM per clock with the A stream (profiles/gather_peak.json,
+    measured by scripts/gather_peak.cu), else the nominal 1."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "gather_peak.json")) as f:
+            return float(json.load(f)["lookups_plus_stream"]), "measured (profiles/gather_peak.json, scripts/gather_peak.cu)"
+    except Exception:
+        return 1.0, "nominal (1 wavefront per clock per SM)"
+
+
 def traffic_lookup(cfg_name, world):
     """dram bytes (read+write) per launch of the dominant kernel, from a committed ncu --set full capture."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -917,11 +927,15 @@ def secondary_table(gfp, args, dev, stream, exclude):
             clk = (ClockSampler(dev.index).max_mhz or 1965) * 1e6
             lookup_wf = terms / 32 * wf
             stream_wf = d["A"].numel() * d["A"].element_size() / 128
-            roof_us = (lookup_wf + stream_wf) / (sms * clk) * 1e6
+            peak_wf, peak_src = gather_peak()
+            floor_us = (lookup_wf + stream_wf) / (sms * clk) * 1e6  # at the nominal 1 wavefront per clock
+            roof_us = floor_us / peak_wf  # at the measured achievable rate
             table[cfg["name"]]["gather_roofline"] = {
                 "bound": "l1tex_data_pipe", "lookups": terms, "wavefronts_per_warp_lookup": round(wf, 3),
                 "lookup_wavefronts": int(lookup_wf), "stream_wavefronts": int(stream_wf),
-                "sms": sms, "clock_mhz": clk / 1e6, "us": round(roof_us, 2), "frac": round(roof_us / (avg * 1e3), 4),
+                "sms": sms, "clock_mhz": clk / 1e6, "peak_wavefronts_per_clock": peak_wf, "peak_source": peak_src,
+                "us": round(roof_us, 2), "frac": round(roof_us / (avg * 1e3), 4),
+                "nominal_us": round(floor_us, 2), "frac_of_nominal": round(floor_us / (avg * 1e3), 4),
                 "lookups_only_us": round(lookup_wf / (sms * clk) * 1e6, 2),
                 "note": "one random antilog lookup per term plus A streamed through L1, 1 data-pipe wavefront per "
                         "clock per SM; the staged x reads (4 wavefronts per warp and 2 rows of 256 terms) are "
