@@ -504,6 +504,27 @@ def test_batch_many_rows_closed_form():
     assert bool((out.to(torch.int32) == n % p).all())
 
 
+def test_batch_beyond_2_32_elements_closed_form():
+    """A matrix of more than 2^32 elements (8 GiB of u16): the 64-bit row offsets of the C5 fast path and of the
+    Zech matrix-vector kernel, with a padded leading dimension; every row of all-(p-1) (the code of -1) dots
+    to n mod p, and a row of zeros placed last dots to 0."""
+    rows, n, lda = (1 << 20) + 5, 4096, 4104
+    p = 65521
+    A = _full(rows * lda, p - 1, torch.uint16)
+    A.view(torch.int16).view(rows, lda)[-1].zero_()
+    x = _full(n, p - 1, torch.uint16)
+    out = gfp.dot_batch(A, x, p, CL, rows=rows, n=n, lda=lda).to(torch.int32)
+    assert bool((out[:-1] == n % p).all()) and int(out[-1]) == 0
+    p = 32749
+    A.view(torch.int16).fill_((p - 1) // 2)  # code of -1 (P:139-140)
+    A.view(torch.int16).view(rows, lda)[-1].zero_()
+    x = _full(n, (p - 1) // 2, torch.uint16)
+    out = gfp.dot_batch(A, x, p, ZE, rows=rows, n=n, lda=lda).to(torch.int32)
+    assert bool((out[:-1] == oracle.zech_encode(p, 2, n % p)).all()) and int(out[-1]) == 0
+    del A
+    torch.cuda.empty_cache()
+
+
 # ------------------------------------------------------------------------------ fused combine (world 1)
 def test_fused_allreduce_single_rank():
     """gfp_dot_allreduce on a one-rank group (the only group one GPU can host): the whole exchange protocol
