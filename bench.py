@@ -616,9 +616,35 @@ def main():
     total_terms = cfg["rows"] * cfg["n"] if cfg["kind"] == "batch" else cfg["n"]
     reps = replicas(d, local_bytes)
     xchg = None
+    combine_note = None
     if cfg["kind"] == "dot" and ((world > 1 and args.combine == "fused") or cfg.get("fused1")):
         from paper_cs_0404008_b200 import dist as gfp_dist
-        xchg = gfp_dist.PeerExchange(group)
+        # the exchange buffers need CUDA IPC between the ranks' processes and peer access between their GPUs;
+        # if any rank cannot set them up, every rank falls back to the NCCL combine (decided collectively)
+        err = None
+        try:
+            xchg = gfp_dist.PeerExchange(group)
+            if world > 1:  # one fused dot on a tiny input before the timed region: the group works end to end
+                t = torch.ones(1024, dtype=reps[0]["a"].dtype, device=dev)
+                gfp_dist.dot_fused(t, t, cfg["p"], cfg["rep"], xchg, stream=stream)
+                torch.cuda.synchronize()
+        except Exception as e:  # noqa: BLE001 -- reported in the line, never silently
+            err = f"{type(e).__name__}: {e}"
+        if world > 1:
+            flags = [None] * world
+            dist.all_gather_object(flags, err)
+            bad = [f for f in flags if f]
+            if bad:
+                if xchg is not None:
+                    try:
+                        xchg.close()
+                    except Exception:  # noqa: BLE001
+                        pass
+                xchg = None
+                combine_note = "fused combine unavailable, NCCL combine used: " + bad[0][:200]
+                print(f"bench.py: {combine_note}", file=sys.stderr, flush=True)
+        elif err:
+            raise RuntimeError(err)
     step, ev, out = make_step(gfp, cfg, reps, world, group, stream, xchg)
 
     with torch.cuda.stream(stream):
@@ -734,7 +760,7 @@ def main():
             "gpu_launches": launches_timed,
             "clocks": clk.summary(), "parity_vs_oracle": parity, "phases": phases,
             "parity_checked_terms_rank0": parity_terms,
-            "combine_equals_nccl_path": combine_check,
+            "combine_equals_nccl_path": combine_check, "combine_note": combine_note,
             "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
