@@ -31,11 +31,19 @@ oracle/liboracle.so: oracle/oracle.c
 oracle-ubsan: oracle/oracle.c
 	$(CC) -O1 -g -fsanitize=undefined,address -fno-omit-frame-pointer -fPIC -shared -o oracle/liboracle_san.so $<
 
-$(LIBGFP): $(GFP_SRCS) $(GFP_HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(GFP_SRCS) -lcudart 2> $(PKG)/build.log || (cat $(PKG)/build.log; exit 1)
+# one object per translation unit (make -j builds them in parallel); ptxas -v reports go to build/gfp/*.log and
+# are concatenated into $(PKG)/build.log
+GFP_OBJS  := $(patsubst $(CSRC)/%,build/gfp/%.o,$(GFP_SRCS))
+build/gfp/%.o: $(CSRC)/% $(GFP_HDRS)
+	@mkdir -p build/gfp
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/gfp/$*.log || (cat build/gfp/$*.log; exit 1)
+
+$(LIBGFP): $(GFP_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(GFP_OBJS) -lcudart
+	cat build/gfp/*.log > $(PKG)/build.log
 
 clean:
-	rm -f synth/libsynth.so oracle/liboracle.so oracle/liboracle_san.so $(LIBGFP)
+	rm -rf synth/libsynth.so oracle/liboracle.so oracle/liboracle_san.so $(LIBGFP) build/gfp
 
 # tuning harness (not the product): standalone executable timed on the GPU box
 tune: scripts/tune_dot

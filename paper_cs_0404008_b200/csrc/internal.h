@@ -1,4 +1,4 @@
-// internal.h -- interface between the C ABI (api.cpp) and the kernel launchers (kernels.cu).
+// internal.h -- interface between the C ABI (api.cpp) and the kernel launchers (kernels_*.cu).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -39,7 +39,7 @@ constexpr int kMaxGrid = 4096;
 
 // Kernel variant selected on the host from the bounds.
 struct DotPlan {
-    int policy;     // enumerated in kernels.cu
+    int policy;     // enumerated in kernels_common.cuh
     int grid, block;
     size_t smem;
     int64_t head;   // scalar elements before the first 16-byte aligned vector (== n if unaligned)

@@ -1,6 +1,6 @@
 """Host-side checks of the fused multi-GPU combine (gfp_dot_allreduce; SURVEY 8(e) fused variant).
 
-1. A model of the device protocol (xchg_allreduce in kernels.cu, step for step): R ranks as threads with
+1. A model of the device protocol (xchg_allreduce in kernels_common.cuh, step for step): R ranks as threads with
    random delays between every step run many epochs on shared "exchange buffers"; every rank must obtain
    the exact sum of all ranks' partials at every epoch.  This exercises the two-slot (epoch parity)
    argument of gfp.h: a rank can only overwrite epoch e's slots after every rank has read them.
