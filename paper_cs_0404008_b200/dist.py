@@ -131,6 +131,8 @@ def dot(a_shard: torch.Tensor, b_shard: torch.Tensor, p: int, rep: int, group=No
     stream, so NCCL orders itself after the partial kernel and the finalize kernel after the reduction."""
     if stream is None:
         stream = torch.cuda.current_stream(a_shard.device)
+    elif not isinstance(stream, torch.cuda.Stream):  # a raw cudaStream_t handle
+        stream = torch.cuda.ExternalStream(int(stream), device=a_shard.device)
     with torch.cuda.stream(stream):
         partial = _dot_partial(a_shard, b_shard, p, rep, stream=stream)
         combine_partials(partial, group)
