@@ -517,11 +517,12 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
             // B200 A/B (scripts/ab_zbatch.py, GF(32749) / GF(65521)): three 512-thread CTAs at 40 registers
             // (U = 2) 152.7 / - us, RP = 1 137.8 / 138.1, RP = 4 (U = 1) 148.7 / 149.1, this 130.7 (65521);
             // a register ping-pong pipeline over (row, chunk) spilled and ran 173-190 us
-            auto kern = batch_zech_kernel<1024, GFP_ZDEC_U, 1, GFP_ZDEC_RP>;
-            const int bps = occupancy(kern, 1024, smem);
-            const int64_t rpb = 32 * GFP_ZDEC_RP;  // rows per CTA per sweep (a warp per RP rows)
+            constexpr int ZNT = GFP_ZDEC_NT;
+            auto kern = batch_zech_kernel<ZNT, GFP_ZDEC_U, 1, GFP_ZDEC_RP>;
+            const int bps = occupancy(kern, ZNT, smem);
+            const int64_t rpb = ZNT / 32 * GFP_ZDEC_RP;  // rows per CTA per sweep (a warp per RP rows)
             const int64_t grid = std::min<int64_t>((rows + rpb - 1) / rpb, (int64_t)num_sms(dev) * bps);
-            cudaError_t le = launch_pdl(kern, dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(1024), smem, s,
+            cudaError_t le = launch_pdl(kern, dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(ZNT), smem, s,
                                         (const uint16_t *)A, lda, (const uint16_t *)x, rows, n, K, O, entries);
             count_launch();
             *err = le != cudaSuccess ? le : cudaGetLastError();

@@ -193,6 +193,9 @@ __device__ __forceinline__ void pdl_exit() {
 #ifndef GFP_ZDEC_RP
 #define GFP_ZDEC_RP 2  // rows a warp of the decode batch walks at once (each staged x read serves RP rows)
 #endif
+#ifndef GFP_ZDEC_NT
+#define GFP_ZDEC_NT 1024  // threads per CTA of the decode batch (one CTA per SM)
+#endif
 #ifndef GFP_ZDEC_U
 #define GFP_ZDEC_U 4  // 16-byte A vectors per row and lane in flight in the decode batch
 #endif
