@@ -548,8 +548,9 @@ def main():
     ap.add_argument("--no-secondary", action="store_true", help="skip the per-config kernel table")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--combine", default="fused", choices=["fused", "nccl"],
-                    help="N > 1 single dots: one fused kernel per rank (peer-memory exchange) or partial + NCCL")
+    ap.add_argument("--combine", default="fused", choices=["fused", "nvls", "nccl"],
+                    help="N > 1 single dots: one fused kernel per rank (peer stores over NVLink; nvls: multimem "
+                         "reductions in the NVSwitch) or partial + NCCL all_reduce + finalize")
     ap.add_argument("--oracle-budget", type=float, default=12.0, help="seconds of oracle work per sample")
     ap.add_argument("--sweep", default=None, metavar="OUT.jsonl",
                     help="SURVEY 8(f) F1: paper-shaped prime sweep of DIM=512 batched dots per strategy, "
@@ -617,13 +618,17 @@ def main():
     reps = replicas(d, local_bytes)
     xchg = None
     combine_note = None
-    if cfg["kind"] == "dot" and ((world > 1 and args.combine == "fused") or cfg.get("fused1")):
+    if cfg["kind"] == "dot" and ((world > 1 and args.combine in ("fused", "nvls")) or cfg.get("fused1")):
         from paper_cs_0404008_b200 import dist as gfp_dist
-        # the exchange buffers need CUDA IPC between the ranks' processes and peer access between their GPUs;
-        # if any rank cannot set them up, every rank falls back to the NCCL combine (decided collectively)
+        # the exchange buffers need CUDA IPC between the ranks' processes and peer access between their GPUs
+        # (nvls: a multicast team); if any rank cannot set them up, every rank falls back to the NCCL combine
+        # (decided collectively)
         err = None
         try:
-            xchg = gfp_dist.PeerExchange(group)
+            if args.combine == "nvls" and world > 1:
+                xchg = gfp_dist.MulticastExchange(group)
+            else:
+                xchg = gfp_dist.PeerExchange(group)
             if world > 1:  # one fused dot on a tiny input before the timed region: the group works end to end
                 t = torch.ones(1024, dtype=reps[0]["a"].dtype, device=dev)
                 gfp_dist.dot_fused(t, t, cfg["p"], cfg["rep"], xchg, stream=stream)
@@ -750,8 +755,10 @@ def main():
             "vs_baseline": None, "dtype": DTYPE_NAMES[np.dtype(cfg["dtype"])], "data": "synthetic",
             "config": {"workload": cfg["workload"], "p": cfg["p"], "representation": REP_NAMES[cfg["rep"]],
                        "n_total": total_terms, "terms_per_rank": local_terms,
-                       "parallelism": f"shard x{world}" + ((" + fused peer-memory combine (1 launch)" if xchg is not None
-                                                            else " + NCCL all_reduce(int64)")
+                       "parallelism": f"shard x{world}" + (((" + fused NVLS multicast combine (1 launch)"
+                                                              if args.combine == "nvls" else
+                                                              " + fused peer-memory combine (1 launch)")
+                                                             if xchg is not None else " + NCCL all_reduce(int64)")
                                                            if world > 1 and cfg["kind"] == "dot" else ""),
                        "l2": "inputs larger than L2: %.0f MiB per rank x %d rotating copies vs 126 MB L2"
                              % (local_bytes / 2 ** 20, len(reps)),

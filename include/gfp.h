@@ -259,6 +259,36 @@ gfp_status gfp_xchg_destroy(void *buf);     /* free a gfp_xchg_create buffer (af
 gfp_status gfp_dot_allreduce(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
                              const gfp_xchg *x, void *out, void *stream);
 
+/* ---- The fused multi-GPU dot through an NVLink SHARP (NVLS) multicast buffer (SURVEY 8(e) "fused variant":
+ * multimem.red into a multicast buffer, then a counter barrier, then finalize -- one launch per rank, no NCCL;
+ * the reduction happens in the NVSwitch).  Same result and calling contract as gfp_dot_allreduce.
+ *
+ * Setup, once per process group (every call on the rank's current device):
+ *   rank 0:      gfp_mc_create(world, &mc, &fd, &bytes) -- a multicast object for `world` devices and a POSIX
+ *                file descriptor for it (owned by mc); the caller passes fd (e.g. SCM_RIGHTS over a Unix
+ *                socket) and bytes to every other rank;
+ *   other ranks: gfp_mc_import(fd_received, bytes, world, &mc);
+ *   every rank:  gfp_mc_add_device(mc); then, after EVERY rank has added its device (a group barrier),
+ *                gfp_mc_bind(mc) -- backs the object with this device's memory, maps it twice (multicast and
+ *                unicast) and zeroes this rank's copy; then a group barrier before the first dot.
+ *   teardown:    gfp_mc_destroy(mc) on every rank after the last dot (unbinds, unmaps, releases, closes fd).
+ * GFP_E_UNSUPPORTED where the device or driver has no multicast (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED).
+ *
+ * Protocol (the kernel's last CTA, one thread): epoch e = this rank's counter + 1, parity e mod 2; add the
+ * partial residue (additive form, < 2^32) to the parity's running sum on every rank's copy (multimem.red.add),
+ * then, with release semantics, one arrival to the parity's counter; poll this rank's copy of the counter
+ * (acquire) until it reaches world x (uses of the parity so far); the group sum is the running total minus its
+ * value at the parity's previous use (u64 wrap-around arithmetic, exact); reduce mod p and encode.  A missing
+ * peer traps after ~30 s instead of hanging. */
+typedef struct gfp_mc gfp_mc;  /* opaque: a multicast object, this rank's backing memory and its two mappings */
+gfp_status gfp_mc_create(int32_t world, gfp_mc **mc, int32_t *fd, uint64_t *bytes);  /* fd, bytes may be NULL */
+gfp_status gfp_mc_import(int32_t fd, uint64_t bytes, int32_t world, gfp_mc **mc);
+gfp_status gfp_mc_add_device(gfp_mc *mc);
+gfp_status gfp_mc_bind(gfp_mc *mc);
+gfp_status gfp_mc_destroy(gfp_mc *mc);
+gfp_status gfp_dot_allreduce_mc(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
+                                gfp_mc *mc, void *out, void *stream);
+
 /* gfp_dot / gfp_dot_batch with explicit options (NULL = defaults): the paper's strategies side by
  * side, exact in every admissible combination.  Same pointers, streams and errors as gfp_dot. */
 gfp_status gfp_dot_ex(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,

@@ -105,6 +105,12 @@ _SIGS = {
     "gfp_xchg_close": [_vp],
     "gfp_xchg_destroy": [_vp],
     "gfp_dot_allreduce": [_u64, _int, _int, _vp, _vp, _i64, ctypes.POINTER(GfpXchg), _vp, _vp],
+    "gfp_mc_create": [ctypes.c_int32, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_u64)],
+    "gfp_mc_import": [ctypes.c_int32, _u64, ctypes.c_int32, ctypes.POINTER(_vp)],
+    "gfp_mc_add_device": [_vp],
+    "gfp_mc_bind": [_vp],
+    "gfp_mc_destroy": [_vp],
+    "gfp_dot_allreduce_mc": [_u64, _int, _int, _vp, _vp, _i64, _vp, _vp, _vp],
 }
 for _name, _args in _SIGS.items():
     getattr(lib, _name).argtypes = _args
@@ -475,4 +481,45 @@ def dot_allreduce(a: torch.Tensor, b: torch.Tensor, p: int, rep: int, xchg: GfpX
     with torch.cuda.device(a.device):
         _check(lib.gfp_dot_allreduce(p, rep, _dt(a, rep), a.data_ptr(), b.data_ptr(), a.numel(), ctypes.byref(xchg),
                                      out.data_ptr(), _stream(a, stream)))
+    return out
+
+
+# ------------------------------------------------------------------------------ NVLS multicast combine
+def mc_create(world: int) -> tuple[int, int, int]:
+    """Rank 0: a multicast object for `world` devices -> (handle, POSIX fd to pass to the other ranks, bytes)."""
+    h, fd, nbytes = ctypes.c_void_p(), ctypes.c_int32(-1), ctypes.c_uint64(0)
+    _check(lib.gfp_mc_create(world, ctypes.byref(h), ctypes.byref(fd), ctypes.byref(nbytes)))
+    return int(h.value), int(fd.value), int(nbytes.value)
+
+
+def mc_import(fd: int, nbytes: int, world: int) -> int:
+    h = ctypes.c_void_p()
+    _check(lib.gfp_mc_import(fd, nbytes, world, ctypes.byref(h)))
+    return int(h.value)
+
+
+def mc_add_device(h: int) -> None:
+    _check(lib.gfp_mc_add_device(h))
+
+
+def mc_bind(h: int) -> None:
+    _check(lib.gfp_mc_bind(h))
+
+
+def mc_destroy(h: int) -> None:
+    _check(lib.gfp_mc_destroy(h))
+
+
+def dot_allreduce_mc(a: torch.Tensor, b: torch.Tensor, p: int, rep: int, mc: int, out: torch.Tensor | None = None,
+                     stream=None) -> torch.Tensor:
+    """gfp_dot_allreduce through an NVLS multicast buffer (gfp_dot_allreduce_mc): one launch per rank, the
+    partials reduced in the NVSwitch."""
+    a, b = _flat_cuda(a, "a"), _flat_cuda(b, "b")
+    if a.numel() != b.numel() or a.dtype != b.dtype:
+        raise ValueError("a and b must have the same length and dtype")
+    if out is None:
+        out = torch.empty(1, dtype=a.dtype, device=a.device)
+    with torch.cuda.device(a.device):
+        _check(lib.gfp_dot_allreduce_mc(p, rep, _dt(a, rep), a.data_ptr(), b.data_ptr(), a.numel(), mc,
+                                        out.data_ptr(), _stream(a, stream)))
     return out

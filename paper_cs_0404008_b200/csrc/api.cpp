@@ -1,6 +1,8 @@
 // api.cpp -- the C ABI of include/gfp.h: argument validation, per-(device, p, rep) constant and
 // table caches, per-(device, stream) workspaces, and the host-buffer pipeline of gfp_dot_host.
+#include <cuda.h>  // driver-API types only (multicast / VMM calls go through cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <cstdio>
 #include <cstring>
@@ -8,6 +10,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "gfp.h"
@@ -195,8 +198,10 @@ gfp_status plan_fail(gfp_status st) {
 }
 
 gfp_status dot_common(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n, void *out,
-                      int mode, cudaStream_t s, const gfp_options *opt = nullptr, uint64_t *xchg = nullptr) {
-    gfp_status st = check_dot_args(dt, a, b, n, out, (mode == OUT_ENCODE || mode == OUT_XCHG) ? dtype_size(dt) : 8);
+                      int mode, cudaStream_t s, const gfp_options *opt = nullptr, uint64_t *xchg = nullptr,
+                      uint64_t *mc = nullptr) {
+    gfp_status st = check_dot_args(dt, a, b, n, out,
+                                   (mode == OUT_ENCODE || mode == OUT_XCHG || mode == OUT_MC) ? dtype_size(dt) : 8);
     if (st != GFP_OK) return st;
     Ctx *c;
     if ((st = get_ctx(p, rep, dt, &c)) != GFP_OK) return st;
@@ -204,7 +209,7 @@ gfp_status dot_common(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, cons
     if ((st = get_ws(s, &ws)) != GFP_OK) return st;
     DotPlan plan;
     if ((st = plan_dot(c->info, c->K, a, b, n, opt, &plan)) != GFP_OK) return plan_fail(st);
-    OutSpec o{out, (int)rep, (int)dt, mode, xchg};
+    OutSpec o{out, (int)rep, (int)dt, mode, xchg, 0, mc};
     cudaError_t e = launch_dot(plan, c->K, a, b, n, ws, o, s);
     return e == cudaSuccess ? GFP_OK : cuda_fail(e, "dot launch");
 }
@@ -320,6 +325,231 @@ gfp_status gfp_dot_allreduce(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *
         }
     }
     return dot_common(p, rep, dt, a, b, n, out, OUT_XCHG, (cudaStream_t)stream, nullptr, own);
+}
+
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------ NVLS multicast exchange
+// Driver-API calls (multicast objects, virtual memory management) through cudaGetDriverEntryPoint: libgfp.so does
+// not link libcuda, so it still loads on hosts without a GPU driver (the CPU tests).
+namespace {
+struct McApi {
+    CUresult (*mcGetGranularity)(size_t *, const CUmulticastObjectProp *, CUmulticastGranularity_flags) = nullptr;
+    CUresult (*mcCreate)(CUmemGenericAllocationHandle *, const CUmulticastObjectProp *) = nullptr;
+    CUresult (*mcAddDevice)(CUmemGenericAllocationHandle, CUdevice) = nullptr;
+    CUresult (*mcBindMem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                          unsigned long long) = nullptr;
+    CUresult (*mcUnbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t) = nullptr;
+    CUresult (*memCreate)(CUmemGenericAllocationHandle *, size_t, const CUmemAllocationProp *, unsigned long long) = nullptr;
+    CUresult (*memRelease)(CUmemGenericAllocationHandle) = nullptr;
+    CUresult (*addrReserve)(CUdeviceptr *, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+    CUresult (*addrFree)(CUdeviceptr, size_t) = nullptr;
+    CUresult (*memMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+    CUresult (*memUnmap)(CUdeviceptr, size_t) = nullptr;
+    CUresult (*memSetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc *, size_t) = nullptr;
+    CUresult (*exportHandle)(void *, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long) = nullptr;
+    CUresult (*importHandle)(CUmemGenericAllocationHandle *, void *, CUmemAllocationHandleType) = nullptr;
+    CUresult (*deviceGet)(CUdevice *, int) = nullptr;
+    CUresult (*deviceGetAttribute)(int *, CUdevice_attribute, CUdevice) = nullptr;
+    bool ok = false;
+};
+
+const McApi *mc_api(std::string *why) {
+    static McApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        bool all = true;
+        auto get = [&](const char *name, auto &fn) {
+            void *f = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+                f == nullptr)
+                all = false;
+            fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(f);
+        };
+        get("cuMulticastGetGranularity", api.mcGetGranularity);
+        get("cuMulticastCreate", api.mcCreate);
+        get("cuMulticastAddDevice", api.mcAddDevice);
+        get("cuMulticastBindMem", api.mcBindMem);
+        get("cuMulticastUnbind", api.mcUnbind);
+        get("cuMemCreate", api.memCreate);
+        get("cuMemRelease", api.memRelease);
+        get("cuMemAddressReserve", api.addrReserve);
+        get("cuMemAddressFree", api.addrFree);
+        get("cuMemMap", api.memMap);
+        get("cuMemUnmap", api.memUnmap);
+        get("cuMemSetAccess", api.memSetAccess);
+        get("cuMemExportToShareableHandle", api.exportHandle);
+        get("cuMemImportFromShareableHandle", api.importHandle);
+        get("cuDeviceGet", api.deviceGet);
+        get("cuDeviceGetAttribute", api.deviceGetAttribute);
+        api.ok = all;
+    });
+    if (!api.ok && why) *why = "the CUDA driver does not provide the multicast / VMM entry points";
+    return api.ok ? &api : nullptr;
+}
+
+gfp_status cu_fail(CUresult r, const char *where) {
+    t_err = std::string(where) + ": CUDA driver error " + std::to_string((int)r);
+    return GFP_E_CUDA;
+}
+}  // namespace
+
+struct gfp_mc {
+    CUmemGenericAllocationHandle mc = 0, mem = 0;
+    CUdeviceptr mc_va = 0, uc_va = 0;
+    size_t size = 0;
+    int world = 0, fd = -1, dev = -1;
+    bool added = false, bound = false;
+};
+
+extern "C" {
+
+gfp_status gfp_mc_create(int32_t world, gfp_mc **mc, int32_t *fd, uint64_t *bytes) {
+    if (mc == nullptr || world < 1 || world > GFP_XCHG_MAX_WORLD)
+        return fail(GFP_E_INVAL, "gfp_mc_create: need mc and 1 <= world <= 16");
+    std::string why;
+    const McApi *A = mc_api(&why);
+    if (!A) return fail(GFP_E_UNSUPPORTED, why);
+    int dev = 0;
+    cudaError_t ce = cudaGetDevice(&dev);
+    if (ce != cudaSuccess) return cuda_fail(ce, "gfp_mc_create");
+    CUdevice cd;
+    CUresult r = A->deviceGet(&cd, dev);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuDeviceGet");
+    int supported = 0;
+    r = A->deviceGetAttribute(&supported, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cd);
+    if (r != CUDA_SUCCESS || !supported) return fail(GFP_E_UNSUPPORTED, "gfp_mc_create: multicast (NVLS) not supported here");
+    CUmulticastObjectProp prop;
+    memset(&prop, 0, sizeof prop);
+    prop.numDevices = (unsigned)world;
+    prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    prop.size = kMcWords * sizeof(uint64_t);
+    size_t gran = 0;
+    if ((r = A->mcGetGranularity(&gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED)) != CUDA_SUCCESS)
+        return cu_fail(r, "cuMulticastGetGranularity");
+    prop.size = (prop.size + gran - 1) / gran * gran;
+    gfp_mc *m = new gfp_mc();
+    m->size = prop.size;
+    m->world = world;
+    if ((r = A->mcCreate(&m->mc, &prop)) != CUDA_SUCCESS) {
+        delete m;
+        // the properties are valid by construction (size a multiple of the granularity): a refusal means this
+        // platform (driver, fabric manager, visible devices) offers no multicast team
+        if (r == CUDA_ERROR_INVALID_VALUE || r == CUDA_ERROR_NOT_SUPPORTED || r == CUDA_ERROR_NOT_PERMITTED)
+            return fail(GFP_E_UNSUPPORTED, "gfp_mc_create: the driver refused a multicast object (CUDA driver error " +
+                                               std::to_string((int)r) + "): no NVLS multicast team on this platform");
+        return cu_fail(r, "cuMulticastCreate");
+    }
+    if (fd != nullptr) {
+        int h = -1;
+        if ((r = A->exportHandle(&h, m->mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0)) != CUDA_SUCCESS) {
+            A->memRelease(m->mc);
+            delete m;
+            return cu_fail(r, "cuMemExportToShareableHandle");
+        }
+        *fd = h;
+        m->fd = h;
+    }
+    if (bytes) *bytes = m->size;
+    *mc = m;
+    return GFP_OK;
+}
+
+gfp_status gfp_mc_import(int32_t fd, uint64_t bytes, int32_t world, gfp_mc **mc) {
+    if (mc == nullptr || fd < 0 || bytes == 0 || world < 1 || world > GFP_XCHG_MAX_WORLD)
+        return fail(GFP_E_INVAL, "gfp_mc_import: need mc, fd >= 0, bytes > 0, 1 <= world <= 16");
+    std::string why;
+    const McApi *A = mc_api(&why);
+    if (!A) return fail(GFP_E_UNSUPPORTED, why);
+    gfp_mc *m = new gfp_mc();
+    m->size = bytes;
+    m->world = world;
+    CUresult r = A->importHandle(&m->mc, (void *)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+    if (r != CUDA_SUCCESS) {
+        delete m;
+        return cu_fail(r, "cuMemImportFromShareableHandle");
+    }
+    *mc = m;
+    return GFP_OK;
+}
+
+gfp_status gfp_mc_add_device(gfp_mc *m) {
+    if (m == nullptr || m->added) return fail(GFP_E_INVAL, "gfp_mc_add_device: NULL or already added");
+    const McApi *A = mc_api(nullptr);
+    int dev = 0;
+    cudaError_t ce = cudaGetDevice(&dev);
+    if (ce != cudaSuccess) return cuda_fail(ce, "gfp_mc_add_device");
+    CUdevice cd;
+    CUresult r = A->deviceGet(&cd, dev);
+    if (r == CUDA_SUCCESS) r = A->mcAddDevice(m->mc, cd);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuMulticastAddDevice");
+    m->dev = dev;
+    m->added = true;
+    return GFP_OK;
+}
+
+gfp_status gfp_mc_bind(gfp_mc *m) {
+    if (m == nullptr || !m->added || m->bound) return fail(GFP_E_INVAL, "gfp_mc_bind: NULL, not added, or bound");
+    const McApi *A = mc_api(nullptr);
+    CUdevice cd;
+    CUresult r = A->deviceGet(&cd, m->dev);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuDeviceGet");
+    CUmemAllocationProp prop;
+    memset(&prop, 0, sizeof prop);
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = m->dev;
+    CUmemAccessDesc acc;
+    memset(&acc, 0, sizeof acc);
+    acc.location = prop.location;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    if ((r = A->memCreate(&m->mem, m->size, &prop, 0)) != CUDA_SUCCESS) return cu_fail(r, "cuMemCreate");
+    if ((r = A->mcBindMem(m->mc, 0, m->mem, 0, m->size, 0)) != CUDA_SUCCESS) return cu_fail(r, "cuMulticastBindMem");
+    if ((r = A->addrReserve(&m->mc_va, m->size, m->size, 0, 0)) != CUDA_SUCCESS ||
+        (r = A->memMap(m->mc_va, m->size, 0, m->mc, 0)) != CUDA_SUCCESS ||
+        (r = A->memSetAccess(m->mc_va, m->size, &acc, 1)) != CUDA_SUCCESS)
+        return cu_fail(r, "multicast mapping");
+    if ((r = A->addrReserve(&m->uc_va, m->size, m->size, 0, 0)) != CUDA_SUCCESS ||
+        (r = A->memMap(m->uc_va, m->size, 0, m->mem, 0)) != CUDA_SUCCESS ||
+        (r = A->memSetAccess(m->uc_va, m->size, &acc, 1)) != CUDA_SUCCESS)
+        return cu_fail(r, "unicast mapping");
+    m->bound = true;
+    // zero this rank's copy, then record the group size in its private words (the caller synchronises the
+    // group -- e.g. a barrier -- before any rank's first gfp_dot_allreduce_mc)
+    std::vector<uint64_t> init(kMcWords, 0);
+    init[1] = (uint64_t)m->world;
+    cudaError_t ce = cudaMemset((void *)m->uc_va, 0, m->size);
+    if (ce == cudaSuccess) ce = cudaMemcpy((void *)m->uc_va, init.data(), init.size() * 8, cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
+    return ce == cudaSuccess ? GFP_OK : cuda_fail(ce, "gfp_mc_bind: init");
+}
+
+gfp_status gfp_mc_destroy(gfp_mc *m) {
+    if (m == nullptr) return fail(GFP_E_INVAL, "gfp_mc_destroy: NULL");
+    const McApi *A = mc_api(nullptr);
+    cudaDeviceSynchronize();
+    if (m->bound) {
+        A->memUnmap(m->mc_va, m->size);
+        A->addrFree(m->mc_va, m->size);
+        A->memUnmap(m->uc_va, m->size);
+        A->addrFree(m->uc_va, m->size);
+        CUdevice cd;
+        if (A->deviceGet(&cd, m->dev) == CUDA_SUCCESS) A->mcUnbind(m->mc, cd, 0, m->size);
+    }
+    if (m->mem) A->memRelease(m->mem);
+    if (m->mc) A->memRelease(m->mc);
+    if (m->fd >= 0) close(m->fd);
+    delete m;
+    return GFP_OK;
+}
+
+gfp_status gfp_dot_allreduce_mc(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
+                                gfp_mc *m, void *out, void *stream) {
+    if (m == nullptr || !m->bound) return fail(GFP_E_INVAL, "gfp_dot_allreduce_mc: multicast buffer not bound");
+    return dot_common(p, rep, dt, a, b, n, out, OUT_MC, (cudaStream_t)stream, nullptr, (uint64_t *)m->uc_va,
+                      (uint64_t *)m->mc_va);
 }
 
 gfp_status gfp_finalize(uint64_t p, gfp_rep rep, gfp_dtype dt, const uint64_t *summed, void *out, void *stream) {

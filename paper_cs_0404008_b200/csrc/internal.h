@@ -17,14 +17,22 @@ struct Workspace {
 };
 
 // Where the final residue goes.  OUT_XCHG: exchange with the group's peers first (fused multi-GPU
-// combine, gfp_dot_allreduce), then encode like OUT_ENCODE.
-enum OutMode { OUT_ENCODE = 0, OUT_PARTIAL = 1, OUT_ACCUMULATE = 2, OUT_XCHG = 3 };
+// combine over peer stores, gfp_dot_allreduce), then encode like OUT_ENCODE.  OUT_MC: the same through an
+// NVLink SHARP (NVLS) multicast buffer (multimem reductions in the switch, gfp_dot_allreduce_mc).
+enum OutMode { OUT_ENCODE = 0, OUT_PARTIAL = 1, OUT_ACCUMULATE = 2, OUT_XCHG = 3, OUT_MC = 4 };
 struct OutSpec {
-    void *out;          // OUT_ENCODE / OUT_XCHG: element of (rep, dtype); else uint64_t*
+    void *out;          // OUT_ENCODE / OUT_XCHG / OUT_MC: element of (rep, dtype); else uint64_t*
     int rep, dtype, mode;
-    uint64_t *xchg;     // OUT_XCHG: this rank's exchange buffer (it holds rank, world and the peer table)
+    uint64_t *xchg;     // OUT_XCHG: this rank's exchange buffer (rank, world, peer table); OUT_MC: this rank's
+                        // unicast mapping of the multicast buffer
     int prefetch;       // set by the launcher: prefetch the first chunk into L2 before griddepcontrol.wait
+    uint64_t *mc;       // OUT_MC: the multicast mapping of the same buffer (multimem.red targets)
 };
+// Multicast-buffer layout (u64 words; gfp_dot_allreduce_mc).  Private to each rank (unicast, never a multimem
+// target): [0] epoch, [1] world, [2 + par] uses of each slot parity, [4 + par] the slot's total at its last
+// use.  Reduced by every rank through the multicast mapping, in their own 128-byte lines: the partial sums
+// [kMcSum + par] and the arrival counts [kMcCnt + par].
+constexpr int kMcSum = 32, kMcCnt = 48, kMcWords = 64;
 // Packed combine: the CTA residues (< p < 2^32) are summed in bits [0, kPackShift), the CTA arrival
 // count in bits [kPackShift, 64): exact for grids below 2^(64 - kPackShift) CTAs.
 constexpr int kPackShift = 48;

@@ -116,6 +116,40 @@ __device__ __forceinline__ uint64_t xchg_allreduce(uint64_t r, uint64_t *own, ui
     return mod_p(sum, p, mu);
 }
 
+// gfp_dot_allreduce_mc (gfp.h protocol): the fused combine through an NVLS multicast buffer.  ONE thread of the
+// last CTA adds this rank's partial residue r (< 2^32) to the parity slot's running sum on every rank at once
+// (multimem.red: the switch applies it to each member's copy), then -- release -- one arrival to the slot's
+// counter; it polls its own copy of the counter (acquire) until world x (uses of this parity) arrivals are in,
+// and this epoch's group sum is the slot's running total minus its total at the parity's previous use
+// (wrapping u64 arithmetic: exact).  A rank can only add to parity e mod 2 at epoch e + 2 after every rank
+// arrived at epoch e + 1, i.e. after every rank read epoch e's total: two parities suffice.  A missing peer
+// traps after ~30 s instead of hanging.
+__device__ __forceinline__ uint64_t mc_allreduce(uint64_t r, uint64_t *uc, uint64_t *mc, uint64_t p, uint64_t mu) {
+    const uint64_t e = uc[0] + 1;  // only this rank's kernels touch its private words, in stream order
+    const int par = (int)(e & 1);
+    const uint64_t world = uc[1], uses = uc[2 + par] + 1;
+    asm volatile("multimem.red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(mc + kMcSum + par), "l"(r) : "memory");
+    asm volatile("multimem.red.release.sys.global.add.u64 [%0], %1;" ::"l"(mc + kMcCnt + par), "l"(1ull) : "memory");
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        uint64_t c;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(c) : "l"(uc + kMcCnt + par) : "memory");
+        if (c >= world * uses) break;
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 30000000000ull) __trap();  // a peer never arrived: fail loudly, do not hang
+        __nanosleep(32);
+    }
+    uint64_t total;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(total) : "l"(uc + kMcSum + par) : "memory");
+    const uint64_t sum = total - uc[4 + par];  // this epoch's sum of world residues < 2^36
+    uc[4 + par] = total;
+    uc[2 + par] = uses;
+    uc[0] = e;
+    return mod_p(sum, p, mu);
+}
+
 // Stage a u16 table (entries padded to a multiple of 8) from global into shared memory.
 __device__ __forceinline__ void stage_table(uint16_t *dst, const uint16_t *src, uint32_t entries) {
     const uint4 *s = reinterpret_cast<const uint4 *>(src);

@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
         if ((old >> kPackShift) == gridDim.x - 1) {
             uint64_t r = mod_p((old & ((1ull << kPackShift) - 1)) + c, K.p, K.mu);
             if (O.mode == OUT_XCHG) r = xchg_allreduce(r, O.xchg, K.p, K.mu);  // fused multi-GPU combine
+            else if (O.mode == OUT_MC) r = mc_allreduce(r, O.xchg, O.mc, K.p, K.mu);  // the same over NVLS
             write_result(r, O, K, 0);
             *word = 0;  // self-reset for the next launch on this stream
         }
@@ -362,6 +363,7 @@ __global__ void __launch_bounds__(NT) zech_add_dot_kernel(const uint16_t *__rest
             // fused multi-GPU combine: exchange the classical value with the peers, then encode the sum
             // (write_result: log table) -- the group's sum of Zech elements is not a sum of codes
             if (O.mode == OUT_XCHG) r = xchg_allreduce(r, O.xchg, K.p, K.mu);
+            else if (O.mode == OUT_MC) r = mc_allreduce(r, O.xchg, O.mc, K.p, K.mu);
             write_result(r, O, K, 0);
         }
         *ws.counter = 0;

@@ -116,10 +116,117 @@ class PeerExchange:
             self.own = None
 
 
-def dot_fused(a_shard: torch.Tensor, b_shard: torch.Tensor, p: int, rep: int, xchg: PeerExchange,
+class _LibMc:
+    """The library's multicast calls (the default backend of MulticastExchange)."""
+
+    @staticmethod
+    def create(world):
+        from . import mc_create
+        return mc_create(world)
+
+    @staticmethod
+    def import_(fd, nbytes, world):
+        from . import mc_import
+        return mc_import(fd, nbytes, world)
+
+    @staticmethod
+    def add_device(h):
+        from . import mc_add_device
+        mc_add_device(h)
+
+    @staticmethod
+    def bind(h):
+        from . import mc_bind
+        mc_bind(h)
+
+    @staticmethod
+    def destroy(h):
+        from . import mc_destroy
+        mc_destroy(h)
+
+
+def _pass_fd(fd, group, rank, world, tag):
+    """Rank 0's file descriptor to every other rank of the group (SCM_RIGHTS over a Unix socket whose path is
+    broadcast with the process group); returns the descriptor as received here (rank 0: its own)."""
+    import os
+    import socket
+    import tempfile
+    path = [None]
+    if rank == 0:
+        path[0] = os.path.join(tempfile.gettempdir(), f"gfp_mc_{os.getpid()}_{tag}.sock")
+        if os.path.exists(path[0]):
+            os.unlink(path[0])
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(path[0])
+        srv.listen(world)
+    dist.broadcast_object_list(path, src=0, group=group)
+    if rank == 0:
+        try:
+            for _ in range(world - 1):
+                conn, _ = srv.accept()
+                with conn:
+                    socket.send_fds(conn, [b"f"], [fd])
+                    conn.recv(1)  # the peer holds its copy of the descriptor
+        finally:
+            srv.close()
+            os.unlink(path[0])
+        return fd
+    cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    cli.connect(path[0])
+    with cli:
+        _, fds, _, _ = socket.recv_fds(cli, 1, 1)
+        cli.sendall(b"k")
+    return fds[0]
+
+
+class MulticastExchange:
+    """The NVLS multicast buffer of a process group for dot_fused_mc (include/gfp.h, gfp_mc_*): rank 0 creates
+    the multicast object and passes its descriptor to the others, every rank adds its device, then -- after a
+    group barrier -- backs and maps it; `handle` is what the kernel launch needs.  `backend` provides create,
+    import_, add_device, bind, destroy (injectable for tests)."""
+
+    def __init__(self, group=None, backend=None):
+        self.backend = backend or _LibMc
+        init = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if init else 1
+        self.rank = dist.get_rank(group) if init else 0
+        self.group = group
+        info = [None, None]
+        if self.rank == 0:
+            self.handle, fd, nbytes = self.backend.create(self.world)
+            info = [fd, nbytes]
+        if self.world > 1:
+            dist.broadcast_object_list(info, src=0, group=group)  # (rank 0's fd number is meaningless elsewhere)
+            fd = _pass_fd(info[0] if self.rank == 0 else None, group, self.rank, self.world, tag=id(self))
+            if self.rank != 0:
+                import os
+                try:
+                    self.handle = self.backend.import_(fd, info[1], self.world)
+                finally:
+                    os.close(fd)  # the imported handle does not need the descriptor
+        self.backend.add_device(self.handle)
+        if self.world > 1:
+            dist.barrier(group=group)  # every device added before any rank binds memory
+        self.backend.bind(self.handle)
+        if self.world > 1:
+            dist.barrier(group=group)  # every copy zeroed before any rank's first reduction
+
+    def close(self):
+        if self.world > 1:
+            dist.barrier(group=self.group)
+        if self.handle is not None:
+            self.backend.destroy(self.handle)
+            self.handle = None
+
+
+def dot_fused(a_shard: torch.Tensor, b_shard: torch.Tensor, p: int, rep: int, xchg,
               out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Exact dot of the globally sharded vectors in ONE kernel launch per rank (compute + exchange +
-    finalize); every rank receives the result (device, 1 element)."""
+    finalize); every rank receives the result (device, 1 element).  `xchg` is a PeerExchange (peer stores
+    over NVLink) or a MulticastExchange (NVLS multimem reductions in the switch)."""
+    if isinstance(xchg, MulticastExchange):
+        from . import dot_allreduce_mc
+        return dot_allreduce_mc(a_shard, b_shard, p, rep, xchg.handle, out=out, stream=stream)
     return _dot_allreduce(a_shard, b_shard, p, rep, xchg.spec, out=out, stream=stream)
 
 

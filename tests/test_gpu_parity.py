@@ -570,6 +570,63 @@ def test_fused_allreduce_single_rank():
         x.close()
 
 
+def _mc_unsupported():
+    """None when a multicast object can be created here, else the library's reason."""
+    try:
+        h = gfp.mc_create(1)[0]
+    except gfp.GfpError as e:
+        if e.status != 4:  # only GFP_E_UNSUPPORTED (no multicast team on this platform) is a skip
+            raise
+        return str(e)
+    gfp.mc_destroy(h)
+    return None
+
+
+def test_fused_allreduce_nvls_single_rank():
+    """gfp_dot_allreduce_mc (NVLS multicast: multimem.red into the switch, counter barrier, finalize) on a one-rank
+    group -- the only group one GPU can host: multimem reductions and the acquire polling run for real through the
+    multicast mapping; repeated epochs exercise both slot parities and the running-total bookkeeping, CUDA-graph
+    replays reuse the device-resident state; every representation against the oracle."""
+    from paper_cs_0404008_b200 import dist as gd
+    why = _mc_unsupported()
+    if why:
+        pytest.skip(why)
+    x = gd.MulticastExchange()
+    try:
+        for p, rep, dt, gen in [(65521, gfp.CLASSICAL, np.uint32, "u"), (2 ** 31 - 1, gfp.MONTGOMERY, np.uint32, "u"),
+                                (67108859, gfp.FP64, np.float64, "u"), (32749, gfp.ZECH, np.uint16, "z"),
+                                (4294967291, gfp.CLASSICAL, np.uint32, "u")]:
+            for n in [0, 1, 1000, 1_000_003]:
+                if gen == "z":
+                    a, b = synth.zech_codes(SEED, 0, 0, n, p - 1), synth.zech_codes(SEED, 1, 0, n, p - 1)
+                else:
+                    a, b = synth.uniform(SEED, 0, 0, n, p, dt), synth.uniform(SEED, 1, 0, n, p, dt)
+                want = oracle.dot_montgomery(p, a, b) if rep == gfp.MONTGOMERY else oracle.dot(p, rep, a, b)
+                ga, gb = cu(a), cu(b)
+                for _ in range(3):  # odd number of epochs per case: the parities alternate across cases
+                    assert result_int(gd.dot_fused(ga, gb, p, rep, x)) == want, (p, rep, n)
+        p, n = 2 ** 31 - 1, 1 << 20
+        a, b = synth.uniform(SEED, 0, 0, n, p, np.uint32), synth.uniform(SEED, 1, 0, n, p, np.uint32)
+        want = oracle.dot_classical(p, a, b)
+        ga, gb = cu(a), cu(b)
+        out = torch.empty(1, dtype=torch.uint32, device=DEV)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            gd.dot_fused(ga, gb, p, gfp.CLASSICAL, x, out=out, stream=s)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(3):
+                    gd.dot_fused(ga, gb, p, gfp.CLASSICAL, x, out=out, stream=s)
+        for _ in range(7):
+            out.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert int(out.cpu().to(torch.int64)[0]) == want
+    finally:
+        torch.cuda.synchronize()
+        x.close()
+
+
 def test_fused_allreduce_pure_zech_plan():
     """an install-time table entry may route an AUTO Zech dot to the pure-Zech kernel (F3); through
     gfp_dot_allreduce that kernel must exchange the classical value of its sum and encode the group's sum --
