@@ -14,6 +14,8 @@ pytestmark = pytest.mark.gpu
 
 gfp = pytest.importorskip("paper_cs_0404008_b200")
 DEV = "cuda:0"
+# GFP_FUZZ_SEED shifts every draw (default 0: the committed, reproducible draws); e.g. GFP_FUZZ_SEED=7 for a fresh set
+SHIFT = int(__import__("os").environ.get("GFP_FUZZ_SEED", "0")) * 1_000_003
 
 PRIMES = {
     ("classical", np.uint16): [2, 3, 5, 251, 257, 4093, 32749, 40009, 65521],
@@ -70,7 +72,7 @@ def _draw_n(rng):
 
 @pytest.mark.parametrize("block", range(6))
 def test_random_dots_at_random_offsets(block):
-    rng = np.random.default_rng(20260 + block)
+    rng = np.random.default_rng(20260 + block + SHIFT)
     keys = list(PRIMES)
     for case in range(120):
         kind, np_dt = keys[rng.integers(len(keys))]
@@ -101,7 +103,7 @@ def test_random_dots_at_random_offsets(block):
 
 @pytest.mark.parametrize("block", range(3))
 def test_random_batches_with_padded_rows(block):
-    rng = np.random.default_rng(4242 + block)
+    rng = np.random.default_rng(4242 + block + SHIFT)
     kinds = [("classical", np.uint16), ("classical", np.uint32), ("montgomery", np.uint32), ("fp64", np.float64),
              ("zech", np.uint16), ("centered", np.int32)]
     for case in range(25):
@@ -117,3 +119,31 @@ def test_random_batches_with_padded_rows(block):
         got = got.numpy() if got.dtype == torch.float64 else got.to(torch.int64).numpy()
         for r in rng.choice(rows, size=min(rows, 12), replace=False):  # sampled rows, each against the oracle
             assert got[r] == _want(kind, p, A[r, :n], x), (kind, np_dt, p, rows, n, lda, int(r))
+
+
+@pytest.mark.parametrize("block", range(3))
+def test_random_batches_explicit_strategies_and_lanes(block):
+    """gfp_dot_batch_ex with random sec.-3 strategies, accumulator widths and lanes per row (1 / 8 / 32 / the
+    library's choice) over classical u16 / u32 rows of random length and padding, against the oracle."""
+    rng = np.random.default_rng(777 + block + SHIFT)
+    for case in range(30):
+        np_dt = np.uint16 if rng.random() < 0.5 else np.uint32
+        p = int(rng.choice(PRIMES[("classical", np_dt)]))
+        rows, n = int(rng.integers(1, 700)), int(rng.integers(1, 2500))
+        lda = n + int(rng.integers(0, 9))
+        seed = synth.BASE_SEED + 9000 + 100 * block + case
+        A = _inputs("classical", np_dt, p, rows * lda, seed, 2).reshape(rows, lda)
+        if rng.random() < 0.3:
+            A[:] = p - 1  # worst-case magnitudes
+        x = _inputs("classical", np_dt, p, n, seed, 3)
+        strat = int(rng.choice([gfp.AUTO, gfp.DELAYED, gfp.BLOCKED, gfp.OVERFLOW, gfp.HYBRID, gfp.CARRY]))
+        m = int(rng.choice([0, 32, 64])) if strat != gfp.AUTO else 0
+        lanes = int(rng.choice([0, 1, 8, 32]))
+        try:
+            got = gfp.dot_batch_ex(torch.from_numpy(A).to(DEV)[:, :n], torch.from_numpy(x).to(DEV), p, gfp.CLASSICAL,
+                                   strategy=strat, acc_bits=m, lanes_per_row=lanes).cpu().to(torch.int64).numpy()
+        except gfp.GfpError as e:
+            assert e.status in (3, 4), (p, n, strat, m, lanes)  # bound / unsupported for this (p, n, m)
+            continue
+        want = oracle.dot_batch_classical(p, A[:, :n].copy(), x).astype(np.int64)
+        assert np.array_equal(got, want), (np_dt, p, rows, n, lda, strat, m, lanes)
