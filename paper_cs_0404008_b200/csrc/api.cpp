@@ -723,6 +723,8 @@ static gfp_status dot_host_common(uint64_t p, gfp_rep rep, gfp_dtype dt, const v
         e = partial_only ? cudaMemcpyAsync(out, S->d_partial, 8, cudaMemcpyDeviceToHost, s)
                          : cudaMemcpyAsync(out, S->d_out, es, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    // the chunks' residues were summed on the device: one remainder makes the partial a residue in [0, p)
+    if (e == cudaSuccess && partial_only) *(uint64_t *)out %= p;
     return e == cudaSuccess ? GFP_OK : cuda_fail(e, "gfp_dot_host");
 }
 

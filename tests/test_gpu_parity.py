@@ -434,6 +434,13 @@ def test_dot_host_end_to_end(rep, p):
     assert gfp.dot_host(ta, tb, p, rep) == want
     assert gfp.dot_host(torch.from_numpy(a[:1000]), torch.from_numpy(b[:1000]), p, rep) == \
         gfp.dot(cu(a[:1000]), cu(b[:1000]), p, rep).cpu().to(torch.float64 if rep == FP else torch.int64)[0].item()
+    # the multi-GPU end-to-end form (bench.py's N > 1 e2e leg): three host shards -> additive-form partials
+    # (gfp_dot_host_partial: for Zech the classical value, never a code) -> sum -> gfp_finalize
+    cuts = [0, n // 3, n // 3 + 17, n]
+    parts = [gfp.dot_host_partial(ta[lo:hi], tb[lo:hi], p, rep) for lo, hi in zip(cuts[:-1], cuts[1:])]
+    assert all(0 <= v < p for v in parts)
+    summed = torch.tensor([sum(parts)], dtype=torch.int64, device=DEV)
+    assert result_int(gfp.finalize(summed, p, rep, ta.dtype)) == want
 
 
 def test_stream_and_graph_capture():
