@@ -171,6 +171,11 @@ def test_plan_block_lengths_match_the_paper():
             assert k * (p - 1) ** 2 + (p - 1) <= 2 ** m - 1 < (k + 1) * (p - 1) ** 2 + (p - 1)
             lam = P(p, CL, 512, strategy=gfp.HYBRID, acc_bits=m)["block"]
             assert lam * p * (p - 1) < 2 ** m <= (lam + 1) * p * (p - 1)
+    # the library's 8 lanes per DIM = 512 row give each accumulator 64 terms: the same step moves to where
+    # 64 (p-1)^2 + (p-1) crosses 2^32 -- k = 64 at 8191, 63 at 8209 (reading G24; the sweep shows it)
+    assert P(8191, CL, 512, strategy=gfp.BLOCKED, acc_bits=32)["block"] == 64
+    assert P(8209, CL, 512, strategy=gfp.BLOCKED, acc_bits=32)["block"] == 63
+    assert 64 * 8190 ** 2 + 8190 <= 2 ** 32 - 1 < 64 * 8208 ** 2 + 8208
     assert P(40009, CL, 10 ** 6, strategy=gfp.DELAYED)["kernel"].endswith("DELAYED>")
     assert P(65521, CL, 10 ** 6, strategy=gfp.OVERFLOW, acc_bits=32)["reductions_per_thread"] >= 1
 
