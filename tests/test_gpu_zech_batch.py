@@ -94,3 +94,19 @@ def test_zech_batch_full_size_sampled_rows(p):
     got = gfp.dot_batch(cu(A), cu(x), p, ZE).cpu().numpy().astype(np.int64)
     idx = np.unique(np.concatenate([np.arange(0, rows, 131), np.arange(rows - 40, rows)]))
     assert np.array_equal(got[idx], rows_oracle(p, A, x, idx))
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 101, 257])
+def test_zech_batch_every_product_exhaustive(p):
+    """Every pair of codes (i, j), zero included: a batch of rows [i, i, ..., i] (n = 8, one 16-byte vector --
+    the decode kernel's vector path) against x = [j] * 8, so row i is 8 g^i g^j; compared with the oracle."""
+    q = p - 1
+    n = 8
+    A = np.repeat(np.arange(q + 1, dtype=np.uint16), n).reshape(q + 1, n)
+    g = oracle.primitive_root(p)
+    dA = cu(A)
+    for j in range(q + 1):
+        x = np.full(n, j, np.uint16)
+        got = gfp.dot_batch(dA, cu(x), p, ZE).cpu().numpy().astype(np.int64)
+        want = np.array([oracle.dot_zech(p, g, A[i], x) for i in range(q + 1)], np.int64)
+        assert np.array_equal(got, want), (p, j)
