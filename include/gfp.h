@@ -119,9 +119,11 @@ typedef enum {
                                (sec. 2.4, Table 1); partial sums never leave the
                                representation.  Same unique result as the default (integer) plan. */
     GFP_STRAT_CARRY = 6     /* classical and Montgomery: the division-on-demand idea of sec. 3.3
-                               with the correction deferred -- count the wraps of the m-bit sum in a
-                               second word (carry += sum < product) and apply carry * (2^m mod p) once at
-                               the end instead of adding CORR at every wrap (SURVEY 8(f) F2 "carry-word") */
+                               with the correction deferred -- the carry flag of each m-bit add (add-with-
+                               carry instructions, no compare) is counted in a second word and carry *
+                               (2^m mod p) applied once at the end instead of adding CORR at every wrap
+                               (SURVEY 8(f) F2 "carry-word"); the built-in plan for classical u32 storage
+                               when lambda of Eq. (2) is below 4 (p > ~2^31.5) */
 } gfp_strategy;
 
 /* Per-call options.  acc_bits: the accumulator width m of Eq. (1): 0 = default (64; 53 for fp64),
@@ -193,7 +195,10 @@ gfp_status gfp_dot(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const v
  * independent dots / a GF(p) matrix-vector product (sec. 1).
  * A: device, row-major with leading dimension lda >= n (elements);
  * x: device, n elements; out: device, `rows` elements of dtype `dt`.
- * Supported reps: classical (u16, u32), Montgomery (u32), fp64, Zech (u16). */
+ * Supported reps: classical (u16, u32), Montgomery (u32), fp64, Zech (u16), centered.
+ * Zech rows (16-byte aligned A, x and lda): each code of A is decoded by one antilog lookup in shared memory
+ * and multiplied by the decoded x (x decoded once per CTA); the row value is encoded back into a code
+ * (reading G25 in DESIGN.md); unaligned rows take the index-add kernel.  One kernel launch. */
 gfp_status gfp_dot_batch(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *A, int64_t lda,
                          const void *x, int64_t rows, int64_t n, void *out, void *stream);
 
