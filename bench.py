@@ -630,9 +630,13 @@ def main():
             else:
                 xchg = gfp_dist.PeerExchange(group)
             if world > 1:  # one fused dot on a tiny input before the timed region: the group works end to end
-                t = torch.ones(1024, dtype=reps[0]["a"].dtype, device=dev)
-                gfp_dist.dot_fused(t, t, cfg["p"], cfg["rep"], xchg, stream=stream)
-                torch.cuda.synchronize()
+                if isinstance(xchg, gfp_dist.PeerExchange):
+                    if not xchg.check(dev):  # soft timeout: a broken exchange is reported, not trapped
+                        raise RuntimeError("peer stores did not arrive within 10 s")
+                else:
+                    t = torch.ones(1024, dtype=reps[0]["a"].dtype, device=dev)
+                    gfp_dist.dot_fused(t, t, cfg["p"], cfg["rep"], xchg, stream=stream)
+                    torch.cuda.synchronize()
         except Exception as e:  # noqa: BLE001 -- reported in the line, never silently
             err = f"{type(e).__name__}: {e}"
         if world > 1:

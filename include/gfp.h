@@ -258,6 +258,13 @@ gfp_status gfp_xchg_create(void **buf, void *ipc_handle);
 gfp_status gfp_xchg_open(const void *ipc_handle, void **peer_buf);
 gfp_status gfp_xchg_close(void *peer_buf);  /* unmap a gfp_xchg_open mapping */
 gfp_status gfp_xchg_destroy(void *buf);     /* free a gfp_xchg_create buffer (after every peer closed it) */
+/* host, synchronous (connectivity checks before relying on the group): arm a SOFT timeout of `ns` nanoseconds
+ * on this rank's own buffer -- a peer missing that long makes gfp_dot_allreduce record the timeout and encode 0
+ * instead of trapping (0 restores the default trap after ~30 s); gfp_xchg_timed_out reads the record (1 if a
+ * soft timeout expired since the last gfp_xchg_soft_timeout).  Never arm it for production calls: a timed-out
+ * call's result is not the dot. */
+gfp_status gfp_xchg_soft_timeout(void *own_buf, uint64_t ns);
+gfp_status gfp_xchg_timed_out(void *own_buf, int32_t *timed_out);
 /* The whole-group dot: a, b are this rank's shards (n may differ across ranks, may be 0); out[0] (device,
  * one element of dt) receives sum over all ranks' shards of a_i b_i in GF(p), in the representation.  One
  * launch; the default (AUTO) accumulation plan. */

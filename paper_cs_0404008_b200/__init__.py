@@ -104,6 +104,8 @@ _SIGS = {
     "gfp_xchg_open": [_vp, ctypes.POINTER(_vp)],
     "gfp_xchg_close": [_vp],
     "gfp_xchg_destroy": [_vp],
+    "gfp_xchg_soft_timeout": [_vp, _u64],
+    "gfp_xchg_timed_out": [_vp, ctypes.POINTER(ctypes.c_int32)],
     "gfp_dot_allreduce": [_u64, _int, _int, _vp, _vp, _i64, ctypes.POINTER(GfpXchg), _vp, _vp],
     "gfp_mc_create": [ctypes.c_int32, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_u64)],
     "gfp_mc_import": [ctypes.c_int32, _u64, ctypes.c_int32, ctypes.POINTER(_vp)],
@@ -467,6 +469,17 @@ def xchg_close(ptr: int) -> None:
 
 def xchg_destroy(ptr: int) -> None:
     _check(lib.gfp_xchg_destroy(ptr))
+
+
+def xchg_soft_timeout(ptr: int, ns: int) -> None:
+    """Arm (ns > 0) or disarm (0) the soft timeout of this rank's exchange buffer (connectivity checks only)."""
+    _check(lib.gfp_xchg_soft_timeout(ptr, ns))
+
+
+def xchg_timed_out(ptr: int) -> bool:
+    v = ctypes.c_int32(0)
+    _check(lib.gfp_xchg_timed_out(ptr, ctypes.byref(v)))
+    return bool(v.value)
 
 
 def dot_allreduce(a: torch.Tensor, b: torch.Tensor, p: int, rep: int, xchg: GfpXchg,

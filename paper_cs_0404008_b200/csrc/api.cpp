@@ -300,6 +300,23 @@ gfp_status gfp_xchg_destroy(void *buf) {
     return e == cudaSuccess ? GFP_OK : cuda_fail(e, "gfp_xchg_destroy");
 }
 
+gfp_status gfp_xchg_soft_timeout(void *own_buf, uint64_t ns) {
+    if (own_buf == nullptr || !aligned(own_buf, 8)) return fail(GFP_E_INVAL, "gfp_xchg_soft_timeout: bad buffer");
+    const uint64_t w[2] = {ns, 0};  // [kXSoft], and clear [kXTimedOut]
+    cudaError_t e = cudaMemcpy((uint64_t *)own_buf + kXSoft, w, sizeof w, cudaMemcpyHostToDevice);
+    return e == cudaSuccess ? GFP_OK : cuda_fail(e, "gfp_xchg_soft_timeout");
+}
+
+gfp_status gfp_xchg_timed_out(void *own_buf, int32_t *timed_out) {
+    if (own_buf == nullptr || timed_out == nullptr || !aligned(own_buf, 8))
+        return fail(GFP_E_INVAL, "gfp_xchg_timed_out: bad arguments");
+    uint64_t v = 0;
+    cudaError_t e = cudaMemcpy(&v, (uint64_t *)own_buf + kXTimedOut, 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "gfp_xchg_timed_out");
+    *timed_out = v != 0;
+    return GFP_OK;
+}
+
 gfp_status gfp_dot_allreduce(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
                              const gfp_xchg *x, void *out, void *stream) {
     if (x == nullptr) return fail(GFP_E_INVAL, "gfp_dot_allreduce: x is NULL");

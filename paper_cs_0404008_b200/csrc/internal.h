@@ -42,6 +42,8 @@ constexpr int kPackShift = 48;
 // kXPeers + r.  Kernel parameters stay small: one pointer.
 constexpr int kXFlags = 8, kXSlots = 8 + 2 * GFP_XCHG_MAX_WORLD, kXPeers = 8 + 4 * GFP_XCHG_MAX_WORLD,
               kXWords = 8 + 5 * GFP_XCHG_MAX_WORLD;
+// [kXSoft]: a soft timeout in ns (0: trap after ~30 s); [kXTimedOut]: set when a soft timeout expired
+constexpr int kXSoft = 3, kXTimedOut = 4;
 
 constexpr int kMaxGrid = 4096;
 

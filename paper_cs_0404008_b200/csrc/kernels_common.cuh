@@ -96,8 +96,12 @@ __device__ __forceinline__ uint64_t xchg_allreduce(uint64_t r, uint64_t *own, ui
     }
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    // a peer that never arrives: trap after ~30 s (fail loudly, do not hang); with a soft timeout armed in
+    // word [kXSoft] (gfp_xchg_soft_timeout: connectivity checks) record it in [kXTimedOut] and return instead
+    const uint64_t soft = own[kXSoft], limit = soft ? soft : 30000000000ull;
+    bool late = false;
     uint64_t sum = 0;
-    for (int q = 0; q < world; ++q) {
+    for (int q = 0; q < world && !late; ++q) {
         const uint64_t *slot = own + kXSlots + par * GFP_XCHG_MAX_WORLD + q;
         for (;;) {
             uint64_t v;
@@ -108,11 +112,19 @@ __device__ __forceinline__ uint64_t xchg_allreduce(uint64_t r, uint64_t *own, ui
             }
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (t - t0 > 30000000000ull) __trap();  // a peer never arrived: fail loudly, do not hang
+            if (t - t0 > limit) {
+                if (!soft) __trap();
+                late = true;
+                break;
+            }
             __nanosleep(32);
         }
     }
     own[0] = e;
+    if (late) {
+        own[kXTimedOut] = 1;
+        return 0;
+    }
     return mod_p(sum, p, mu);
 }
 

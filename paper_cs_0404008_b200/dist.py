@@ -104,6 +104,20 @@ class PeerExchange:
             self.spec.peers[r] = ptr
         self.group = group
 
+    def check(self, device, seconds: float = 10.0) -> bool:
+        """Connectivity check before relying on the group: one fused dot of a tiny input with a SOFT timeout armed
+        (gfp_xchg_soft_timeout), so a peer whose stores never arrive is reported here as False instead of
+        trapping the kernel.  Every rank of the group must call it (it is one collective epoch)."""
+        from . import CLASSICAL, dot_allreduce, xchg_soft_timeout, xchg_timed_out
+        xchg_soft_timeout(self.own, int(seconds * 1e9))
+        try:
+            t = torch.ones(1024, dtype=torch.uint32, device=device)
+            dot_allreduce(t, t, 65521, CLASSICAL, self.spec)
+            torch.cuda.synchronize(device)
+            return not xchg_timed_out(self.own)
+        finally:
+            xchg_soft_timeout(self.own, 0)
+
     def close(self):
         """Unmap the peers' buffers, wait for every rank to have done the same, free this rank's buffer."""
         for ptr in self.opened:

@@ -671,6 +671,38 @@ def test_dist_dot_on_a_side_stream():
     assert result_int(out) == oracle.dot_classical(p, a, b)
 
 
+def test_fused_allreduce_soft_timeout_reports_a_missing_peer():
+    """A two-rank group whose second rank never runs (its buffer lives in this process, nobody publishes to
+    it): with a soft timeout armed, rank 0's fused dot gives up after the timeout and records it instead of
+    trapping -- the connectivity check bench.py runs before timing a multi-GPU group -- and the one-rank
+    group's check passes."""
+    from paper_cs_0404008_b200 import dist as gd
+    own, _ = gfp.xchg_create()
+    other, _ = gfp.xchg_create()
+    try:
+        spec = gfp.GfpXchg()
+        spec.rank, spec.world = 0, 2
+        spec.peers[0], spec.peers[1] = own, other
+        gfp.xchg_soft_timeout(own, 200_000_000)  # 0.2 s
+        t = cu(np.ones(1000, np.uint32))
+        gfp.dot_allreduce(t, t, 65521, CL, spec)
+        torch.cuda.synchronize()
+        assert gfp.xchg_timed_out(own)
+        gfp.xchg_soft_timeout(own, 0)
+        assert not gfp.xchg_timed_out(own)  # re-arming clears the record
+    finally:
+        torch.cuda.synchronize()
+        gfp.xchg_destroy(own)
+        gfp.xchg_destroy(other)
+    x = gd.PeerExchange()
+    try:
+        assert x.check(torch.device(DEV))
+        a = synth.uniform(SEED, 0, 0, 5000, 65521, np.uint32)
+        assert result_int(gd.dot_fused(cu(a), cu(a), 65521, CL, x)) == oracle.dot_classical(65521, a, a)
+    finally:
+        x.close()
+
+
 def test_fused_allreduce_rejects_bad_groups():
     xs = gfp.GfpXchg()
     xs.rank, xs.world = 0, 0
