@@ -116,3 +116,22 @@ def test_gpus2_without_enough_gpus_fails_loudly():
                        env=_env(WORLD_SIZE="1", RANK="0", LOCAL_RANK="0"), capture_output=True, text=True,
                        timeout=300, cwd=ROOT)
     assert r.returncode != 0 and "WORLD_SIZE=1" in r.stderr
+
+
+def test_lookup_wavefronts_matches_a_direct_count():
+    """bench.lookup_wavefronts (the Zech matrix-vector gather roofline) against a direct per-warp count: lane l
+    looks up code 8 (v0 + l) + k for k in 0..7; a warp lookup takes max over banks of the distinct 32-bit words."""
+    rng = np.random.default_rng(5)
+    A = rng.integers(0, 32749, size=(4, 4096)).astype(np.uint16)
+    A[:, ::10] = 0
+    direct = []
+    for row in A.astype(np.int64):
+        for v0 in range(0, 4096 // 8, 32):
+            for k in range(8):
+                codes = [row[8 * (v0 + l) + k] for l in range(32)]
+                banks = {}
+                for c in codes:
+                    banks.setdefault((c >> 1) & 31, set()).add(c >> 1)
+                direct.append(max(len(s) for s in banks.values()))
+    assert abs(bench.lookup_wavefronts(A, sample_rows=4) - float(np.mean(direct))) < 1e-9
+    assert bench.lookup_wavefronts(np.zeros((2, 4096), np.uint16)) == 1.0  # every lane reads one word
