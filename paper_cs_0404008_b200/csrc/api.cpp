@@ -418,7 +418,7 @@ struct gfp_mc {
     CUdeviceptr mc_va = 0, uc_va = 0;
     size_t size = 0;
     int world = 0, fd = -1, dev = -1;
-    bool added = false, bound = false;
+    bool added = false, bound = false, mc_mapped = false, uc_mapped = false, ready = false;
 };
 
 extern "C" {
@@ -509,6 +509,7 @@ gfp_status gfp_mc_add_device(gfp_mc *m) {
 
 gfp_status gfp_mc_bind(gfp_mc *m) {
     if (m == nullptr || !m->added || m->bound) return fail(GFP_E_INVAL, "gfp_mc_bind: NULL, not added, or bound");
+    if (m->mem) return fail(GFP_E_INVAL, "gfp_mc_bind: a previous bind failed part-way: destroy and recreate");
     const McApi *A = mc_api(nullptr);
     CUdevice cd;
     CUresult r = A->deviceGet(&cd, m->dev);
@@ -522,17 +523,18 @@ gfp_status gfp_mc_bind(gfp_mc *m) {
     memset(&acc, 0, sizeof acc);
     acc.location = prop.location;
     acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    // every step records what it set up, so that gfp_mc_destroy undoes exactly that after a partial failure
     if ((r = A->memCreate(&m->mem, m->size, &prop, 0)) != CUDA_SUCCESS) return cu_fail(r, "cuMemCreate");
     if ((r = A->mcBindMem(m->mc, 0, m->mem, 0, m->size, 0)) != CUDA_SUCCESS) return cu_fail(r, "cuMulticastBindMem");
-    if ((r = A->addrReserve(&m->mc_va, m->size, m->size, 0, 0)) != CUDA_SUCCESS ||
-        (r = A->memMap(m->mc_va, m->size, 0, m->mc, 0)) != CUDA_SUCCESS ||
-        (r = A->memSetAccess(m->mc_va, m->size, &acc, 1)) != CUDA_SUCCESS)
-        return cu_fail(r, "multicast mapping");
-    if ((r = A->addrReserve(&m->uc_va, m->size, m->size, 0, 0)) != CUDA_SUCCESS ||
-        (r = A->memMap(m->uc_va, m->size, 0, m->mem, 0)) != CUDA_SUCCESS ||
-        (r = A->memSetAccess(m->uc_va, m->size, &acc, 1)) != CUDA_SUCCESS)
-        return cu_fail(r, "unicast mapping");
     m->bound = true;
+    if ((r = A->addrReserve(&m->mc_va, m->size, m->size, 0, 0)) != CUDA_SUCCESS) return cu_fail(r, "multicast reserve");
+    if ((r = A->memMap(m->mc_va, m->size, 0, m->mc, 0)) != CUDA_SUCCESS) return cu_fail(r, "multicast map");
+    m->mc_mapped = true;
+    if ((r = A->memSetAccess(m->mc_va, m->size, &acc, 1)) != CUDA_SUCCESS) return cu_fail(r, "multicast access");
+    if ((r = A->addrReserve(&m->uc_va, m->size, m->size, 0, 0)) != CUDA_SUCCESS) return cu_fail(r, "unicast reserve");
+    if ((r = A->memMap(m->uc_va, m->size, 0, m->mem, 0)) != CUDA_SUCCESS) return cu_fail(r, "unicast map");
+    m->uc_mapped = true;
+    if ((r = A->memSetAccess(m->uc_va, m->size, &acc, 1)) != CUDA_SUCCESS) return cu_fail(r, "unicast access");
     // zero this rank's copy, then record the group size in its private words (the caller synchronises the
     // group -- e.g. a barrier -- before any rank's first gfp_dot_allreduce_mc)
     std::vector<uint64_t> init(kMcWords, 0);
@@ -540,18 +542,20 @@ gfp_status gfp_mc_bind(gfp_mc *m) {
     cudaError_t ce = cudaMemset((void *)m->uc_va, 0, m->size);
     if (ce == cudaSuccess) ce = cudaMemcpy((void *)m->uc_va, init.data(), init.size() * 8, cudaMemcpyHostToDevice);
     if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
-    return ce == cudaSuccess ? GFP_OK : cuda_fail(ce, "gfp_mc_bind: init");
+    if (ce != cudaSuccess) return cuda_fail(ce, "gfp_mc_bind: init");
+    m->ready = true;
+    return GFP_OK;
 }
 
 gfp_status gfp_mc_destroy(gfp_mc *m) {
     if (m == nullptr) return fail(GFP_E_INVAL, "gfp_mc_destroy: NULL");
     const McApi *A = mc_api(nullptr);
     cudaDeviceSynchronize();
+    if (m->mc_mapped) A->memUnmap(m->mc_va, m->size);
+    if (m->mc_va) A->addrFree(m->mc_va, m->size);
+    if (m->uc_mapped) A->memUnmap(m->uc_va, m->size);
+    if (m->uc_va) A->addrFree(m->uc_va, m->size);
     if (m->bound) {
-        A->memUnmap(m->mc_va, m->size);
-        A->addrFree(m->mc_va, m->size);
-        A->memUnmap(m->uc_va, m->size);
-        A->addrFree(m->uc_va, m->size);
         CUdevice cd;
         if (A->deviceGet(&cd, m->dev) == CUDA_SUCCESS) A->mcUnbind(m->mc, cd, 0, m->size);
     }
@@ -564,7 +568,7 @@ gfp_status gfp_mc_destroy(gfp_mc *m) {
 
 gfp_status gfp_dot_allreduce_mc(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const void *b, int64_t n,
                                 gfp_mc *m, void *out, void *stream) {
-    if (m == nullptr || !m->bound) return fail(GFP_E_INVAL, "gfp_dot_allreduce_mc: multicast buffer not bound");
+    if (m == nullptr || !m->ready) return fail(GFP_E_INVAL, "gfp_dot_allreduce_mc: multicast buffer not bound");
     return dot_common(p, rep, dt, a, b, n, out, OUT_MC, (cudaStream_t)stream, nullptr, (uint64_t *)m->uc_va,
                       (uint64_t *)m->mc_va);
 }
