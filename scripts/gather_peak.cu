@@ -3,11 +3,13 @@
 // conversions.  The analogue of MEASURED_PEAKS.json's copy bandwidth for HBM: a measured peak,
 // not a datasheet figure.
 //
-//   k_lookup : every thread walks an LCG in registers (1 IMAD + 2 ALU per code), looks the code up in a
-//              64 KB u16 table in shared memory and sums the values -- no global memory at all.  Reports
+//   k_lookup : every thread holds 16 hashed codes in registers and, each iteration, looks up code ^ key (a
+//              warp-uniform key: the same conflict degree, one LOP per lookup) in a 64 KB u16 table in shared
+//              memory and sums the values -- no global memory at all.  Reports
 //              lookups/s and L1TEX data-pipe wavefronts per SM per clock, using the expected wavefronts of a
-//              warp-wide random lookup (the most distinct 32-bit words one of the 32 banks serves, E = 3.52
-//              for 32 active lanes, computed here by simulation of the same codes).
+//              warp-wide random lookup (the most distinct 32-bit words one of the 32 banks serves, E ~ 3.4
+//              for hashed codes with 10% zeros, computed here by simulation of the same codes; ncu's own
+//              wavefront count and pipe utilisation are the primary numbers).
 //   k_stream : the same plus the Zech batch's A stream (a 16-byte LDG per 8 lookups, L1::no_allocate), to
 //              show what streaming A through the same pipe costs.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/gather_peak scripts/gather_peak.cu
@@ -30,26 +32,38 @@
         }                                                                                   \
     } while (0)
 
-constexpr uint32_t kQbar = 32748;            // GF(32749): codes in [0, qbar]
-constexpr uint32_t kA = 1664525u, kC = 1013904223u;  // LCG (Numerical Recipes constants)
+constexpr uint32_t kTabEntries = 32768;  // a 64 KB u16 table (GF(32749)'s codes are 15-bit): every 15-bit index is valid
+constexpr int kCodes = 16;               // codes held in registers per thread
 
-__device__ __forceinline__ uint32_t code_of(uint32_t x) { return min(x >> 17, kQbar); }
+// a thread's codes: hashed from its global index (independent across lanes: E ~ 3.4 wavefronts per warp lookup,
+// as for the Zech matrix-vector product's uniform codes), the zero element (code 0) with probability ~1/10
+__host__ __device__ __forceinline__ uint32_t code_of(uint32_t gid, uint32_t j) {
+    uint32_t h = (gid * 16u + j) * 0x9E3779B1u;
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    return (h & 1023u) < 102u ? 0u : (h >> 17);
+}
+// iteration key, uniform over the warp: index = code ^ key permutes the banks (bank(c ^ k) = bank(c) ^ bank(k)),
+// so every iteration's warp lookup has the same conflict degree as the codes themselves, for one LOP per lookup
+__host__ __device__ __forceinline__ uint32_t key_of(uint32_t it) { return (it * 2654435761u) >> 17; }
 
 template <int NT, int ITERS>
 __global__ void __launch_bounds__(NT, 1) k_lookup(const uint16_t *tabg, unsigned long long *out) {
     extern __shared__ __align__(16) uint16_t tab[];
-    for (int i = threadIdx.x; i < (int)(kQbar + 8) / 8; i += NT)
+    for (int i = threadIdx.x; i < (int)kTabEntries / 8; i += NT)
         reinterpret_cast<uint4 *>(tab)[i] = reinterpret_cast<const uint4 *>(tabg)[i];
     __syncthreads();
-    uint32_t x[8];
+    const uint32_t gid = blockIdx.x * NT + threadIdx.x;
+    uint32_t c[kCodes];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = (blockIdx.x * NT + threadIdx.x) * 2654435761u + j * 40503u;
+    for (int j = 0; j < kCodes; ++j) c[j] = code_of(gid, j);
     uint32_t s0 = 0, s1 = 0;
     for (int it = 0; it < ITERS; ++it) {
+        const uint32_t k = key_of(it);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            x[j] = x[j] * kA + kC;
-            const uint32_t v = tab[code_of(x[j])];
+        for (int j = 0; j < kCodes; ++j) {
+            const uint32_t v = tab[c[j] ^ k];
             if (j & 1) s1 += v; else s0 += v;
         }
     }
@@ -60,52 +74,54 @@ template <int NT, int ITERS>
 __global__ void __launch_bounds__(NT, 1) k_stream(const uint16_t *tabg, const uint4 *A, int64_t nvec,
                                                    unsigned long long *out) {
     extern __shared__ __align__(16) uint16_t tab[];
-    for (int i = threadIdx.x; i < (int)(kQbar + 8) / 8; i += NT)
+    for (int i = threadIdx.x; i < (int)kTabEntries / 8; i += NT)
         reinterpret_cast<uint4 *>(tab)[i] = reinterpret_cast<const uint4 *>(tabg)[i];
     __syncthreads();
-    uint32_t x[8];
+    const uint32_t gid = blockIdx.x * NT + threadIdx.x;
+    uint32_t c[kCodes];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = (blockIdx.x * NT + threadIdx.x) * 2654435761u + j * 40503u;
+    for (int j = 0; j < kCodes; ++j) c[j] = code_of(gid, j);
     uint32_t s0 = 0, s1 = 0, sa = 0;
     int64_t v = (int64_t)blockIdx.x * NT + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * NT;
     for (int it = 0; it < ITERS; ++it) {
-        uint4 a;
-        asm("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
-            : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(A + v));
-        v += stride;
-        if (v >= nvec) v -= nvec;
+        const uint32_t k = key_of(it);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            x[j] = x[j] * kA + kC;
-            const uint32_t val = tab[code_of(x[j])];
-            if (j & 1) s1 += val; else s0 += val;
+        for (int h = 0; h < kCodes / 8; ++h) {  // a 16-byte stream load per 8 lookups (the Zech batch's ratio)
+            uint4 a;
+            asm("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(A + v));
+            v += stride;
+            if (v >= nvec) v -= nvec;
+#pragma unroll
+            for (int j = 8 * h; j < 8 * h + 8; ++j) {
+                const uint32_t val = tab[c[j] ^ k];
+                if (j & 1) s1 += val; else s0 += val;
+            }
+            sa += a.x ^ a.y ^ a.z ^ a.w;
         }
-        sa += a.x ^ a.y ^ a.z ^ a.w;
     }
     if (s0 + s1 + sa == 0xFFFFFFFFu) atomicAdd(out, 1ull);
 }
 
-// expected wavefronts of one warp-wide lookup of the codes thread t's LCG produces (the same sequence)
+// expected wavefronts of one warp-wide lookup, over the same codes and keys
 static double expected_wavefronts(int NT, int grid, int samples) {
     double tot = 0;
     int n = 0;
     for (int w = 0; w < samples; ++w) {
-        const int warp = (w * 7919) % (grid * NT / 32);
-        uint32_t x[32];
-        for (int l = 0; l < 32; ++l) x[l] = (uint32_t)(warp * 32 + l) * 2654435761u + 0 * 40503u;
-        for (int it = 0; it < 16; ++it) {
-            std::vector<std::set<uint32_t>> bank(32);
-            for (int l = 0; l < 32; ++l) {
-                x[l] = x[l] * kA + kC;
-                const uint32_t c = std::min(x[l] >> 17, kQbar);
-                bank[(c >> 1) & 31].insert(c >> 1);
+        const uint32_t warp = (uint32_t)((w * 7919) % (grid * NT / 32));
+        for (int j = 0; j < kCodes; ++j)
+            for (int it = 0; it < 4; ++it) {
+                std::vector<std::set<uint32_t>> bank(32);
+                for (uint32_t l = 0; l < 32; ++l) {
+                    const uint32_t c = code_of(warp * 32 + l, j) ^ key_of(it);
+                    bank[(c >> 1) & 31].insert(c >> 1);
+                }
+                size_t mx = 0;
+                for (auto &b : bank) mx = std::max(mx, b.size());
+                tot += (double)mx;
+                ++n;
             }
-            size_t mx = 0;
-            for (auto &b : bank) mx = std::max(mx, b.size());
-            tot += (double)mx;
-            ++n;
-        }
     }
     return tot / n;
 }
@@ -115,7 +131,7 @@ int main() {
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     CK(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev));
-    std::vector<uint16_t> h(kQbar + 8);
+    std::vector<uint16_t> h(kTabEntries);
     for (size_t i = 0; i < h.size(); ++i) h[i] = (uint16_t)(i * 7 + 1);
     uint16_t *tab = nullptr;
     unsigned long long *out = nullptr;
@@ -127,7 +143,7 @@ int main() {
     CK(cudaMalloc(&A, nvec * 16));
     CK(cudaMemset(A, 1, nvec * 16));
     constexpr int NT = 1024, ITERS = 4096;
-    const size_t smem = (kQbar + 8) * 2;
+    const size_t smem = kTabEntries * 2;
     CK(cudaFuncSetAttribute(k_lookup<NT, ITERS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaFuncSetAttribute(k_stream<NT, ITERS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const double E = expected_wavefronts(NT, sms, 512);
@@ -143,9 +159,9 @@ int main() {
             CK(cudaEventSynchronize(e1));
             float ms = 0;
             CK(cudaEventElapsedTime(&ms, e0, e1));
-            const double lookups = (double)sms * NT * ITERS * 8;
+            const double lookups = (double)sms * NT * ITERS * kCodes;
             const double warp_lookups = lookups / 32;
-            const double wf = warp_lookups * E + (k == 1 ? (double)sms * NT * ITERS * 16 / 128 : 0.0);
+            const double wf = warp_lookups * E + (k == 1 ? (double)sms * NT * ITERS * (kCodes / 8) * 16 / 128 : 0.0);
             const double per_sm_clk = wf / sms / (ms * 1e-3) / 1e9;  // wavefronts per SM per ns
             printf("%s rep %d: %.3f ms, %.3f T lookups/s, E = %.3f wavefronts per warp lookup, "
                    "%.3f G wavefronts per SM per second (%.3f per clock at the %d MHz max clock)%s\n",
