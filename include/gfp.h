@@ -42,8 +42,11 @@
  * Pointers.  Unless a function says "host", every array pointer is a CUDA
  * device pointer on the current device, owned by the caller.  Element
  * pointers must be aligned to their element size (GFP_E_INVAL otherwise);
- * 16-byte alignment of both operands (at equal offsets) enables the
- * vectorised path, anything else is handled by a slower scalar path.
+ * Any alignment is accepted: elements before a's first 16-byte boundary
+ * are a scalar head; b at a different 16-byte phase than a is read as
+ * aligned vectors and realigned in registers by the built-in plans, the
+ * sec. 3.4 hybrid and the sec. 3.3 carry word (other explicit strategies
+ * and GFP_STRAT_ZECH_ADD then take a slower scalar path).
  *
  * Streams.  `stream` is a cudaStream_t passed as void* (NULL = the legacy
  * default stream).  Device-pointer calls are asynchronous: they enqueue work

@@ -52,7 +52,8 @@ struct DotPlan {
     int policy;     // enumerated in kernels_common.cuh
     int grid, block;
     size_t smem;
-    int64_t head;   // scalar elements before the first 16-byte aligned vector (== n if unaligned)
+    int64_t head;   // scalar elements before a's first 16-byte boundary (== n: the whole input scalar)
+    int bshift;     // bytes b's element `head` sits past a 16-byte boundary (0: co-aligned)
     int acc;        // gfp_acc reported for the plan
     int strategy;   // gfp_strategy actually used
     int acc_bits;   // m of the accumulator

@@ -162,6 +162,21 @@ __device__ __forceinline__ uint64_t mc_allreduce(uint64_t r, uint64_t *uc, uint6
     return mod_p(sum, p, mu);
 }
 
+// Bytes [sh, sh + 16) of the 32-byte concatenation lo:hi (sh in {2, 4, ..., 14}, a whole number of elements):
+// the 16-byte window of an operand that is not co-aligned with the other one, from the two aligned vectors it
+// straddles.  Word k of the window is word q + k funnel-shifted with word q + k + 1 (q = sh / 4).
+__device__ __forceinline__ uint4 realign16(uint4 lo, uint4 hi, int sh) {
+    const int q = sh >> 2, r = (sh & 3) * 8;
+    const uint32_t w0 = lo.x, w1 = lo.y, w2 = lo.z, w3 = lo.w, w4 = hi.x, w5 = hi.y, w6 = hi.z, w7 = hi.w;
+    const uint32_t s0 = q == 0 ? w0 : q == 1 ? w1 : q == 2 ? w2 : w3;
+    const uint32_t s1 = q == 0 ? w1 : q == 1 ? w2 : q == 2 ? w3 : w4;
+    const uint32_t s2 = q == 0 ? w2 : q == 1 ? w3 : q == 2 ? w4 : w5;
+    const uint32_t s3 = q == 0 ? w3 : q == 1 ? w4 : q == 2 ? w5 : w6;
+    const uint32_t s4 = q == 0 ? w4 : q == 1 ? w5 : q == 2 ? w6 : w7;
+    return make_uint4(__funnelshift_r(s0, s1, r), __funnelshift_r(s1, s2, r), __funnelshift_r(s2, s3, r),
+                      __funnelshift_r(s3, s4, r));
+}
+
 // Stage a u16 table (entries padded to a multiple of 8) from global into shared memory.
 __device__ __forceinline__ void stage_table(uint16_t *dst, const uint16_t *src, uint32_t entries) {
     const uint4 *s = reinterpret_cast<const uint4 *>(src);

@@ -46,21 +46,28 @@ cudaError_t launch_xchg_setup(uint64_t *own, int rank, int world, uint64_t *cons
 
 // ------------------------------------------------------------------------------ single dot
 
-template <class R, int NT, int U, bool PIPE>
+// CO: a and b co-aligned (bshift == 0, the common case: its code carries no realignment); !CO: the instance for
+// operands whose 16-byte alignments differ (built-in policies only; see plan_dot)
+template <class R, int NT, int U, bool PIPE, bool CO = true>
 __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restrict__ a,
                                                  const typename R::elem *__restrict__ b, int64_t n,
-                                                 int64_t head, KParams K, Workspace ws, OutSpec O) {
+                                                 int64_t head, int bshift, KParams K, Workspace ws, OutSpec O) {
     extern __shared__ __align__(16) uint16_t s_tab[];
     __shared__ uint64_t red[32];
     typename R::Acc acc;
     R::init(acc);
     const int64_t gtid = (int64_t)blockIdx.x * NT + threadIdx.x;
     const int64_t gstride = (int64_t)gridDim.x * NT;
-    const int64_t nvec = (n - head) / R::W;
+    // bshift != 0: b is not co-aligned with a (its element `head` sits bshift bytes past a 16-byte boundary):
+    // every 16-byte window of b is re-assembled from the two aligned vectors it straddles (realign16), and the
+    // last vector goes to the scalar tail, so that no load reaches past b's last element
+    const int64_t nvec = (!CO && (n - head) / R::W > 0) ? (n - head) / R::W - 1 : (n - head) / R::W;
     const uint4 *av = reinterpret_cast<const uint4 *>(a + head);
-    const uint4 *bv = reinterpret_cast<const uint4 *>(b + head);
+    const uint4 *bv = CO ? reinterpret_cast<const uint4 *>(b + head)
+                         : reinterpret_cast<const uint4 *>(reinterpret_cast<uintptr_t>(b + head) & ~uintptr_t(15));
     int64_t i0 = (int64_t)blockIdx.x * (NT * U) + threadIdx.x;
     pdl_prefetch<U, NT>(av, bv, i0, nvec, O.prefetch != 0);
+
     if constexpr (R::kTable && GFP_STAGE_EARLY) stage_table(s_tab, K.antilog, K.antilog_entries);
     pdl_wait();
     const int64_t step = (int64_t)gridDim.x * (NT * U);
@@ -71,7 +78,7 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
     // Without GFP_STAGE_EARLY the first loads are issued before the Zech antilog table is staged, so the
     // stream's DRAM latency overlaps the table copy from L2 into shared memory.
     uint4 ca[U], cb[U];
-    bool have = PIPE && i0 + (U - 1) * NT < nvec;
+    bool have = PIPE && CO && i0 + (U - 1) * NT < nvec;  // (not co-aligned: the plain loop below)
     if (PIPE && have) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -84,7 +91,7 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
         __syncthreads();
         tab = s_tab;
     }
-    if constexpr (PIPE) {
+    if constexpr (PIPE && CO) {
         // two register sets in ping-pong: the next step's loads land in the set not being consumed
         uint4 na[U], nb[U];
         auto step_once = [&](uint4 (&cx)[U], uint4 (&cy)[U], uint4 (&nx_a)[U], uint4 (&nx_b)[U]) {
@@ -109,16 +116,20 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
         }
     }
 
-    // scalar head (the whole input when a and b are not co-aligned)
+    // scalar head (the elements before a's first 16-byte boundary)
     for (int64_t i = gtid; i < head; i += gstride) R::term(acc, a[i], b[i], K, tab);
 
-    // 16-byte vector body (!PIPE): U independent loads of each operand in flight per thread
+    // 16-byte vector body (!PIPE, or b not co-aligned): U independent loads of each operand in flight per thread
+    auto ldb = [&](int64_t i) -> uint4 {
+        if constexpr (CO) return ld_stream(bv + i);
+        else return realign16(ld_stream(bv + i), ld_stream(bv + i + 1), bshift);
+    };
     for (; i0 + (U - 1) * NT < nvec; i0 += step) {
         uint4 xa[U], xb[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             xa[u] = ld_stream(av + i0 + u * NT);
-            xb[u] = ld_stream(bv + i0 + u * NT);
+            xb[u] = ldb(i0 + u * NT);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) R::vec(acc, xa[u], xb[u], K, tab);
@@ -126,7 +137,7 @@ __global__ void __launch_bounds__(NT) dot_kernel(const typename R::elem *__restr
     if (i0 < nvec) {
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            if (i0 + u * NT < nvec) R::vec(acc, ld_stream(av + i0 + u * NT), ld_stream(bv + i0 + u * NT), K, tab);
+            if (i0 + u * NT < nvec) R::vec(acc, ld_stream(av + i0 + u * NT), ldb(i0 + u * NT), K, tab);
     }
     // scalar tail (< W elements)
     for (int64_t i = head + nvec * R::W + gtid; i < n; i += gstride) R::term(acc, a[i], b[i], K, tab);
@@ -379,13 +390,38 @@ __global__ void finalize_kernel(const uint64_t *summed, int count, KParams K, Ou
     write_result(r, O, K, 0);
 }
 
+// policies with a non-co-aligned instance (the built-in plans; explicit strategies take the scalar path then)
+template <class R>
+struct MisOk : std::false_type {};
+template <int M>
+struct MisOk<ClassicalU32<M>> : std::true_type {};
+template <int M>
+struct MisOk<ClassicalU16<M>> : std::true_type {};
+template <int KR>
+struct MisOk<Montgomery<KR>> : std::true_type {};
+template <int KF>
+struct MisOk<Fp64<KF>> : std::true_type {};
+template <bool SM, bool ALL>
+struct MisOk<Zech<SM, ALL>> : std::true_type {};
+template <>
+struct MisOk<ClassicalS<uint64_t, uint32_t, S_HYBRID>> : std::true_type {};
+template <>
+struct MisOk<ClassicalS<uint64_t, uint32_t, S_CARRY>> : std::true_type {};
+// the host side of MisOk: policies whose launch can take bshift != 0
+static bool mis_ok(int pol) {
+    return (pol >= P_CL32_ALL && pol <= P_ZL_THREAD) || pol == cs_policy(true, true, GFP_STRAT_HYBRID) ||
+           pol == cs_policy(true, true, GFP_STRAT_CARRY);
+}
+
 template <class R, int NT, int U, bool PIPE>
 static cudaError_t launch_dot_t(const DotPlan &P, const KParams &K, const void *a, const void *b, int64_t n,
                                 Workspace ws, OutSpec O, cudaStream_t s) {
-    auto kern = dot_kernel<R, NT, U, PIPE>;
+    auto kern = dot_kernel<R, NT, U, PIPE, true>;
+    if constexpr (MisOk<R>::value)
+        if (P.bshift != 0) kern = dot_kernel<R, NT, U, PIPE, false>;
     occupancy(kern, NT, P.smem);  // sets the smem attribute once
     cudaError_t e = launch_pdl(kern, dim3(P.grid), dim3(NT), P.smem, s, (const typename R::elem *)a,
-                               (const typename R::elem *)b, n, P.head, K, ws, O);
+                               (const typename R::elem *)b, n, P.head, P.bshift, K, ws, O);
     count_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -646,9 +682,11 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
     if (xpol >= 0) pol = xpol;
     if (pol == P_ZECH_ADD) smem = (size_t)(zech_add_fast(I.p) ? K.zplus1s_entries : K.zplus1_entries) * 2;
     const int NT = policy_block(pol), U = policy_unroll(pol), W = policy_width(pol);
+    // head: the elements before a's first 16-byte boundary; bshift: how far b's matching element sits past a
+    // 16-byte boundary (0 = co-aligned).  The pure-Zech kernel keeps the scalar path for non-co-aligned inputs.
     const uintptr_t pa = (uintptr_t)a, pb = (uintptr_t)b;
-    int64_t head = n;
-    if (pa % 16 == pb % 16) head = std::min<int64_t>(n, (int64_t)(((16 - pa % 16) % 16) / es));
+    int64_t head = std::min<int64_t>(n, (int64_t)(((16 - pa % 16) % 16) / es));
+    int bshift = (int)((pb + (uintptr_t)head * es) % 16);
     const int64_t nvec = (n - head) / W;
     const int dev_sms = [] {
         int d = 0;
@@ -777,11 +815,18 @@ gfp_status plan_dot(const gfp_info &I, const KParams &K, const void *a, const vo
         } else if (strat == GFP_STRAT_BLOCKED || strat == GFP_STRAT_HYBRID)
             reductions = (int64_t)(kblk ? per_thread / kblk : 0) + 1;
     }
+    // operands not co-aligned: the built-in policies have a realigning kernel instance (MisOk); the other
+    // explicit strategies and the pure-Zech kernel take the scalar path over the whole input
+    if (bshift != 0 && !mis_ok(pol)) {
+        head = n;
+        bshift = 0;
+    }
     P->policy = pol;
     P->grid = (int)grid;
     P->block = NT;
     P->smem = smem;
     P->head = head;
+    P->bshift = bshift;
     P->acc = acc;
     P->strategy = strat;
     P->acc_bits = acc_bits;

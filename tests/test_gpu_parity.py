@@ -127,6 +127,67 @@ def test_misaligned_and_ragged():
         assert result_int(r) == oracle.dot_classical(p, a16[oa:oa + m], b16[ob:ob + m])
 
 
+NON_CO_ALIGNED = [  # (rep, storage, p, explicit strategy or None): every kernel with a realigning instance
+    ("classical", np.uint16, 65521, None),        # 16-bit classical, one remainder
+    ("classical", np.uint32, 65521, None),        # 32-bit classical
+    ("classical", np.uint32, 2 ** 31 - 1, None),  # sec. 3.4 hybrid (lambda = 4)
+    ("classical", np.uint32, 4294967291, None),   # sec. 3.3 carry word (lambda < 4)
+    ("classical", np.uint32, 2 ** 31 - 1, "carry"),
+    ("montgomery", np.uint32, 2 ** 31 - 1, None),
+    ("fp64", np.float64, 67108859, None),
+    ("zech", np.uint16, 32749, None),
+]
+
+
+@pytest.mark.parametrize("case", NON_CO_ALIGNED, ids=lambda c: f"{c[0]}-{np.dtype(c[1]).name}-{c[2]}-{c[3]}")
+def test_non_co_aligned_operands_every_byte_shift(case):
+    """b's element 0 at every byte distance from a's 16-byte phase (the realigned vector path: each 16-byte
+    window of b assembled from the two aligned vectors it straddles), at lengths around the vector width and at
+    several tiles with a ragged tail, against the oracle on the same elements."""
+    kind, dt, p, strat = case
+    es = np.dtype(dt).itemsize
+    per = 16 // es
+    nmax = 70003
+    if kind == "zech":
+        g = gfp.query(p, ZE)["g"]
+        A = synth.zech_codes(SEED + 41, 0, 0, nmax + per, p - 1)
+        B = synth.zech_codes(SEED + 41, 1, 0, nmax + per, p - 1)
+    else:
+        A = residues(p, nmax + per, 0, dt, SEED + 41)
+        B = residues(p, nmax + per, 1, dt, SEED + 41)
+    tA, tB = cu(A), cu(B)
+    if kind == "montgomery":
+        tA, tB = gfp.to_rep(tA, p, MO), gfp.to_rep(tB, p, MO)
+        A, B = host(tA), host(tB)
+    rep = {"classical": CL, "montgomery": MO, "fp64": FP, "zech": ZE}[kind]
+
+    def want(x, y):
+        if kind == "classical":
+            return oracle.dot_classical(p, x, y)
+        if kind == "montgomery":
+            return oracle.dot_montgomery(p, x, y)
+        if kind == "fp64":
+            return oracle.dot_fp64(p, x, y)
+        return oracle.dot_zech(p, g, x, y)
+
+    for oa in range(per):
+        for ob in range(per):
+            if oa == ob:
+                continue
+            for n in (0, 1, per - 1, per, per + 1, 2 * per + 3, 3 * per, 1037, nmax):
+                x, y = tA[oa:oa + n], tB[ob:ob + n]
+                if strat == "carry":
+                    r = gfp.dot_ex(x, y, p, rep, strategy=gfp.CARRY)
+                else:
+                    r = gfp.dot(x, y, p, rep)
+                got = result_int(r)
+                w = want(A[oa:oa + n], B[ob:ob + n])
+                if kind == "fp64":
+                    assert bits(got) == bits(w), (oa, ob, n)
+                else:
+                    assert got == w, (oa, ob, n)
+
+
 def test_empty_gives_zero_in_every_representation():
     e16 = torch.empty(0, dtype=torch.uint16, device=DEV)
     e32 = torch.empty(0, dtype=torch.uint32, device=DEV)
