@@ -903,6 +903,31 @@ def lookup_wavefronts(A, lanes=32, per_vec=8, sample_rows=64):
     return float(counts.max(axis=1).mean())
 
 
+def split_lookup_wavefronts(A, p, lanes=32, per_vec=8, sample_rows=64):
+    """Shared-memory wavefronts per warp-wide lookup of the split-exponent Zech matrix-vector kernel
+    (batch_zsplit_kernel) on these codes, from its address map: e = c - 1 (16 bits), the L lookup reads byte
+    address 0x10000 | (e & 255) << 8 | 4 lane, the H lookup 0x10000 | (e >> 8) << 8 | 128 + 4 lane (p > 65281: the
+    zero code reads 0xFF80 + 4 lane instead); a warp lookup takes as many wavefronts as the most distinct 32-bit
+    words any bank is asked for.  Returns the mean over the L and H lookups (1.0: every lane in its own bank)."""
+    A = np.asarray(A[:sample_rows], dtype=np.int64)
+    n = A.shape[1] // (lanes * per_vec) * (lanes * per_vec)
+    c = A[:, :n].reshape(-1, lanes, per_vec).transpose(0, 2, 1).reshape(-1, lanes)  # (warp lookups, lanes)
+    e = (c - 1) & 0xFFFF
+    lane4 = 4 * np.arange(lanes, dtype=np.int64)[None, :]
+    addr_l = 0x10000 | ((e & 255) << 8) | lane4
+    addr_h = np.where((c == 0) & (p > 65281), 0xFF80 | lane4, 0x10000 | ((e >> 8) << 8) | (128 + lane4))
+    out = []
+    for addr in (addr_l, addr_h):
+        words = addr >> 2
+        key = np.sort(((words & 31) << 20) | words, axis=1)
+        new = np.ones_like(key, dtype=bool)
+        new[:, 1:] = key[:, 1:] != key[:, :-1]
+        counts = np.zeros((key.shape[0], 32), dtype=np.int64)
+        np.add.at(counts, (np.repeat(np.arange(key.shape[0]), lanes)[new.reshape(-1)], (key >> 20)[new]), 1)
+        out.append(float(counts.max(axis=1).mean()))
+    return (out[0] + out[1]) / 2
+
+
 def secondary_table(gfp, args, dev, stream, exclude):
     """Kernel-only throughput of every other config (1 GPU), with roofline fraction."""
     peak, _ = peak_hbm()
@@ -955,28 +980,32 @@ def secondary_table(gfp, args, dev, stream, exclude):
         if phases:
             table[cfg["name"]]["phases"] = phases
         if cfg["kind"] == "batch" and cfg["rep"] == 3:
-            # the binding roofline: each SM's L1TEX data pipe moves one 128-byte wavefront per clock, shared by
-            # the random table lookups (one per term: the most distinct 32-bit words any bank serves per warp
-            # lookup, measured on these codes) and the stream of A through L1 (one wavefront per 128 bytes);
-            # ncu: the pipe is 88.7% busy in the index-add kernel (profiles/r02_zbatch_indexadd_32749_ncu_full.txt)
-            wf = lookup_wavefronts(h["A"])
+            # the data-pipe roofline of batch_zsplit_kernel: each SM's L1TEX data pipe moves one 128-byte wavefront
+            # per clock, shared by the table lookups (TWO per term, g^c = H[e >> 8] L[e & 255] with e = c - 1, each
+            # a conflict-free warp lookup into the bank-replicated 256-entry tables: wavefronts per warp lookup
+            # computed from the kernel's address map on these codes) and the stream of A through L1 (one wavefront
+            # per 128 bytes).  HBM (2 bytes per term) is the other floor, about as low.
+            wf = split_lookup_wavefronts(h["A"], cfg["p"])
             sms = torch.cuda.get_device_properties(dev).multi_processor_count
             clk = (ClockSampler(dev.index).max_mhz or 1965) * 1e6
-            lookup_wf = terms / 32 * wf
+            lookup_wf = 2 * terms / 32 * wf
             stream_wf = d["A"].numel() * d["A"].element_size() / 128
             peak_wf, peak_src = gather_peak()
             floor_us = (lookup_wf + stream_wf) / (sms * clk) * 1e6  # at the nominal 1 wavefront per clock
             roof_us = floor_us / peak_wf  # at the measured achievable rate
             table[cfg["name"]]["gather_roofline"] = {
-                "bound": "l1tex_data_pipe", "lookups": terms, "wavefronts_per_warp_lookup": round(wf, 3),
+                "bound": "l1tex_data_pipe", "kernel": "batch_zsplit_kernel", "lookups": 2 * terms,
+                "wavefronts_per_warp_lookup": round(wf, 3),
                 "lookup_wavefronts": int(lookup_wf), "stream_wavefronts": int(stream_wf),
                 "sms": sms, "clock_mhz": clk / 1e6, "peak_wavefronts_per_clock": peak_wf, "peak_source": peak_src,
                 "us": round(roof_us, 2), "frac": round(roof_us / (avg * 1e3), 4),
                 "nominal_us": round(floor_us, 2), "frac_of_nominal": round(floor_us / (avg * 1e3), 4),
                 "lookups_only_us": round(lookup_wf / (sms * clk) * 1e6, 2),
-                "note": "one random antilog lookup per term plus A streamed through L1, 1 data-pipe wavefront per "
-                        "clock per SM; the staged x reads (4 wavefronts per warp and 2 rows of 256 terms) are "
-                        "implementation overhead, not in the floor"}
+                "hbm_floor_us": round(nbytes / (peak * 1e9) * 1e6, 2),
+                "note": "two conflict-free lookups per term (split exponent, bank-replicated 256-entry tables) plus A "
+                        "streamed through L1, 1 data-pipe wavefront per clock per SM; the staged x reads (4 "
+                        "wavefronts per warp and 2 rows of 256 terms) are implementation overhead, not in the floor; "
+                        "the round-2 single-lookup kernel (3.37 wavefronts per lookup) had a 115.9 us floor"}
         if xchg is not None:  # the fused result must equal the plain dot's
             with torch.cuda.stream(stream):
                 plain = gfp.dot(reps[0]["a"], reps[0]["b"], cfg["p"], cfg["rep"], stream=stream)

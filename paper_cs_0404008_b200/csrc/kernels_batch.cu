@@ -216,6 +216,163 @@ __global__ void __launch_bounds__(NT, MINB) batch_zech_kernel(const uint16_t *__
     pdl_exit();
 }
 
+// ------------------------------------------------------------------------------ batch: Zech matrix-vector, split exponent
+// Zech codes (sec. 2.4): a nonzero code c in [1, qbar] is g^c.  Write e = c - 1 = 256 h + l (16 bits):
+// g^c = H[h] L[l] with L[l] = g^(l + 1) and H[h] = g^(256 h), two lookups into 256-entry tables instead of one
+// into a q-entry table.  The small tables are REPLICATED per bank: row r of the table region is 256 bytes,
+// words [0, 32) hold L[r] 32 times and words [32, 64) H[r] 32 times, so lane i reads word i (+ 32) of its row
+// and a warp-wide lookup touches 32 distinct banks -- ONE shared-memory wavefront, where a random lookup into
+// the q-entry table costs ~3.4 (the most distinct words one bank is asked for).  Two conflict-free
+// lookups per term (2 wavefronts per 32 terms) against 3.37 move the L1TEX data-pipe floor of the matrix-vector
+// product from ~116 us to ~80 us at 65536 x 4096, near the HBM floor (~72 us).
+// Addresses are built by byte permutes: the table region sits at the absolute shared address 0x10000 (64 KB
+// aligned), so a row address is the byte pattern [lane*4 (+128), row, 0x01, 0] -- one PRMT from e and a base
+// register per lookup.  The zero code:
+//   FLAG = false (p <= 65281, so e <= qbar - 1 < 0xFF00): e = c - 1 per 16-bit half (one VIADD.16x2 per pair of
+//     codes) sends code 0 to e = 0xFFFF, whose row h = 255 no nonzero code uses: H[255] = 0.
+//   FLAG = true (any p): t = c + 0xFFFF in 32 bits holds e in bytes 0-1 and [c != 0] in byte 2; the H address
+//     takes byte 2 of t as its 64 KB page, so code 0 reads the zero words at absolute 0xFF80 + 4 lane instead.
+// Products: v = L H < p^2 < 2^32 (one IMAD), v x_j < 2^48 added into a u64 per row and lane (one IMAD.WIDE);
+// the row total n (p - 1)^3 < 2^64 is host-checked.  x is decoded once per CTA and staged as u16 (one LDS.128 per
+// 8 columns serves the RP rows of a warp), rows end with one mod p and the log-table encoding.
+constexpr uint32_t kZsTab = 0x10000u;  // absolute shared address of the split table (256 rows x 256 bytes)
+constexpr int64_t kZsXBytes = 0xFF80 - 0x1000;  // staged x below the zero words, allowing 4 KB of reserved base
+template <int NT, int U, int RP, bool FLAG>
+__global__ void __launch_bounds__(NT, 1) batch_zsplit_kernel(const uint16_t *__restrict__ A, int64_t lda,
+                                                              const uint16_t *__restrict__ x, int64_t rows, int64_t n,
+                                                              KParams K, OutSpec O) {
+    extern __shared__ __align__(16) uint16_t s_x[];  // decoded x (u16), below the table; smem = 128 KB
+    const uint32_t sx = (uint32_t)__cvta_generic_to_shared(s_x);
+    const uint32_t qbar = K.qbar;
+    // the split table (library-owned values): staged before the PDL wait
+    for (uint32_t i = threadIdx.x; i < 4096; i += NT) {  // 16-byte pieces: row i / 16, piece i % 16
+        const uint32_t r = i >> 4;
+        const bool hi = (i & 15) >= 8;
+        const uint32_t ex = hi ? 256 * r : r + 1, t = ex % qbar;  // exponent in [1, qbar] (g^qbar = g^0)
+        uint32_t v = K.antilog[t == 0 ? qbar : t];
+        if (!FLAG && hi && r == 255) v = 0;  // the zero code's row (e = 0xFFFF)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(kZsTab + 16 * i), "r"(v) : "memory");
+    }
+    if (FLAG && threadIdx.x < 8)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(kZsTab - 128 + 16 * threadIdx.x), "r"(0u) : "memory");
+    batch_pdl_enter<U, 32, NT>(A, lda, rows, n / 8, true);
+    // x decoded (0 for the zero code, g^c else) in the vector layout: vector slots [0, 32 vpl) of which those at
+    // or past nvec hold zeros (a lane without a vector there re-reads a valid one: its products vanish), then
+    // the < 8 tail elements
+    const int64_t nvec = n / 8;
+    const int vpl = (int)max((nvec + 31) / 32, (int64_t)1);  // 16-byte vectors per row, per lane
+    const int64_t xtail = 256 * (int64_t)vpl, nxs = xtail + 8;
+    if (sx + 2 * (uint64_t)nxs > kZsTab - 128) __trap();  // host-checked: x fits below the table
+    for (int64_t j = threadIdx.x; j < nxs; j += NT) {
+        const int64_t src = j < xtail ? (j < nvec * 8 ? j : n) : nvec * 8 + (j - xtail);
+        const uint32_t c = src < n ? min((uint32_t)x[src], qbar) : 0u;
+        s_x[j] = c == 0 ? (uint16_t)0 : K.antilog[c];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t bL = kZsTab | (4u * lane), bH = (FLAG ? 0u : kZsTab) | (4u * lane + 128u);
+    auto lds = [](uint32_t a) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+        return v;
+    };
+    // two codes of one 32-bit word against their decoded x values
+    auto pair = [&](uint32_t w, uint32_t xa, uint32_t xb, uint64_t &acc) {
+        uint32_t la, ha, lb, hb;
+        if constexpr (FLAG) {
+            const uint32_t ta = (w & 0xFFFFu) + 0xFFFFu, tb = (w >> 16) + 0xFFFFu;
+            la = lds(__byte_perm(ta, bL, 0x7604));
+            ha = lds(__byte_perm(ta, bH, 0x7214));
+            lb = lds(__byte_perm(tb, bL, 0x7604));
+            hb = lds(__byte_perm(tb, bH, 0x7214));
+        } else {
+            uint32_t t;
+            asm("add.u16x2 %0, %1, %2;" : "=r"(t) : "r"(w), "r"(0xFFFFFFFFu));  // e = c - 1 per half
+            la = lds(__byte_perm(t, bL, 0x7604));
+            ha = lds(__byte_perm(t, bH, 0x7614));
+            lb = lds(__byte_perm(t, bL, 0x7624));
+            hb = lds(__byte_perm(t, bH, 0x7634));
+        }
+        acc += (uint64_t)(la * ha) * xa;
+        acc += (uint64_t)(lb * hb) * xb;
+    };
+    auto vec8 = [&](const uint4 a, const uint4 xw, uint64_t &acc) {
+        pair(a.x, xw.x & 0xFFFFu, xw.x >> 16, acc);
+        pair(a.y, xw.y & 0xFFFFu, xw.y >> 16, acc);
+        pair(a.z, xw.z & 0xFFFFu, xw.z >> 16, acc);
+        pair(a.w, xw.w & 0xFFFFu, xw.w >> 16, acc);
+    };
+    const uint4 *xv = reinterpret_cast<const uint4 *>(s_x);
+    // row indices in 32 bits (the launcher checks rows < 2^31)
+    const int nrows = (int)rows;
+    const int warp0 = (int)blockIdx.x * (NT / 32) + (int)(threadIdx.x >> 5);
+    const int gstride = (int)gridDim.x * (NT / 32) * RP;  // rows between a warp's row groups
+    // A warp walks a stream of elements (row group of RP rows, vector k < vpl of each row); a ring of U elements
+    // is in flight per lane: the slot just consumed is refilled at once with the element U ahead (the same row
+    // group or, in a group's last turn, the next one), so ~U elements stay in flight while the lane computes.
+    // Loads are never predicated off: a row past the matrix re-reads the last row (its sum is never written),
+    // a vector slot past the row re-reads a valid vector (its staged x is 0).
+    const uint4 *A4 = reinterpret_cast<const uint4 *>(A);
+    const int64_t lda8 = lda / 8;  // row stride in 16-byte vectors (the launcher checks lda * 2 % 16 == 0)
+    const int vmax = (int)max(nvec, (int64_t)1) - 1;
+    int lrow = warp0 * RP;  // row group being loaded
+    const uint4 *lp;        // its first row (clamped into the matrix)
+    int loff[RP];           // offsets of its rows in vectors (a row past the matrix: the last row's)
+    auto set_group = [&]() {
+        const int r0 = lrow < nrows ? lrow : nrows - 1;
+        lp = A4 + (int64_t)r0 * lda8;
+#pragma unroll
+        for (int r = 1; r < RP; ++r) loff[r] = (r0 + r < nrows ? r : nrows - 1 - r0) * (int)lda8;
+    };
+    // element k of a lane: vector lane + 32 k of each row of the group
+    auto load = [&](uint4 (&e)[RP], int k) {
+        const int v = min(lane + 32 * k, vmax);
+#pragma unroll
+        for (int r = 0; r < RP; ++r) e[r] = ld_stream(lp + (r == 0 ? v : loff[r] + v));
+    };
+    set_group();
+    uint4 ring[U][RP];
+#pragma unroll
+    for (int u = 0; u < U; ++u) load(ring[u], u);
+    uint64_t acc[RP];
+#pragma unroll
+    for (int r = 0; r < RP; ++r) acc[r] = 0;
+    // U divides vpl (launcher): each row group is vpl / U unrolled ring turns, then its completion
+    for (int urow = warp0 * RP; urow < nrows; urow += gstride) {
+#pragma unroll 2  // two turns per iteration: the ring is renamed instead of copied (B200: 108.3 -> 101.8 us)
+        for (int uk = 0; uk < vpl; uk += U) {
+            int lk = uk + U;  // elements loaded in this turn: k = lk + u of the load group
+            if (lk == vpl) {
+                lk = 0;
+                lrow += gstride;
+                set_group();
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                uint4 cur[RP];
+#pragma unroll
+                for (int r = 0; r < RP; ++r) cur[r] = ring[u][r];
+                load(ring[u], lk + u);
+                const uint4 xw = xv[lane + 32 * (uk + u)];
+#pragma unroll
+                for (int r = 0; r < RP; ++r) vec8(cur[r], xw, acc[r]);
+            }
+        }
+        for (int64_t j = nvec * 8 + lane; j < n; j += 32) {  // scalar tail: code and x in the low halves
+#pragma unroll
+            for (int r = 0; r < RP; ++r)
+                if (urow + r < nrows) pair((uint32_t)A[(int64_t)(urow + r) * lda + j], s_x[xtail + j - nvec * 8], 0u, acc[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+            const uint64_t t = warp_sum(acc[r]);  // row total < n (p-1)^3 < 2^64 (host-checked)
+            if (lane == 0 && urow + r < nrows) write_result(mod_p(t, K.p, K.mu), O, K, urow + r);
+            acc[r] = 0;
+        }
+    }
+    pdl_exit();
+}
+
 // ------------------------------------------------------------------------------ batch: generic
 // Row loads: with L >= 8 lanes per row a warp's 16-byte loads cover whole 128-byte lines (streamed past L1);
 // with one lane per row each lane walks its own row, so its loads may allocate in L1: the second half of a
@@ -508,6 +665,29 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
     case GFP_REP_ZECH: {
         // decode kernel (batch_zech_kernel) for aligned rows: one lookup per term in a q-entry table; the row
         // total n (p-1)^2 must fit the u64 (always for n < 2^32)
+        // split-exponent kernel (batch_zsplit_kernel): two conflict-free lookups per term; the row total
+        // n (p-1)^3 must fit the u64 and x must fit below the table (absolute shared 0xFF80, less the reserved base)
+        const int64_t zvpl = std::max<int64_t>((n / 8 + 31) / 32, 1);
+        if (GFP_ZSPLIT && vec && lanes == 0 && n >= 8 && rows < (int64_t(1) << 31) && lda / 8 * 2 < (int64_t(1) << 31) && (u128)n * q2 * pm1 <= max64 && 2 * (256 * zvpl + 8) <= kZsXBytes) {
+            constexpr int ZNT = GFP_ZS_NT, ZU = GFP_ZS_U, ZRP = GFP_ZS_RP;
+            const bool flag = I.p > 65281;  // the zero code needs the flag page (no free H row)
+            // ring depth: the largest of {ZU, 2, 1} dividing the vectors per lane and row
+            const int64_t vpl = zvpl;
+            auto kern = flag ? batch_zsplit_kernel<ZNT, 1, ZRP, true> : batch_zsplit_kernel<ZNT, 1, ZRP, false>;
+            if (vpl % ZU == 0)
+                kern = flag ? batch_zsplit_kernel<ZNT, ZU, ZRP, true> : batch_zsplit_kernel<ZNT, ZU, ZRP, false>;
+            else if (vpl % 2 == 0)
+                kern = flag ? batch_zsplit_kernel<ZNT, 2, ZRP, true> : batch_zsplit_kernel<ZNT, 2, ZRP, false>;
+            const size_t smem = 2 * (size_t)kZsTab;  // the table ends at absolute 0x20000
+            const int bps = occupancy(kern, ZNT, smem);
+            const int64_t rpb = ZNT / 32 * GFP_ZS_RP;
+            const int64_t grid = std::min<int64_t>((rows + rpb - 1) / rpb, (int64_t)num_sms(dev) * bps);
+            cudaError_t le = launch_pdl(kern, dim3((unsigned)std::max<int64_t>(grid, 1)), dim3(ZNT), smem, s,
+                                        (const uint16_t *)A, lda, (const uint16_t *)x, rows, n, K, O);
+            count_launch();
+            *err = le != cudaSuccess ? le : cudaGetLastError();
+            break;
+        }
         const uint32_t zentries = (uint32_t)((I.p + 7) & ~7ull);  // codes [0, qbar] = p entries
         const size_t zsmem = (size_t)zentries * 2 + (size_t)(((n + 1) / 2 + 3) & ~int64_t(3)) * 4;
         if (GFP_ZBATCH_DECODE && vec && lanes == 0 && (u128)n * q2 <= max64 && zsmem <= kBatchSmemX) {

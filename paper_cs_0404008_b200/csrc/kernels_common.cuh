@@ -251,6 +251,18 @@ __device__ __forceinline__ void pdl_exit() {
 #ifndef GFP_ZBATCH_DECODE
 #define GFP_ZBATCH_DECODE 1  // 1: Zech matrix-vector by decode + DP2A (batch_zech_kernel); 0: index-add batch_kernel
 #endif
+#ifndef GFP_ZSPLIT
+#define GFP_ZSPLIT 1  // 1: Zech matrix-vector by split-exponent lookups (batch_zsplit_kernel) where it applies
+#endif
+#ifndef GFP_ZS_NT
+#define GFP_ZS_NT 1024  // threads per CTA of the split-exponent batch (one CTA per SM: 128 KB of shared memory)
+#endif
+#ifndef GFP_ZS_U
+#define GFP_ZS_U 2  // 16-byte A vectors per row and lane in flight in the split-exponent batch
+#endif
+#ifndef GFP_ZS_RP
+#define GFP_ZS_RP 2  // rows a warp of the split-exponent batch walks at once
+#endif
 #ifndef GFP_ZDEC_RP
 #define GFP_ZDEC_RP 2  // rows a warp of the decode batch walks at once (each staged x read serves RP rows)
 #endif

@@ -135,3 +135,21 @@ def test_lookup_wavefronts_matches_a_direct_count():
                 direct.append(max(len(s) for s in banks.values()))
     assert abs(bench.lookup_wavefronts(A, sample_rows=4) - float(np.mean(direct))) < 1e-9
     assert bench.lookup_wavefronts(np.zeros((2, 4096), np.uint16)) == 1.0  # every lane reads one word
+
+
+def test_split_lookup_wavefronts_every_lane_in_its_own_bank():
+    """bench.split_lookup_wavefronts (the split-exponent kernel's roofline): from the kernel's address map every
+    warp lookup is one wavefront, whatever the codes (random, all equal, zeros, both zero-code layouts); and a
+    direct recount of one warp lookup's banks from the byte addresses agrees."""
+    rng = np.random.default_rng(7)
+    for p in (32749, 65269, 65287, 65521):
+        A = rng.integers(0, p, size=(4, 4096)).astype(np.uint16)
+        A[:, ::10] = 0
+        assert bench.split_lookup_wavefronts(A, p, sample_rows=4) == 1.0
+        assert bench.split_lookup_wavefronts(np.zeros((2, 4096), np.uint16), p) == 1.0
+        assert bench.split_lookup_wavefronts(np.full((2, 4096), p - 1, np.uint16), p) == 1.0
+    codes = rng.integers(0, 65521, size=32)
+    e = (codes - 1) & 0xFFFF
+    for addr in (0x10000 | ((e & 255) << 8) | 4 * np.arange(32), 0x10000 | ((e >> 8) << 8) | (128 + 4 * np.arange(32))):
+        banks = (addr >> 2) & 31
+        assert sorted(banks.tolist()) == list(range(32))  # 32 distinct banks: one wavefront

@@ -1,8 +1,9 @@
-"""GPU parity of the Zech matrix-vector product (gfp_dot_batch over Zech codes, sec. 2.4): the decode kernel
-(batch_zech_kernel: one antilog lookup per code of A, x decoded once per CTA, DP2A products) and its fallback
-(the index-add batch_kernel<Zech> for unaligned rows or an explicit lanes_per_row), each row compared with
-the oracle's Zech dot (independent decoding by repeated multiplication, one 128-bit remainder per term,
-brute-force discrete-log encoding)."""
+"""GPU parity of the Zech matrix-vector product (gfp_dot_batch over Zech codes, sec. 2.4): the split-exponent
+kernel (batch_zsplit_kernel: g^c = H[(c-1) >> 8] L[(c-1) & 255] from bank-replicated tables, the zero code through
+a free H row for p <= 65281 or a flag page above), the single-lookup decode kernel (batch_zech_kernel, rows too
+long for the split kernel's bound) and the index-add fallback (batch_kernel<Zech>: unaligned rows or an explicit
+lanes_per_row), each row compared with the oracle's Zech dot (independent decoding by repeated multiplication,
+one 128-bit remainder per term, brute-force discrete-log encoding)."""
 import numpy as np
 import pytest
 import torch
@@ -34,8 +35,9 @@ def rows_oracle(p, A, x, rows_idx):
     return np.array([oracle.dot_zech(p, g, A[r], x) for r in rows_idx], np.int64)
 
 
-@pytest.mark.parametrize("p", [2, 3, 5, 101, 257, 2903, 32749, 40009, 65521])
-@pytest.mark.parametrize("shape", [(1, 1), (7, 8), (33, 255), (65, 4096), (3, 4103), (130, 777), (2, 0)])
+@pytest.mark.parametrize("p", [2, 3, 5, 101, 257, 2903, 32749, 40009, 65269, 65287, 65521])
+@pytest.mark.parametrize("shape", [(1, 1), (7, 8), (33, 255), (65, 4096), (3, 4103), (130, 777), (2, 0), (257, 768),
+                                   (5, 16), (4099, 512)])
 def test_zech_batch_shapes(p, shape):
     rows, n = shape
     seed = synth.BASE_SEED + p
@@ -45,7 +47,7 @@ def test_zech_batch_shapes(p, shape):
     assert np.array_equal(got, rows_oracle(p, A, x, range(rows))), (p, shape)
 
 
-@pytest.mark.parametrize("p", [32749, 65521])
+@pytest.mark.parametrize("p", [32749, 65269, 65287, 65521])
 def test_zech_batch_worst_case_and_zeros(p):
     """Rows of the code of -1 (value p - 1: the largest products), rows of zeros, x of -1 / of zeros."""
     g = oracle.primitive_root(p)
@@ -110,3 +112,29 @@ def test_zech_batch_every_product_exhaustive(p):
         got = gfp.dot_batch(dA, cu(x), p, ZE).cpu().numpy().astype(np.int64)
         want = np.array([oracle.dot_zech(p, g, A[i], x) for i in range(q + 1)], np.int64)
         assert np.array_equal(got, want), (p, j)
+
+
+@pytest.mark.parametrize("p", [65269, 65287, 65521])
+def test_zech_batch_zero_row_codes(p):
+    """The codes whose e = c - 1 sits in the split kernel's last H row (e >> 8 = 255: zero-code row at p <= 65281,
+    shared with the zero code's flag page above) and the codes around every 256 boundary, against the oracle."""
+    g = oracle.primitive_root(p)
+    q = p - 1
+    special = [0, 1, 2, 255, 256, 257, q - 1, q] + [c for c in range(0xFF00, q + 1, 7)]
+    special = np.array(sorted(set(c for c in special if 0 <= c <= q)), np.uint16)
+    n = 4096
+    A = np.resize(special, (64, n)).astype(np.uint16)
+    A[1::2] = np.roll(A[1::2], 3, axis=1)
+    x = np.resize(special[::-1], n).astype(np.uint16)
+    got = gfp.dot_batch(cu(A), cu(x), p, ZE).cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, rows_oracle(p, A, x, range(64)))
+
+
+def test_zech_batch_rows_past_the_split_bound():
+    """Rows too long for the split kernel's bound n (p-1)^3 < 2^64 at GF(65521) (n > 65536) still match the oracle
+    (the other Zech batch kernels serve them)."""
+    p, rows, n = 65521, 3, 70000
+    A = synth.zech_codes(synth.BASE_SEED, 2, 0, rows * n, p - 1).reshape(rows, n)
+    x = synth.zech_codes(synth.BASE_SEED, 3, 0, n, p - 1)
+    got = gfp.dot_batch(cu(A), cu(x), p, ZE).cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, rows_oracle(p, A, x, range(rows)))
