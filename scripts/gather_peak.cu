@@ -104,6 +104,83 @@ __global__ void __launch_bounds__(NT, 1) k_stream(const uint16_t *tabg, const ui
     if (s0 + s1 + sa == 0xFFFFFFFFu) atomicAdd(out, 1ull);
 }
 
+// the same lookups while each warp streams A through a TMA ring in shared memory instead of LDG: per 8 lookups per
+// lane, lane 0 re-arms one stage (512 bytes, the warp's 16 bytes per lane) with cp.async.bulk and an mbarrier
+// transaction count; READ = every lane also reads its 16 bytes back (LDS.128), as a consumer would.  Shows what the
+// copy engine's shared-memory writes cost the lookups (a TMA-fed A stream for the Zech matrix-vector
+// product).
+constexpr int kStages = 4;
+__device__ __forceinline__ uint32_t sa(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+template <int NT, int ITERS, bool READ>
+__global__ void __launch_bounds__(NT, 1) k_tma(const uint16_t *tabg, const uint4 *A, int64_t nvec,
+                                                unsigned long long *out) {
+    extern __shared__ __align__(16) uint16_t tab[];
+    uint4 *ring = reinterpret_cast<uint4 *>(tab + kTabEntries);  // [warp][stage][32 lanes]
+    __shared__ __align__(8) uint64_t mbar[NT / 32][kStages];
+    for (int i = threadIdx.x; i < (int)kTabEntries / 8; i += NT)
+        reinterpret_cast<uint4 *>(tab)[i] = reinterpret_cast<const uint4 *>(tabg)[i];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t nch = nvec / 32;  // 512-byte chunks
+    int64_t ch = (int64_t)blockIdx.x * (NT / 32) + w;
+    const int64_t cstride = (int64_t)gridDim.x * (NT / 32);
+    uint4 *wr = ring + (size_t)w * kStages * 32;
+    auto issue = [&](int st) {
+        const uint32_t mb = sa(&mbar[w][st]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(512));
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(sa(wr + st * 32)), "l"(A + ch * 32), "r"(512), "r"(mb) : "memory");
+        ch += cstride;
+        if (ch >= nch) ch -= nch;
+    };
+    if (lane == 0) {
+        for (int st = 0; st < kStages; ++st) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&mbar[w][st])));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+        for (int st = 0; st < kStages; ++st) issue(st);
+    }
+    __syncthreads();
+    const uint32_t gid = blockIdx.x * NT + threadIdx.x;
+    uint32_t c[kCodes];
+#pragma unroll
+    for (int j = 0; j < kCodes; ++j) c[j] = code_of(gid, j);
+    uint32_t s0 = 0, s1 = 0, sa_ = 0;
+    uint32_t step = 0;
+    for (int it = 0; it < ITERS; ++it) {
+        const uint32_t k = key_of(it);
+#pragma unroll
+        for (int h = 0; h < kCodes / 8; ++h, ++step) {
+            const int st = step % kStages;
+            const uint32_t par = (step / kStages) & 1, mb = sa(&mbar[w][st]);
+            uint32_t done = 0;
+            while (!done)
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                             : "=r"(done) : "r"(mb), "r"(par) : "memory");
+            if (READ) {
+                const uint4 a = wr[st * 32 + lane];
+                sa_ += a.x ^ a.y ^ a.z ^ a.w;
+            }
+#pragma unroll
+            for (int j = 8 * h; j < 8 * h + 8; ++j) {
+                const uint32_t val = tab[c[j] ^ k];
+                if (j & 1) s1 += val; else s0 += val;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(st);
+            }
+        }
+    }
+    if (lane == 0)  // drain the ring before the CTA exits
+        for (int st = 0; st < kStages; ++st, ++step) {
+            const uint32_t par = (step / kStages) & 1, mb = sa(&mbar[w][step % kStages]);
+            uint32_t done = 0;
+            while (!done)
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                             : "=r"(done) : "r"(mb), "r"(par) : "memory");
+        }
+    if (s0 + s1 + sa_ == 0xFFFFFFFFu) atomicAdd(out, 1ull);
+}
+
 // expected wavefronts of one warp-wide lookup, over the same codes and keys
 static double expected_wavefronts(int NT, int grid, int samples) {
     double tot = 0;
@@ -146,28 +223,37 @@ int main() {
     const size_t smem = kTabEntries * 2;
     CK(cudaFuncSetAttribute(k_lookup<NT, ITERS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaFuncSetAttribute(k_stream<NT, ITERS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const size_t smem_tma = smem + (size_t)(NT / 32) * kStages * 512;
+    CK(cudaFuncSetAttribute(k_tma<NT, ITERS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tma));
+    CK(cudaFuncSetAttribute(k_tma<NT, ITERS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tma));
     const double E = expected_wavefronts(NT, sms, 512);
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    for (int k = 0; k < 2; ++k) {
+    const char *names[4] = {"k_lookup (random u16 lookups, no global memory)", "k_stream (+ a 16-byte LDG per 8 lookups)",
+                            "k_tma_read (+ the same bytes by TMA into smem, read back with LDS.128)",
+                            "k_tma_noread (+ the same bytes by TMA into smem, not read)"};
+    for (int k = 0; k < 4; ++k) {
         for (int rep = 0; rep < 6; ++rep) {
             CK(cudaEventRecord(e0));
             if (k == 0) k_lookup<NT, ITERS><<<sms, NT, smem>>>(tab, out);
-            else k_stream<NT, ITERS><<<sms, NT, smem>>>(tab, A, nvec, out);
+            else if (k == 1) k_stream<NT, ITERS><<<sms, NT, smem>>>(tab, A, nvec, out);
+            else if (k == 2) k_tma<NT, ITERS, true><<<sms, NT, smem_tma>>>(tab, A, nvec, out);
+            else k_tma<NT, ITERS, false><<<sms, NT, smem_tma>>>(tab, A, nvec, out);
+            CK(cudaGetLastError());
             CK(cudaEventRecord(e1));
             CK(cudaEventSynchronize(e1));
             float ms = 0;
             CK(cudaEventElapsedTime(&ms, e0, e1));
             const double lookups = (double)sms * NT * ITERS * kCodes;
             const double warp_lookups = lookups / 32;
-            const double wf = warp_lookups * E + (k == 1 ? (double)sms * NT * ITERS * (kCodes / 8) * 16 / 128 : 0.0);
+            const double wf = warp_lookups * E + (k >= 1 ? (double)sms * NT * ITERS * (kCodes / 8) * 16 / 128 : 0.0);
             const double per_sm_clk = wf / sms / (ms * 1e-3) / 1e9;  // wavefronts per SM per ns
             printf("%s rep %d: %.3f ms, %.3f T lookups/s, E = %.3f wavefronts per warp lookup, "
                    "%.3f G wavefronts per SM per second (%.3f per clock at the %d MHz max clock)%s\n",
-                   k == 0 ? "k_lookup (random u16 lookups, no global memory)" : "k_stream (+ a 16-byte LDG per 8 lookups)",
+                   names[k],
                    rep, ms, lookups / (ms * 1e-3) / 1e12, E, per_sm_clk, per_sm_clk / (clk_khz * 1e-6), clk_khz / 1000,
-                   k == 1 ? " (stream wavefronts counted at 1 per 128 B)" : "");
+                   k >= 1 ? " (stream wavefronts counted at 1 per 128 B)" : "");
         }
     }
     return 0;
