@@ -33,7 +33,7 @@ def main():
             head.append(ns)
     total = sum(sum(v) for v in per.values())
     print(f"# ncu --metrics gpu__time_duration.sum --clock-control none -c 4000, command: python bench.py (default), "
-          f"round 1 ({tag})")
+          f"evidence tag {tag}")
     print("# per kernel: launches, total us, mean us, share of all profiled kernel time (cold-cache, serialised)")
     for name, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
         print(f"{name[:90]:90s} {len(v):6d} {sum(v) / 1e3:12.1f} {sum(v) / len(v) / 1e3:10.2f} "
