@@ -138,3 +138,25 @@ def test_zech_batch_rows_past_the_split_bound():
     x = synth.zech_codes(synth.BASE_SEED, 3, 0, n, p - 1)
     got = gfp.dot_batch(cu(A), cu(x), p, ZE).cpu().numpy().astype(np.int64)
     assert np.array_equal(got, rows_oracle(p, A, x, range(rows)))
+
+
+@pytest.mark.parametrize("block", range(4))
+def test_zech_batch_fuzz_aligned_rows(block):
+    """Random shapes whose rows are 16-byte aligned (the split-exponent kernel's path: lda a multiple of 8), random
+    primes on both sides of 65281, zero-heavy and zero-free codes; every row against the oracle."""
+    rng = np.random.default_rng(9100 + block)
+    primes = [3, 7, 257, 1009, 7919, 32749, 40009, 65267, 65269, 65287, 65293, 65519, 65521]
+    for case in range(12):
+        p = int(rng.choice(primes))
+        rows = int(rng.integers(1, 200))
+        n = int(rng.integers(8, 9000))
+        lda = (n + 7) // 8 * 8 + 8 * int(rng.integers(0, 3))
+        seed = synth.BASE_SEED + 9100 + 100 * block + case
+        A = synth.zech_codes(seed, 2, 0, rows * lda, p - 1).reshape(rows, lda)
+        x = synth.zech_codes(seed, 3, 0, n, p - 1)
+        if case % 3 == 1:
+            A[:, ::3] = 0  # many zero codes
+        elif case % 3 == 2:
+            A[A == 0] = p - 1  # none
+        got = gfp.dot_batch(cu(A)[:, :n], cu(x), p, ZE).cpu().numpy().astype(np.int64)
+        assert np.array_equal(got, rows_oracle(p, A[:, :n], x, range(rows))), (p, rows, n, lda)
