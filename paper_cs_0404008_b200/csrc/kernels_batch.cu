@@ -668,7 +668,10 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
         // split-exponent kernel (batch_zsplit_kernel): two conflict-free lookups per term; the row total
         // n (p-1)^3 must fit the u64 and x must fit below the table (absolute shared 0xFF80, less the reserved base)
         const int64_t zvpl = std::max<int64_t>((n / 8 + 31) / 32, 1);
-        if (GFP_ZSPLIT && vec && lanes == 0 && n >= 8 && rows < (int64_t(1) << 31) && lda / 8 * 2 < (int64_t(1) << 31) && (u128)n * q2 * pm1 <= max64 && 2 * (256 * zvpl + 8) <= kZsXBytes) {
+        // (row indices and the in-group row offsets r * lda / 8, r < GFP_ZS_RP, are 32-bit in the kernel)
+        const bool idx32 = rows < (int64_t(1) << 31) && lda / 8 * GFP_ZS_RP < (int64_t(1) << 31);
+        if (GFP_ZSPLIT && vec && lanes == 0 && n >= 8 && idx32 && (u128)n * q2 * pm1 <= max64 &&
+            2 * (256 * zvpl + 8) <= kZsXBytes) {
             constexpr int ZNT = GFP_ZS_NT, ZU = GFP_ZS_U, ZRP = GFP_ZS_RP;
             const bool flag = I.p > 65281;  // the zero code needs the flag page (no free H row)
             // ring depth: the largest of {ZU, 2, 1} dividing the vectors per lane and row
