@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(NT, MINB) batch_zech_kernel(const uint16_t *__
 // and a warp-wide lookup touches 32 distinct banks -- ONE shared-memory wavefront, where a random lookup into
 // the q-entry table costs ~3.4 (the most distinct words one bank is asked for).  Two conflict-free
 // lookups per term (2 wavefronts per 32 terms) against 3.37 move the L1TEX data-pipe floor of the matrix-vector
-// product from ~116 us to ~80 us at 65536 x 4096, near the HBM floor (~72 us).
+// product from ~116 us to ~75 us at 65536 x 4096, about the HBM floor (~72 us at the read ceiling).
 // Addresses are built by byte permutes: the table region sits at the absolute shared address 0x10000 (64 KB
 // aligned), so a row address is the byte pattern [lane*4 (+128), row, 0x01, 0] -- one PRMT from e and a base
 // register per lookup.  The zero code:
@@ -303,13 +303,15 @@ __global__ void __launch_bounds__(NT, 1) batch_zsplit_kernel(const uint16_t *__r
         pair(a.w, xw.w & 0xFFFFu, xw.w >> 16, acc);
     };
     const uint4 *xv = reinterpret_cast<const uint4 *>(s_x);
-    // row indices in 32 bits (the launcher checks rows < 2^31)
+    // row indices in 32 bits (the launcher checks rows < 2^30: row + 2 x gstride cannot wrap)
     const int nrows = (int)rows;
     const int warp0 = (int)blockIdx.x * (NT / 32) + (int)(threadIdx.x >> 5);
     const int gstride = (int)gridDim.x * (NT / 32) * RP;  // rows between a warp's row groups
     // A warp walks a stream of elements (row group of RP rows, vector k < vpl of each row); a ring of U elements
-    // is in flight per lane: the slot just consumed is refilled at once with the element U ahead (the same row
-    // group or, in a group's last turn, the next one), so ~U elements stay in flight while the lane computes.
+    // per lane: the slot just consumed is refilled at once with the element U ahead (the same row group or, in a
+    // group's last turn, the next one), so loads stay in flight while the lane computes across row groups.  (ptxas
+    // waits for the ring's loads as one scoreboard, so the effective prefetch distance is about one element; 64
+    // registers per thread at 1024 threads leave no room for a deeper ring: profiles/r02_zsplit_ab.txt.)
     // Loads are never predicated off: a row past the matrix re-reads the last row (its sum is never written),
     // a vector slot past the row re-reads a valid vector (its staged x is 0).
     const uint4 *A4 = reinterpret_cast<const uint4 *>(A);
@@ -669,7 +671,7 @@ gfp_status launch_batch(const gfp_info &I, const KParams &K, const void *A, int6
         // n (p-1)^3 must fit the u64 and x must fit below the table (absolute shared 0xFF80, less the reserved base)
         const int64_t zvpl = std::max<int64_t>((n / 8 + 31) / 32, 1);
         // (row indices and the in-group row offsets r * lda / 8, r < GFP_ZS_RP, are 32-bit in the kernel)
-        const bool idx32 = rows < (int64_t(1) << 31) && lda / 8 * GFP_ZS_RP < (int64_t(1) << 31);
+        const bool idx32 = rows < (int64_t(1) << 30) && lda / 8 * GFP_ZS_RP < (int64_t(1) << 31);
         if (GFP_ZSPLIT && vec && lanes == 0 && n >= 8 && idx32 && (u128)n * q2 * pm1 <= max64 &&
             2 * (256 * zvpl + 8) <= kZsXBytes) {
             constexpr int ZNT = GFP_ZS_NT, ZU = GFP_ZS_U, ZRP = GFP_ZS_RP;
