@@ -811,6 +811,9 @@ def test_non_canonical_inputs_never_fault():
     p = 32749
     a, b = synth.zech_codes(SEED, 0, 0, n, p - 1), synth.zech_codes(SEED, 1, 0, n, p - 1)
     assert int(gfp.dot(cu(a), cu(b), p, gfp.ZECH).cpu().to(torch.int64)[0]) == oracle.dot_zech(p, 2, a, b)
+    A = a[: 49 * 1000].reshape(49, 1000)  # and a canonical Zech batch (the split-exponent kernel) after them
+    got = gfp.dot_batch(cu(A), cu(b[:1000]), p, gfp.ZECH).cpu().numpy().astype(np.int64)
+    assert got.tolist() == [oracle.dot_zech(p, 2, A[r], b[:1000]) for r in range(49)]
 
 
 def test_back_to_back_dots_keep_stream_order():
