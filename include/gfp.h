@@ -199,9 +199,10 @@ gfp_status gfp_dot(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *a, const v
  * A: device, row-major with leading dimension lda >= n (elements);
  * x: device, n elements; out: device, `rows` elements of dtype `dt`.
  * Supported reps: classical (u16, u32), Montgomery (u32), fp64, Zech (u16), centered.
- * Zech rows (16-byte aligned A, x and lda): each code of A is decoded by one antilog lookup in shared memory
- * and multiplied by the decoded x (x decoded once per CTA); the row value is encoded back into a code
- * (reading G25 in DESIGN.md); unaligned rows take the index-add kernel.  One kernel launch. */
+ * Zech rows (16-byte aligned A, x and lda): each code c of A is decoded as g^c = H[(c-1) >> 8] * L[(c-1) & 255]
+ * from two 256-entry tables replicated per shared-memory bank (readings G25/G26 in DESIGN.md; n (p-1)^3 < 2^64,
+ * else one antilog lookup per code) and multiplied by the decoded x (x decoded once per CTA); the row value is
+ * encoded back into a code; unaligned rows take the index-add kernel.  One kernel launch. */
 gfp_status gfp_dot_batch(uint64_t p, gfp_rep rep, gfp_dtype dt, const void *A, int64_t lda,
                          const void *x, int64_t rows, int64_t n, void *out, void *stream);
 
